@@ -1,0 +1,667 @@
+/*
+ * oracle_scheme.c — ORACLE (test infrastructure only; see oracle.h).
+ *
+ * Grid-level algorithm of one SSP-RK3 stage, in the order of DESIGN.md §2
+ * (SURVEY.md §8(c) "Stage algorithm"):
+ *   1. ghost fill of the 8 primitives (rho, u~^i, p, B^i = U_B/sqrt(gamma)),
+ *      g = 5 deep, axis-sequential, ghost(i) = owned(((i mod n)+n) mod n) for
+ *      periodic, owned(clamp(i,0,n-1)) for outflow            [A12, A13]
+ *   2. for axis a = 1,2,3: per line, every face i+1/2, i = -3..n+1:
+ *      WENO5 of the 8 primitives (left state from cells i-2..i+2, right state
+ *      the mirror from cells i+3..i-1) [A2, A3], positivity fallback [A25],
+ *      HLL flux with the face metric [A4]; DER correction of the face fluxes
+ *      [A5]; L_q -= (H_{i+1/2} - H_{i-1/2}) / Delta_a for the 5 hydro vars;
+ *      field-CD EMF contributions Omega (or, divb=none, B flux differences) [A6]
+ *   3. L += sqrt(gamma) s  (metric sources at cell centres)
+ *   4. L(sqrt(gamma) B^i) = -D_j Omega_k + D_k Omega_j, (i,j,k) cyclic,
+ *      Omega ghosts filled with the same boundary rule      [A6]
+ *   5. RK combine in the literal SPEC.md:154 forms             [A7]
+ *   6. con2prim + floors                                       [A8, A9]
+ * Two evaluation paths share the face/cell functions bit for bit: the full
+ * grid (padded arrays) and the per-cell path (index-mapped reads) used for
+ * sampled parity at full size; a pin test checks they agree bitwise.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+#include "oracle_internal.h"
+
+#define G ORC_G
+
+static int nthreads_of(const orc_cfg* c) {
+#ifdef _OPENMP
+  return c->nthreads > 0 ? c->nthreads : omp_get_max_threads();
+#else
+  (void)c;
+  return 1;
+#endif
+}
+
+static double dx_of(const orc_cfg* c, int a) { return (c->hi[a] - c->lo[a]) / c->n[a]; }
+static double centre_of(const orc_cfg* c, int a, long long i) { return c->lo[a] + (i + 0.5) * dx_of(c, a); }
+static double face_of(const orc_cfg* c, int a, long long i) { return c->lo[a] + (i + 1) * dx_of(c, a); } /* face i+1/2 */
+
+/* ghost index rule (A12/A13) */
+static long long map_index(const orc_cfg* c, int a, long long i) {
+  long long n = c->n[a];
+  if (i < 0) {
+    if (c->bc[a][0] == ORC_BC_PERIODIC) return ((i % n) + n) % n;
+    return 0;
+  }
+  if (i >= n) {
+    if (c->bc[a][1] == ORC_BC_PERIODIC) return ((i % n) + n) % n;
+    return n - 1;
+  }
+  return i;
+}
+
+static long long ncells(const orc_cfg* c) { return (long long)c->n[0] * c->n[1] * c->n[2]; }
+static long long lin(const orc_cfg* c, long long i, long long j, long long k) {
+  return (k * c->n[1] + j) * c->n[0] + i;
+}
+
+/* ------------------------------------------------------------------ */
+/* Reconstruction and DER (A2, A5)                                     */
+/* ------------------------------------------------------------------ */
+double orc_weno5_left(const double u[5], int rec) {
+  const double eps = 1e-6;
+  double b0 = 13.0 / 12.0 * (u[0] - 2.0 * u[1] + u[2]) * (u[0] - 2.0 * u[1] + u[2])
+            + 0.25 * (u[0] - 4.0 * u[1] + 3.0 * u[2]) * (u[0] - 4.0 * u[1] + 3.0 * u[2]);
+  double b1 = 13.0 / 12.0 * (u[1] - 2.0 * u[2] + u[3]) * (u[1] - 2.0 * u[2] + u[3])
+            + 0.25 * (u[1] - u[3]) * (u[1] - u[3]);
+  double b2 = 13.0 / 12.0 * (u[2] - 2.0 * u[3] + u[4]) * (u[2] - 2.0 * u[3] + u[4])
+            + 0.25 * (3.0 * u[2] - 4.0 * u[3] + u[4]) * (3.0 * u[2] - 4.0 * u[3] + u[4]);
+  double q0, q1, q2, d0, d1, d2;
+  if (rec == 0) { /* point-value interpolation form (A2) */
+    q0 = (3.0 * u[0] - 10.0 * u[1] + 15.0 * u[2]) / 8.0;
+    q1 = (-u[1] + 6.0 * u[2] + 3.0 * u[3]) / 8.0;
+    q2 = (3.0 * u[2] + 6.0 * u[3] - u[4]) / 8.0;
+    d0 = 1.0 / 16.0;
+    d1 = 10.0 / 16.0;
+    d2 = 5.0 / 16.0;
+  } else { /* finite-volume form */
+    q0 = (2.0 * u[0] - 7.0 * u[1] + 11.0 * u[2]) / 6.0;
+    q1 = (-u[1] + 5.0 * u[2] + 2.0 * u[3]) / 6.0;
+    q2 = (2.0 * u[2] + 5.0 * u[3] - u[4]) / 6.0;
+    d0 = 1.0 / 10.0;
+    d1 = 6.0 / 10.0;
+    d2 = 3.0 / 10.0;
+  }
+  double a0 = d0 / ((eps + b0) * (eps + b0));
+  double a1 = d1 / ((eps + b1) * (eps + b1));
+  double a2 = d2 / ((eps + b2) * (eps + b2));
+  double w0 = a0 / (a0 + a1 + a2);
+  double w1 = a1 / (a0 + a1 + a2);
+  double w2 = a2 / (a0 + a1 + a2);
+  return w0 * q0 + w1 * q1 + w2 * q2;
+}
+
+double orc_der(const double F[5], int der) {
+  if (der == 6)
+    return F[2] - (F[1] - 2.0 * F[2] + F[3]) / 24.0
+         + 3.0 * (F[0] - 4.0 * F[1] + 6.0 * F[2] - 4.0 * F[3] + F[4]) / 640.0;
+  if (der == 4) return F[2] - (F[1] - 2.0 * F[2] + F[3]) / 24.0;
+  return F[2];
+}
+
+/* Face flux at face i+1/2 from the stencil st[m][v] = prims of cells i-2+m,
+ * m = 0..5, v = 0..7; xf = face coordinates; a = axis.  Shared by both paths. */
+static void face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8]) {
+  double qL[8], qR[8];
+  for (int v = 0; v < 8; v++) {
+    double l[5], r[5];
+    for (int m = 0; m < 5; m++) l[m] = st[m][v];     /* cells i-2 .. i+2 */
+    for (int m = 0; m < 5; m++) r[m] = st[5 - m][v]; /* cells i+3 .. i-1 (mirror) */
+    qL[v] = orc_weno5_left(l, c->rec);
+    qR[v] = orc_weno5_left(r, c->rec);
+  }
+  /* A25 positivity fallback: a non-positive reconstructed rho or p takes the
+   * value of the cell the state was reconstructed in */
+  if (!(qL[0] > 0.0)) qL[0] = st[2][0];
+  if (!(qL[4] > 0.0)) qL[4] = st[2][4];
+  if (!(qR[0] > 0.0)) qR[0] = st[3][0];
+  if (!(qR[4] > 0.0)) qR[4] = st[3][4];
+  orc_met m;
+  orc_met_eval(c, xf, &m);
+  orc_hll(&m, c->gamma, qL, qR, a, F);
+}
+
+/* prims (8) of an owned cell from the state arrays */
+static void owned_prim(const orc_cfg* c, const double* U8, const double* P5, long long i, long long j,
+                       long long k, double out[8]) {
+  long long N = ncells(c), id = lin(c, i, j, k);
+  double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+  orc_met m;
+  orc_met_eval(c, x, &m);
+  for (int q = 0; q < 5; q++) out[q] = P5[q * N + id];
+  for (int q = 0; q < 3; q++) out[5 + q] = U8[(5 + q) * N + id] / m.sqrtg;
+}
+
+/* ------------------------------------------------------------------ */
+/* Full-grid right-hand side                                           */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  long long N[3];
+  double* a; /* [8][N2][N1][N0] */
+} padded;
+
+static double* pget(padded* p, int v, long long i, long long j, long long k) {
+  return &p->a[(((long long)v * p->N[2] + (k + G)) * p->N[1] + (j + G)) * p->N[0] + (i + G)];
+}
+
+static void ghost_fill(const orc_cfg* c, padded* P) {
+  int nt = nthreads_of(c);
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2];
+  /* axis 0 ghosts on owned (j,k) */
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = -G; i < n0 + G; i++) {
+        if (i >= 0 && i < n0) continue;
+        long long s = map_index(c, 0, i);
+        for (int v = 0; v < 8; v++) *pget(P, v, i, j, k) = *pget(P, v, s, j, k);
+      }
+  /* axis 1 ghosts on every i (including axis-0 ghosts), owned k */
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = -G; j < n1 + G; j++) {
+      if (j >= 0 && j < n1) continue;
+      long long s = map_index(c, 1, j);
+      for (long long i = -G; i < n0 + G; i++)
+        for (int v = 0; v < 8; v++) *pget(P, v, i, j, k) = *pget(P, v, i, s, k);
+    }
+  /* axis 2 ghosts everywhere */
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = -G; k < n2 + G; k++) {
+    if (k >= 0 && k < n2) continue;
+    long long s = map_index(c, 2, k);
+    for (long long j = -G; j < n1 + G; j++)
+      for (long long i = -G; i < n0 + G; i++)
+        for (int v = 0; v < 8; v++) *pget(P, v, i, j, k) = *pget(P, v, i, j, s);
+  }
+}
+
+/* Omega arrays padded by one cell per side */
+typedef struct {
+  long long N[3];
+  double* a; /* [3][n2+2][n1+2][n0+2] */
+} omega_t;
+static double* oget(omega_t* o, int v, long long i, long long j, long long k) {
+  return &o->a[(((long long)v * o->N[2] + (k + 1)) * o->N[1] + (j + 1)) * o->N[0] + (i + 1)];
+}
+
+/* accumulate the contribution of axis a at one cell: hydro rhs and Omega / B rhs.
+ * Hp, Hm = DER fluxes at faces i+1/2 and i-1/2 of the cell. */
+static void accumulate_axis(const orc_cfg* c, int a, const double Hp[8], const double Hm[8], double L[8],
+                            double Om[3]) {
+  double d = dx_of(c, a);
+  for (int q = 0; q < 5; q++) L[q] = L[q] - (Hp[q] - Hm[q]) / d;
+  int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
+  if (c->divb == 1) {
+    L[5 + b1] = L[5 + b1] - (Hp[5 + b1] - Hm[5 + b1]) / d;
+    L[5 + b2] = L[5 + b2] - (Hp[5 + b2] - Hm[5 + b2]) / d;
+  } else {
+    /* field-CD (A6): axis-a flux of B^{a+1} -> -1/4 into Omega_{a+2};
+     *                axis-a flux of B^{a+2} -> +1/4 into Omega_{a+1} */
+    Om[b2] = Om[b2] - 0.25 * (Hp[5 + b1] + Hm[5 + b1]);
+    Om[b1] = Om[b1] + 0.25 * (Hp[5 + b2] + Hm[5 + b2]);
+  }
+}
+
+static void add_sources(const orc_cfg* c, const double pr[8], const double x[3], double L[8]) {
+  orc_met m;
+  orc_metd d;
+  orc_met_eval(c, x, &m);
+  orc_met_deriv_eval(c, x, &d);
+  double s[8];
+  orc_sources(&m, &d, c->gamma, pr, s);
+  for (int q = 1; q < 5; q++) L[q] = L[q] + m.sqrtg * s[q];
+}
+
+/* L(sqrt(gamma) B^i) = -(Om_k(j+1) - Om_k(j-1))/(2 D_j) + (Om_j(k+1) - Om_j(k-1))/(2 D_k),
+ * (i,j,k) cyclic.  om(v, axis, +-1) returns Omega_v at the neighbour. */
+static void curl_from(const orc_cfg* c, const double onb[3][3][2], double L[8]) {
+  /* onb[v][axis][0:-1, 1:+1] */
+  for (int i = 0; i < 3; i++) {
+    int j = (i + 1) % 3, k = (i + 2) % 3;
+    L[5 + i] = -(onb[k][j][1] - onb[k][j][0]) / (2.0 * dx_of(c, j))
+             + (onb[j][k][1] - onb[j][k][0]) / (2.0 * dx_of(c, k));
+  }
+}
+
+int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  int nt = nthreads_of(c);
+  padded P;
+  P.N[0] = n0 + 2 * G;
+  P.N[1] = n1 + 2 * G;
+  P.N[2] = n2 + 2 * G;
+  P.a = (double*)malloc(sizeof(double) * 8 * P.N[0] * P.N[1] * P.N[2]);
+  omega_t O;
+  O.N[0] = n0 + 2;
+  O.N[1] = n1 + 2;
+  O.N[2] = n2 + 2;
+  O.a = (double*)calloc((size_t)3 * O.N[0] * O.N[1] * O.N[2], sizeof(double));
+  if (!P.a || !O.a) {
+    free(P.a);
+    free(O.a);
+    return -3;
+  }
+  /* 1. owned primitives, then ghosts */
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        double pr[8];
+        owned_prim(c, U8, P5, i, j, k, pr);
+        for (int v = 0; v < 8; v++) *pget(&P, v, i, j, k) = pr[v];
+      }
+  ghost_fill(c, &P);
+  for (long long q = 0; q < 8 * N; q++) L8[q] = 0.0;
+
+  /* 2. axis sweeps, a = 0,1,2 in this order */
+  for (int a = 0; a < 3; a++) {
+    int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
+    long long na = c->n[a], nl = (long long)c->n[t1] * c->n[t2];
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (long long line = 0; line < nl; line++) {
+      long long cell[3];
+      cell[t1] = line % c->n[t1];
+      cell[t2] = line / c->n[t1];
+      double* F = (double*)malloc(sizeof(double) * 8 * (na + 5));
+      double* H = (double*)malloc(sizeof(double) * 8 * (na + 1));
+      for (long long fi = -3; fi < na + 2; fi++) { /* face fi+1/2 */
+        double st[6][8];
+        for (int m = 0; m < 6; m++) {
+          long long cc[3] = {cell[0], cell[1], cell[2]};
+          cc[a] = fi - 2 + m;
+          for (int v = 0; v < 8; v++) st[m][v] = *pget(&P, v, cc[0], cc[1], cc[2]);
+        }
+        double xf[3];
+        xf[a] = face_of(c, a, fi);
+        xf[t1] = centre_of(c, t1, cell[t1]);
+        xf[t2] = centre_of(c, t2, cell[t2]);
+        face_flux(c, st, xf, a, &F[8 * (fi + 3)]);
+      }
+      for (long long hi = -1; hi < na; hi++) { /* DER flux at face hi+1/2 */
+        for (int q = 0; q < 8; q++) {
+          double f5[5];
+          for (int m = 0; m < 5; m++) f5[m] = F[8 * (hi - 2 + m + 3) + q];
+          H[8 * (hi + 1) + q] = orc_der(f5, c->der);
+        }
+      }
+      for (long long i = 0; i < na; i++) {
+        long long cc[3] = {cell[0], cell[1], cell[2]};
+        cc[a] = i;
+        long long id = lin(c, cc[0], cc[1], cc[2]);
+        double L[8], Om[3];
+        for (int q = 0; q < 8; q++) L[q] = L8[q * N + id];
+        for (int q = 0; q < 3; q++) Om[q] = *oget(&O, q, cc[0], cc[1], cc[2]);
+        accumulate_axis(c, a, &H[8 * (i + 1)], &H[8 * i], L, Om);
+        for (int q = 0; q < 8; q++) L8[q * N + id] = L[q];
+        for (int q = 0; q < 3; q++) *oget(&O, q, cc[0], cc[1], cc[2]) = Om[q];
+      }
+      free(F);
+      free(H);
+    }
+  }
+
+  /* 3. metric sources at cell centres */
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        long long id = lin(c, i, j, k);
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        double pr[8], L[8];
+        for (int v = 0; v < 8; v++) pr[v] = *pget(&P, v, i, j, k);
+        for (int q = 0; q < 8; q++) L[q] = L8[q * N + id];
+        add_sources(c, pr, x, L);
+        for (int q = 0; q < 8; q++) L8[q * N + id] = L[q];
+      }
+
+  /* 4. field-CD curl with Omega ghosts filled by the same rule */
+  if (c->divb == 0) {
+    for (long long k = -1; k <= n2; k++)
+      for (long long j = -1; j <= n1; j++)
+        for (long long i = -1; i <= n0; i++) {
+          if (i >= 0 && i < n0 && j >= 0 && j < n1 && k >= 0 && k < n2) continue;
+          long long si = map_index(c, 0, i), sj = map_index(c, 1, j), sk = map_index(c, 2, k);
+          for (int v = 0; v < 3; v++) *oget(&O, v, i, j, k) = *oget(&O, v, si, sj, sk);
+        }
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (long long k = 0; k < n2; k++)
+      for (long long j = 0; j < n1; j++)
+        for (long long i = 0; i < n0; i++) {
+          long long id = lin(c, i, j, k);
+          double onb[3][3][2];
+          for (int v = 0; v < 3; v++) {
+            onb[v][0][0] = *oget(&O, v, i - 1, j, k);
+            onb[v][0][1] = *oget(&O, v, i + 1, j, k);
+            onb[v][1][0] = *oget(&O, v, i, j - 1, k);
+            onb[v][1][1] = *oget(&O, v, i, j + 1, k);
+            onb[v][2][0] = *oget(&O, v, i, j, k - 1);
+            onb[v][2][1] = *oget(&O, v, i, j, k + 1);
+          }
+          double L[8];
+          for (int q = 0; q < 8; q++) L[q] = L8[q * N + id];
+          curl_from(c, onb, L);
+          for (int q = 0; q < 8; q++) L8[q * N + id] = L[q];
+        }
+  }
+  free(P.a);
+  free(O.a);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Per-cell path (index-mapped reads), for sampled parity at full size */
+/* ------------------------------------------------------------------ */
+static void prim_at(const orc_cfg* c, const double* U8, const double* P5, long long i, long long j, long long k,
+                    double out[8]) {
+  owned_prim(c, U8, P5, map_index(c, 0, i), map_index(c, 1, j), map_index(c, 2, k), out);
+}
+
+/* DER flux at face (cell[a])+1/2 of the line through cell */
+static void hhat_at(const orc_cfg* c, const double* U8, const double* P5, int a, const long long cell[3],
+                    double H[8]) {
+  int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
+  double F[5][8];
+  for (int f = 0; f < 5; f++) {
+    long long fi = cell[a] - 2 + f;
+    double st[6][8];
+    for (int m = 0; m < 6; m++) {
+      long long cc[3] = {cell[0], cell[1], cell[2]};
+      cc[a] = fi - 2 + m;
+      prim_at(c, U8, P5, cc[0], cc[1], cc[2], st[m]);
+    }
+    double xf[3];
+    xf[a] = face_of(c, a, fi);
+    xf[t1] = centre_of(c, t1, cell[t1]);
+    xf[t2] = centre_of(c, t2, cell[t2]);
+    face_flux(c, st, xf, a, F[f]);
+  }
+  for (int q = 0; q < 8; q++) {
+    double f5[5];
+    for (int m = 0; m < 5; m++) f5[m] = F[m][q];
+    H[q] = orc_der(f5, c->der);
+  }
+}
+
+/* hydro/divb-none rhs and Omega of an owned cell, sweeps in axis order */
+static void axes_at(const orc_cfg* c, const double* U8, const double* P5, const long long cell[3], double L[8],
+                    double Om[3]) {
+  for (int q = 0; q < 8; q++) L[q] = 0.0;
+  for (int q = 0; q < 3; q++) Om[q] = 0.0;
+  for (int a = 0; a < 3; a++) {
+    double Hp[8], Hm[8];
+    long long cm[3] = {cell[0], cell[1], cell[2]};
+    cm[a] -= 1;
+    hhat_at(c, U8, P5, a, cell, Hp);
+    hhat_at(c, U8, P5, a, cm, Hm);
+    accumulate_axis(c, a, Hp, Hm, L, Om);
+  }
+}
+
+static void rhs_cell(const orc_cfg* c, const double* U8, const double* P5, const long long cell[3], double L[8]) {
+  double Om[3];
+  axes_at(c, U8, P5, cell, L, Om);
+  double pr[8];
+  owned_prim(c, U8, P5, cell[0], cell[1], cell[2], pr);
+  double x[3] = {centre_of(c, 0, cell[0]), centre_of(c, 1, cell[1]), centre_of(c, 2, cell[2])};
+  add_sources(c, pr, x, L);
+  if (c->divb == 0) {
+    double onb[3][3][2];
+    for (int ax = 0; ax < 3; ax++)
+      for (int s = 0; s < 2; s++) {
+        long long nb[3] = {cell[0], cell[1], cell[2]};
+        nb[ax] += s ? 1 : -1;
+        for (int b = 0; b < 3; b++) nb[b] = map_index(c, b, nb[b]);
+        double Ld[8], Omn[3];
+        axes_at(c, U8, P5, nb, Ld, Omn);
+        for (int v = 0; v < 3; v++) onb[v][ax][s] = Omn[v];
+      }
+    curl_from(c, onb, L);
+  }
+}
+
+int orc_rhs_cells(const orc_cfg* c, const double* U8, const double* P5, long long ncell, const long long* idx,
+                  double* out) {
+  int nt = nthreads_of(c);
+#pragma omp parallel for num_threads(nt) schedule(dynamic)
+  for (long long m = 0; m < ncell; m++) rhs_cell(c, U8, P5, &idx[3 * m], &out[8 * m]);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* RK stage (A7) + con2prim/floors (A8, A9)                            */
+/* ------------------------------------------------------------------ */
+static void combine(int s, double dt, const double Un[8], const double Us[8], const double L[8], double Uo[8]) {
+  for (int q = 0; q < 8; q++) {
+    if (s == 1)
+      Uo[q] = Un[q] + dt * L[q];
+    else if (s == 2)
+      Uo[q] = 0.75 * Un[q] + 0.25 * (Us[q] + dt * L[q]);
+    else
+      Uo[q] = (1.0 / 3.0) * Un[q] + (2.0 / 3.0) * (Us[q] + dt * L[q]);
+  }
+}
+
+static void update_cell(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
+                        long long i, long long j, long long k, const double L[8], double Uo[8], double Po[5],
+                        long long* nfl, long long* nfa) {
+  long long N = ncells(c), id = lin(c, i, j, k);
+  double un[8], us[8], pp[5];
+  for (int q = 0; q < 8; q++) {
+    un[q] = Un[q * N + id];
+    us[q] = Us[q * N + id];
+  }
+  for (int q = 0; q < 5; q++) pp[q] = Ps[q * N + id];
+  combine(s, dt, un, us, L, Uo);
+  double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+  orc_met m;
+  orc_met_eval(c, x, &m);
+  orc_c2p_floors(c, &m, Uo, pp, Po, nfl, nfa);
+}
+
+int orc_stage(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
+              double* Uout, double* Pout, orc_counts* cnt) {
+  long long N = ncells(c);
+  double* L8 = (double*)malloc(sizeof(double) * 8 * N);
+  if (!L8) return -3;
+  int rc = orc_rhs(c, Us, Ps, L8);
+  if (rc) {
+    free(L8);
+    return rc;
+  }
+  long long nfl = 0, nfa = 0;
+  int nt = nthreads_of(c);
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2];
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(+ : nfl, nfa)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        long long id = lin(c, i, j, k);
+        double L[8], Uo[8], Po[5];
+        for (int q = 0; q < 8; q++) L[q] = L8[q * N + id];
+        update_cell(c, s, dt, Un, Us, Ps, i, j, k, L, Uo, Po, &nfl, &nfa);
+        for (int q = 0; q < 8; q++) Uout[q * N + id] = Uo[q];
+        for (int q = 0; q < 5; q++) Pout[q * N + id] = Po[q];
+      }
+  free(L8);
+  if (cnt) {
+    cnt->floor_events += nfl;
+    cnt->c2p_failures += nfa;
+  }
+  return 0;
+}
+
+int orc_stage_cells(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
+                    long long ncell, const long long* idx, double* Uout, double* Pout, orc_counts* cnt) {
+  long long nfl = 0, nfa = 0;
+  int nt = nthreads_of(c);
+#pragma omp parallel for num_threads(nt) schedule(dynamic) reduction(+ : nfl, nfa)
+  for (long long m = 0; m < ncell; m++) {
+    double L[8];
+    rhs_cell(c, Us, Ps, &idx[3 * m], L);
+    update_cell(c, s, dt, Un, Us, Ps, idx[3 * m], idx[3 * m + 1], idx[3 * m + 2], L, &Uout[8 * m],
+                &Pout[5 * m], &nfl, &nfa);
+  }
+  if (cnt) {
+    cnt->floor_events += nfl;
+    cnt->c2p_failures += nfa;
+  }
+  return 0;
+}
+
+int orc_step(const orc_cfg* c, double dt, double* U8, double* P5, orc_counts* cnt) {
+  long long N = ncells(c);
+  double* U1 = (double*)malloc(sizeof(double) * 8 * N);
+  double* P1 = (double*)malloc(sizeof(double) * 5 * N);
+  double* U2 = (double*)malloc(sizeof(double) * 8 * N);
+  double* P2 = (double*)malloc(sizeof(double) * 5 * N);
+  if (!U1 || !P1 || !U2 || !P2) {
+    free(U1);
+    free(P1);
+    free(U2);
+    free(P2);
+    return -3;
+  }
+  int rc = orc_stage(c, 1, dt, U8, U8, P5, U1, P1, cnt);
+  if (!rc) rc = orc_stage(c, 2, dt, U8, U1, P1, U2, P2, cnt);
+  if (!rc) rc = orc_stage(c, 3, dt, U8, U2, P2, U8, P5, cnt);
+  free(U1);
+  free(P1);
+  free(U2);
+  free(P2);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* CFL (SPEC.md:163 form, A11), con2prim, div B, set/get               */
+/* ------------------------------------------------------------------ */
+int orc_max_dt(const orc_cfg* c, const double* U8, const double* P5, double cfl, double* dt) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2];
+  int nt = nthreads_of(c);
+  double mx = 0.0;
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(max : mx)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        double pr[8];
+        owned_prim(c, U8, P5, i, j, k, pr);
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        orc_met m;
+        orc_met_eval(c, x, &m);
+        double sum = 0.0;
+        for (int a = 0; a < 3; a++) {
+          double lm, lp;
+          orc_speeds(&m, c->gamma, pr, a, &lm, &lp);
+          sum += fmax(fabs(lp), fabs(lm)) / dx_of(c, a);
+        }
+        if (sum > mx) mx = sum;
+      }
+  if (!(mx > 0.0)) return -1;
+  *dt = cfl / mx;
+  return 0;
+}
+
+int orc_con2prim(const orc_cfg* c, double* U8, double* P5, orc_counts* cnt) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  int nt = nthreads_of(c);
+  long long nfl = 0, nfa = 0;
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(+ : nfl, nfa)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        long long id = lin(c, i, j, k);
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        orc_met m;
+        orc_met_eval(c, x, &m);
+        double Uc[8], pp[5], po[5];
+        for (int q = 0; q < 8; q++) Uc[q] = U8[q * N + id];
+        for (int q = 0; q < 5; q++) pp[q] = P5[q * N + id];
+        orc_c2p_floors(c, &m, Uc, pp, po, &nfl, &nfa);
+        for (int q = 0; q < 8; q++) U8[q * N + id] = Uc[q];
+        for (int q = 0; q < 5; q++) P5[q * N + id] = po[q];
+      }
+  if (cnt) {
+    cnt->floor_events += nfl;
+    cnt->c2p_failures += nfa;
+  }
+  return 0;
+}
+
+double orc_divb(const orc_cfg* c, const double* U8) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  double mx = 0.0;
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        long long ci[3] = {i, j, k};
+        double div = 0.0;
+        for (int a = 0; a < 3; a++) {
+          long long p[3] = {i, j, k}, m[3] = {i, j, k};
+          p[a] = map_index(c, a, ci[a] + 1);
+          m[a] = map_index(c, a, ci[a] - 1);
+          div += (U8[(5 + a) * N + lin(c, p[0], p[1], p[2])] - U8[(5 + a) * N + lin(c, m[0], m[1], m[2])])
+               / (2.0 * dx_of(c, a));
+        }
+        if (fabs(div) > mx) mx = fabs(div);
+      }
+  return mx;
+}
+
+int orc_set_prims(const orc_cfg* c, const double* P8, double* U8, double* P5, long long* bad) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        long long id = lin(c, i, j, k);
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        orc_met m;
+        orc_met_eval(c, x, &m);
+        double v[3] = {P8[1 * N + id], P8[2 * N + id], P8[3 * N + id]};
+        double v2 = 0.0;
+        for (int a = 0; a < 3; a++)
+          for (int b = 0; b < 3; b++) v2 += m.g[a][b] * v[a] * v[b];
+        double rho = P8[0 * N + id], p = P8[4 * N + id];
+        if (!(rho > 0.0) || !(p > 0.0) || !(v2 < 1.0)) {
+          if (bad) *bad = id;
+          return -5;
+        }
+        double W = 1.0 / sqrt(1.0 - v2);
+        double pr[8] = {rho, W * v[0], W * v[1], W * v[2], p, P8[5 * N + id], P8[6 * N + id], P8[7 * N + id]};
+        double u[8];
+        orc_p2c(&m, c->gamma, pr, u);
+        for (int q = 0; q < 8; q++) U8[q * N + id] = m.sqrtg * u[q];
+        for (int q = 0; q < 5; q++) P5[q * N + id] = pr[q];
+      }
+  return 0;
+}
+
+int orc_get_prims(const orc_cfg* c, const double* U8, const double* P5, double* P8) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        long long id = lin(c, i, j, k);
+        double pr[8];
+        owned_prim(c, U8, P5, i, j, k, pr);
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        orc_met m;
+        orc_met_eval(c, x, &m);
+        double u2 = 0.0;
+        for (int a = 0; a < 3; a++)
+          for (int b = 0; b < 3; b++) u2 += m.g[a][b] * pr[1 + a] * pr[1 + b];
+        double W = sqrt(1.0 + u2);
+        P8[0 * N + id] = pr[0];
+        for (int a = 0; a < 3; a++) P8[(1 + a) * N + id] = pr[1 + a] / W;
+        P8[4 * N + id] = pr[4];
+        for (int a = 0; a < 3; a++) P8[(5 + a) * N + id] = pr[5 + a];
+      }
+  return 0;
+}

@@ -1,0 +1,314 @@
+"""Brute-force per-cell L(U) in mpmath (50 digits) — pin P6 for the oracle.
+
+An independent transcription of DESIGN.md §3 (readings A1-A6, A12, A13, A25)
+for tiny grids (4^3), written without looking at oracle/*.c structure:
+every face flux is evaluated from the definition at 50 digits, metric
+derivatives come from mpmath numerical differentiation (not from the oracle's
+hand-derived formulas), and the 3x3 inverse / determinant from mpmath
+matrices.  Used only by tests/test_oracle_bruteforce.py.
+"""
+from __future__ import annotations
+
+import mpmath as mp
+
+mp.mp.dps = 50
+
+
+class Grid:
+    def __init__(self, n, lo, hi, bc, metric=0, M=1, a=0, gamma=mp.mpf(4) / 3, rec=0, der=6, divb=0):
+        self.n = list(n)
+        self.lo = [mp.mpf(v) for v in lo]
+        self.hi = [mp.mpf(v) for v in hi]
+        self.bc = bc
+        self.metric = metric
+        self.M = mp.mpf(M)
+        self.a = mp.mpf(a)
+        self.gamma = mp.mpf(gamma)
+        self.rec = rec
+        self.der = der
+        self.divb = divb
+
+    def d(self, a):
+        return (self.hi[a] - self.lo[a]) / self.n[a]
+
+    def centre(self, a, i):
+        return self.lo[a] + (i + mp.mpf(1) / 2) * self.d(a)
+
+    def face(self, a, i):  # face i+1/2
+        return self.lo[a] + (i + 1) * self.d(a)
+
+    def wrap(self, a, i):
+        n = self.n[a]
+        if i < 0:
+            return i % n if self.bc[a][0] == 0 else 0
+        if i >= n:
+            return i % n if self.bc[a][1] == 0 else n - 1
+        return i
+
+
+# ------------------------------------------------------------- metric
+def _gamma_ij(G: Grid, x):
+    if G.metric == 0:
+        return mp.eye(3)
+    r = mp.e ** x[0]
+    th = x[1]
+    s, c = mp.sin(th), mp.cos(th)
+    rho2 = r ** 2 + G.a ** 2 * c ** 2
+    z = 2 * G.M * r / rho2
+    g = mp.matrix(3, 3)
+    g[0, 0] = r ** 2 * (1 + z)
+    g[0, 2] = g[2, 0] = r * (-G.a * (1 + z) * s ** 2)
+    g[1, 1] = rho2
+    g[2, 2] = s ** 2 * (rho2 + G.a ** 2 * (1 + z) * s ** 2)
+    return g
+
+
+def _alpha(G: Grid, x):
+    if G.metric == 0:
+        return mp.mpf(1)
+    r = mp.e ** x[0]
+    z = 2 * G.M * r / (r ** 2 + G.a ** 2 * mp.cos(x[1]) ** 2)
+    return 1 / mp.sqrt(1 + z)
+
+
+def _beta(G: Grid, x):
+    if G.metric == 0:
+        return [mp.mpf(0)] * 3
+    r = mp.e ** x[0]
+    z = 2 * G.M * r / (r ** 2 + G.a ** 2 * mp.cos(x[1]) ** 2)
+    return [z / (1 + z) / r, mp.mpf(0), mp.mpf(0)]
+
+
+class Met:
+    def __init__(self, G: Grid, x, derivs=False):
+        self.alpha = _alpha(G, x)
+        self.beta = _beta(G, x)
+        self.g = _gamma_ij(G, x)
+        self.gi = self.g ** -1
+        self.sqrtg = mp.sqrt(mp.det(self.g))
+        if derivs:
+            self.dalpha, self.dbeta, self.dg = [], [], []
+            for k in range(3):
+                def along(f, k=k):
+                    return mp.diff(lambda t: f([x[m] if m != k else t for m in range(3)]), x[k])
+                if G.metric == 0 or k == 2:
+                    self.dalpha.append(mp.mpf(0))
+                    self.dbeta.append([mp.mpf(0)] * 3)
+                    self.dg.append(mp.zeros(3, 3))
+                    continue
+                self.dalpha.append(along(lambda y: _alpha(G, y)))
+                self.dbeta.append([along(lambda y, i=i: _beta(G, y)[i]) for i in range(3)])
+                dg = mp.zeros(3, 3)
+                for i in range(3):
+                    for j in range(3):
+                        dg[i, j] = along(lambda y, i=i, j=j: _gamma_ij(G, y)[i, j])
+                self.dg.append(dg)
+
+
+# ------------------------------------------------------------- physics
+def aux(m: Met, gam, pr):
+    rho, ut, p, B = pr[0], pr[1:4], pr[4], pr[5:8]
+    W = mp.sqrt(1 + sum(m.g[i, j] * ut[i] * ut[j] for i in range(3) for j in range(3)))
+    v = [ut[i] / W for i in range(3)]
+    vl = [sum(m.g[i, j] * v[j] for j in range(3)) for i in range(3)]
+    Bl = [sum(m.g[i, j] * B[j] for j in range(3)) for i in range(3)]
+    v2 = sum(vl[i] * v[i] for i in range(3))
+    B2 = sum(Bl[i] * B[i] for i in range(3))
+    vB = sum(vl[i] * B[i] for i in range(3))
+    h = 1 + gam / (gam - 1) * p / rho
+    Z = rho * h * W ** 2
+    D = rho * W
+    S = [(Z + B2) * vl[i] - vB * Bl[i] for i in range(3)]
+    Su = [sum(m.gi[i, j] * S[j] for j in range(3)) for i in range(3)]
+    E2 = B2 * v2 - vB ** 2
+    U = Z - p + (E2 + B2) / 2
+    # E^i = -eps^{ijk} v_j B_k with eps^{ijk} = [ijk]/sqrt(gamma)
+    E = [-(vl[(i + 1) % 3] * Bl[(i + 2) % 3] - vl[(i + 2) % 3] * Bl[(i + 1) % 3]) / m.sqrtg for i in range(3)]
+    Wst = [[Z * v[i] * v[j] - E[i] * E[j] - B[i] * B[j] + (p + (E2 + B2) / 2) * m.gi[i, j] for j in range(3)]
+           for i in range(3)]
+    return dict(W=W, v=v, vl=vl, v2=v2, B2=B2, vB=vB, h=h, Z=Z, D=D, S=S, Su=Su, U=U, tau=U - D, Wst=Wst)
+
+
+def cons(m, gam, pr):
+    q = aux(m, gam, pr)
+    return [q["D"], *q["S"], q["tau"], *pr[5:8]]
+
+
+def flux(m, gam, pr, j):
+    q = aux(m, gam, pr)
+    B = pr[5:8]
+    a = m.alpha
+    f = [(a * q["v"][j] - m.beta[j]) * q["D"]]
+    for i in range(3):
+        f.append(a * sum(q["Wst"][j][k] * m.g[k, i] for k in range(3)) - m.beta[j] * q["S"][i])
+    f.append(a * (q["Su"][j] - q["D"] * q["v"][j]) - m.beta[j] * q["tau"])
+    for i in range(3):
+        f.append((a * q["v"][j] - m.beta[j]) * B[i] - (a * q["v"][i] - m.beta[i]) * B[j])
+    return f
+
+
+def speeds(m, gam, pr, j):
+    q = aux(m, gam, pr)
+    rho, p = pr[0], pr[4]
+    cs2 = gam * p / (rho * q["h"])
+    b2 = q["B2"] / q["W"] ** 2 + q["vB"] ** 2
+    ca2 = b2 / (rho * q["h"] + b2)
+    a2 = cs2 + ca2 - cs2 * ca2
+    disc = a2 * (1 - q["v2"]) * (m.gi[j, j] * (1 - q["v2"] * a2) - q["v"][j] ** 2 * (1 - a2))
+    sq = mp.sqrt(max(disc, 0))
+    den = 1 - q["v2"] * a2
+    return (m.alpha * (q["v"][j] * (1 - a2) - sq) / den - m.beta[j],
+            m.alpha * (q["v"][j] * (1 - a2) + sq) / den - m.beta[j])
+
+
+def hll(m, gam, pl, pr, j):
+    uL, uR = cons(m, gam, pl), cons(m, gam, pr)
+    fL, fR = flux(m, gam, pl, j), flux(m, gam, pr, j)
+    lmL, lpL = speeds(m, gam, pl, j)
+    lmR, lpR = speeds(m, gam, pr, j)
+    sl = min(0, lmL, lmR)
+    sr = max(0, lpL, lpR)
+    if sr - sl > 0:
+        F = [(sr * fL[q] - sl * fR[q] + sl * sr * (uR[q] - uL[q])) / (sr - sl) for q in range(8)]
+    else:
+        F = [(fL[q] + fR[q]) / 2 for q in range(8)]
+    return [m.sqrtg * v for v in F]
+
+
+def sources(m: Met, gam, pr):
+    q = aux(m, gam, pr)
+    s = [mp.mpf(0)] * 8
+    for i in range(3):
+        t1 = sum(q["Wst"][j][k] * m.dg[i][j, k] for j in range(3) for k in range(3))
+        t2 = sum(q["S"][j] * m.dbeta[i][j] for j in range(3))
+        s[1 + i] = m.alpha * t1 / 2 + t2 - q["U"] * m.dalpha[i]
+    e1 = sum(q["Wst"][i][k] * sum(m.beta[j] * m.dg[j][i, k] for j in range(3)) / 2
+             for i in range(3) for k in range(3))
+    e2 = sum(sum(m.g[i, k] * q["Wst"][k][j] for k in range(3)) * m.dbeta[j][i] for i in range(3) for j in range(3))
+    e3 = sum(q["Su"][j] * m.dalpha[j] for j in range(3))
+    s[4] = e1 + e2 - e3
+    return s
+
+
+def weno(u, rec):
+    eps = mp.mpf("1e-6")
+    b0 = mp.mpf(13) / 12 * (u[0] - 2 * u[1] + u[2]) ** 2 + (u[0] - 4 * u[1] + 3 * u[2]) ** 2 / 4
+    b1 = mp.mpf(13) / 12 * (u[1] - 2 * u[2] + u[3]) ** 2 + (u[1] - u[3]) ** 2 / 4
+    b2 = mp.mpf(13) / 12 * (u[2] - 2 * u[3] + u[4]) ** 2 + (3 * u[2] - 4 * u[3] + u[4]) ** 2 / 4
+    if rec == 0:
+        q = [(3 * u[0] - 10 * u[1] + 15 * u[2]) / 8, (-u[1] + 6 * u[2] + 3 * u[3]) / 8, (3 * u[2] + 6 * u[3] - u[4]) / 8]
+        d = [mp.mpf(1) / 16, mp.mpf(10) / 16, mp.mpf(5) / 16]
+    else:
+        q = [(2 * u[0] - 7 * u[1] + 11 * u[2]) / 6, (-u[1] + 5 * u[2] + 2 * u[3]) / 6, (2 * u[2] + 5 * u[3] - u[4]) / 6]
+        d = [mp.mpf(1) / 10, mp.mpf(6) / 10, mp.mpf(3) / 10]
+    al = [d[k] / (eps + b) ** 2 for k, b in enumerate((b0, b1, b2))]
+    return sum(al[k] * q[k] for k in range(3)) / sum(al)
+
+
+def derf(F, order):
+    if order == 6:
+        return F[2] - (F[1] - 2 * F[2] + F[3]) / 24 + 3 * (F[0] - 4 * F[1] + 6 * F[2] - 4 * F[3] + F[4]) / 640
+    if order == 4:
+        return F[2] - (F[1] - 2 * F[2] + F[3]) / 24
+    return F[2]
+
+
+# ------------------------------------------------------------- scheme
+class Scheme:
+    """L(U) on every owned cell of a tiny grid, from fp64 state arrays (converted exactly to mp)."""
+
+    def __init__(self, G: Grid, U8, P5):
+        self.G = G
+        self.U8 = U8
+        self.P5 = P5
+        self._prim = {}
+        self._face = {}
+        self._H = {}
+
+    def prim(self, i, j, k):
+        G = self.G
+        key = (G.wrap(0, i), G.wrap(1, j), G.wrap(2, k))
+        if key not in self._prim:
+            a, b, c = key
+            m = Met(G, [G.centre(0, a), G.centre(1, b), G.centre(2, c)])
+            pr = [mp.mpf(float(self.P5[q, c, b, a])) for q in range(5)]
+            pr += [mp.mpf(float(self.U8[5 + q, c, b, a])) / m.sqrtg for q in range(3)]
+            self._prim[key] = pr
+        return self._prim[key]
+
+    def face_flux(self, ax, cell):  # face cell[ax]+1/2, cell transverse owned
+        key = (ax, tuple(cell))
+        if key in self._face:
+            return self._face[key]
+        G = self.G
+        st = []
+        for mm in range(6):
+            cc = list(cell)
+            cc[ax] = cell[ax] - 2 + mm
+            st.append(self.prim(*cc))
+        qL = [weno([st[mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        qR = [weno([st[5 - mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        if not qL[0] > 0:
+            qL[0] = st[2][0]
+        if not qL[4] > 0:
+            qL[4] = st[2][4]
+        if not qR[0] > 0:
+            qR[0] = st[3][0]
+        if not qR[4] > 0:
+            qR[4] = st[3][4]
+        x = [G.centre(b, cell[b]) for b in range(3)]
+        x[ax] = G.face(ax, cell[ax])
+        F = hll(Met(G, x), G.gamma, qL, qR, ax)
+        self._face[key] = F
+        return F
+
+    def H(self, ax, cell):
+        key = (ax, tuple(cell))
+        if key not in self._H:
+            Fs = []
+            for mm in range(5):
+                cc = list(cell)
+                cc[ax] = cell[ax] - 2 + mm
+                Fs.append(self.face_flux(ax, cc))
+            self._H[key] = [derf([Fs[mm][q] for mm in range(5)], self.G.der) for q in range(8)]
+        return self._H[key]
+
+    def axes(self, cell):
+        G = self.G
+        L = [mp.mpf(0)] * 8
+        Om = [mp.mpf(0)] * 3
+        for ax in range(3):
+            cm = list(cell)
+            cm[ax] -= 1
+            Hp, Hm = self.H(ax, cell), self.H(ax, cm)
+            d = G.d(ax)
+            for q in range(5):
+                L[q] -= (Hp[q] - Hm[q]) / d
+            b1, b2 = (ax + 1) % 3, (ax + 2) % 3
+            if G.divb == 1:
+                L[5 + b1] -= (Hp[5 + b1] - Hm[5 + b1]) / d
+                L[5 + b2] -= (Hp[5 + b2] - Hm[5 + b2]) / d
+            else:
+                Om[b2] -= (Hp[5 + b1] + Hm[5 + b1]) / 4
+                Om[b1] += (Hp[5 + b2] + Hm[5 + b2]) / 4
+        return L, Om
+
+    def rhs_cell(self, cell):
+        G = self.G
+        L, _ = self.axes(cell)
+        x = [G.centre(b, cell[b]) for b in range(3)]
+        if G.metric != 0:
+            m = Met(G, x, derivs=True)
+            s = sources(m, G.gamma, self.prim(*cell))
+            for q in range(1, 5):
+                L[q] += m.sqrtg * s[q]
+        if G.divb == 0:
+            def om(ax, sgn, v):
+                nb = list(cell)
+                nb[ax] += sgn
+                nb = [G.wrap(b, nb[b]) for b in range(3)]
+                return self.axes(nb)[1][v]
+            for i in range(3):
+                j, k = (i + 1) % 3, (i + 2) % 3
+                L[5 + i] = -(om(j, 1, k) - om(j, -1, k)) / (2 * G.d(j)) + (om(k, 1, j) - om(k, -1, j)) / (2 * G.d(k))
+        return L

@@ -1,0 +1,356 @@
+"""Pins of the oracle's point-wise pieces against values and identities the
+mathematics fixes.
+CPU only."""
+import math
+
+import numpy as np
+import pytest
+
+import echo_inputs as I
+
+X0 = [0.5, 0.5, 0.5]
+
+
+def mk(orc, **kw):
+    return orc.Cfg(**kw)
+
+
+def prim(rho, v, p, B):
+    """prims (rho, u~, p, B) from a Minkowski 3-velocity v."""
+    v = np.asarray(v, float)
+    W = 1.0 / math.sqrt(1.0 - v @ v)
+    return [rho, *(W * v), p, *B]
+
+
+# ------------------------------------------------------------------ WENO5
+def test_weno5_worked_values(orc):
+    for rec in (0, 1):
+        for c in (0.0, 1.0, -3.7, 1e5):
+            assert orc.weno5_left([c] * 5, rec) == pytest.approx(c, rel=1e-15, abs=1e-300)
+        # (1,2,3,4,5) -> 3.5 (both forms)
+        assert orc.weno5_left([1, 2, 3, 4, 5], rec) == pytest.approx(3.5, rel=1e-15)
+    # point samples of x^2 at x=-2..2: exact interface value 1/4 (point form, A2);
+    # the finite-volume candidates return 1/6
+    assert orc.weno5_left([4, 1, 0, 1, 4], 0) == pytest.approx(0.25, rel=1e-14)
+    assert orc.weno5_left([4, 1, 0, 1, 4], 1) == pytest.approx(1.0 / 6.0, rel=1e-14)
+
+
+def test_weno5_ideal_weights(orc):
+    rng = np.random.default_rng(1)
+    for _ in range(100):
+        # smooth data with beta << eps: nonlinear weights -> ideal weights d_k
+        lin = np.array([3.0, -20.0, 90.0, 60.0, -5.0]) / 128.0  # 5th-order midpoint interpolant
+        smooth = np.polyval([0.01, -0.02, 0.3, 1.0, 2.0], np.arange(-2, 3) * 1e-2)
+        assert orc.weno5_left(smooth, 0) == pytest.approx(lin @ smooth, rel=1e-9)
+
+
+def _weno_err(orc, rec, N):
+    h = 2 * math.pi / N
+    x = np.arange(N) * h
+    u = np.sin(x)
+    return max(abs(orc.weno5_left([u[(i + m) % N] for m in range(-2, 3)], rec) - math.sin(x[i] + h / 2))
+               for i in range(N))
+
+
+def test_weno5_order(orc):
+    # F3: point form is 5th order on point samples, FV form only 2nd
+    e0 = [_weno_err(orc, 0, N) for N in (32, 64, 128)]
+    e1 = [_weno_err(orc, 1, N) for N in (32, 64, 128)]
+    for a, b in zip(e0, e0[1:]):
+        assert math.log2(a / b) > 4.8
+    for a, b in zip(e1, e1[1:]):
+        assert 1.9 < math.log2(a / b) < 2.1
+
+
+# ------------------------------------------------------------------ DER
+def test_der_values(orc):
+    for o in (2, 4, 6):
+        assert orc.der([2.5] * 5, o) == 2.5
+    # App. A: F = cell average of sin over [x-h/2, x+h/2]; max |DER(F) - sin|
+    want = {2: [6.41e-3, 1.61e-3, 4.02e-4, 1.00e-4], 4: [1.11e-4, 6.95e-6, 4.35e-7, 2.72e-8],
+            6: [2.51e-6, 3.98e-8, 6.24e-10, 9.76e-12]}
+    for o, ref in want.items():
+        for N, r in zip((16, 32, 64, 128), ref):
+            h = 2 * math.pi / N
+            x = np.arange(N) * h
+            F = np.sin(x) * math.sin(h / 2) / (h / 2)
+            e = max(abs(orc.der([F[(i + m) % N] for m in range(-2, 3)], o) - math.sin(x[i])) for i in range(N))
+            assert e == pytest.approx(r, rel=6e-3)
+
+
+# ------------------------------------------------------------ prim2cons
+APP_A_P2C = [
+    # (rho, v, p, B) -> (D, S, U)  SURVEY App. A (sympy, Gamma = 4/3)
+    ((1, (0, 0, 0), 1, (0, 0, 0)), (1.0, (0, 0, 0), 4.0)),
+    ((1, (0, 0, 0), 1, (0.5, 0, 0)), (1.0, (0, 0, 0), 4.125)),
+    ((1, (0.1, 0, 0), 1, (0.5, 0, 0)), (1.00503781525921, (0.505050505050505, 0, 0), 4.17550505050505)),
+    ((0.01, (0, 0, 0), 0.001, (0.1, 0, 0)), (0.01, (0, 0, 0), 0.018)),
+    ((0.01, (0.6, 0.3, 0), 1, (0.1, 0, 0)), (0.0134839972492648, (4.374545454545455, 2.190272727272728, 0),
+                                             6.29635909090909)),
+]
+
+
+@pytest.mark.parametrize("case", APP_A_P2C)
+def test_prim2cons_worked(orc, case):
+    (rho, v, p, B), (D, S, U) = case
+    u = orc.prim2cons_pt(mk(orc), X0, prim(rho, v, p, B))
+    assert u[0] == pytest.approx(D, rel=1e-13)
+    for i in range(3):
+        assert u[1 + i] == pytest.approx(S[i], rel=1e-13, abs=1e-15)
+    assert u[4] + u[0] == pytest.approx(U, rel=1e-13)
+    assert list(u[5:]) == list(B)
+
+
+def test_prim2cons_rest_frame(orc):
+    # fluid at rest: D = rho, S = 0, tau = p/(Gamma-1) + B^2/2 (textbook)
+    rng = np.random.default_rng(2)
+    for _ in range(50):
+        rho, p = rng.uniform(0.01, 10, 2)
+        B = rng.normal(size=3)
+        u = orc.prim2cons_pt(mk(orc), X0, [rho, 0, 0, 0, p, *B])
+        assert u[0] == rho and np.all(u[1:4] == 0)
+        assert u[4] == pytest.approx(3 * p + 0.5 * B @ B, rel=1e-14)
+
+
+# ----------------------------------------------------------------- speeds
+APP_A_SPEEDS = [
+    ((1, (0, 0, 0), 1, (0, 0, 0)), (-0.516397779494322, 0.516397779494322)),
+    ((1, (0, 0, 0), 1, (0.5, 0, 0)), (-0.549169647365276, 0.549169647365276)),
+    ((1, (0.1, 0, 0), 1, (0.5, 0, 0)), (-0.475270035124538, 0.615375113933645)),
+    ((0.01, (0, 0, 0), 0.001, (0.1, 0, 0)), (-0.687184270936277, 0.687184270936277)),
+    ((0.01, (0.6, 0.3, 0), 1, (0.1, 0, 0)), (0.0763249619071452, 0.864230029959631)),
+]
+
+
+@pytest.mark.parametrize("case", APP_A_SPEEDS)
+def test_speeds_worked(orc, case):
+    (rho, v, p, B), (lm, lp) = case
+    a, b = orc.speeds_pt(mk(orc), X0, prim(rho, v, p, B), 0)
+    assert a == pytest.approx(lm, rel=1e-12)
+    assert b == pytest.approx(lp, rel=1e-12)
+
+
+def test_speeds_hydro_velocity_addition(orc):
+    # B = 0, flow along the axis: relativistic velocity addition (v +- c_s)/(1 +- v c_s)
+    rng = np.random.default_rng(3)
+    g = 4.0 / 3.0
+    for _ in range(50):
+        rho, p = rng.uniform(0.01, 10, 2)
+        v = rng.uniform(-0.95, 0.95)
+        h = 1 + g / (g - 1) * p / rho
+        cs = math.sqrt(g * p / (rho * h))
+        for d in range(3):
+            vv = [0.0, 0.0, 0.0]
+            vv[d] = v
+            lm, lp = orc.speeds_pt(mk(orc), X0, prim(rho, vv, p, [0, 0, 0]), d)
+            assert lp == pytest.approx((v + cs) / (1 + v * cs), rel=1e-12, abs=1e-14)
+            assert lm == pytest.approx((v - cs) / (1 - v * cs), rel=1e-12, abs=1e-14)
+
+
+def test_speeds_subluminal(orc):
+    rng = np.random.default_rng(4)
+    for _ in range(300):
+        v = rng.normal(size=3)
+        v *= rng.uniform(0, 0.999) / np.linalg.norm(v)
+        pr = prim(10 ** rng.uniform(-3, 1), v, 10 ** rng.uniform(-4, 1), rng.normal(size=3) * 3)
+        for d in range(3):
+            lm, lp = orc.speeds_pt(mk(orc), X0, pr, d)
+            assert -1 < lm <= lp < 1
+
+
+# ------------------------------------------------------------------ flux
+def test_flux_rest_state(orc):
+    # rest state along x -> (0, 1, 0, 0, 0, 0, 0, 0) (only pressure in x-momentum)
+    f = orc.flux_pt(mk(orc), X0, [1, 0, 0, 0, 1, 0, 0, 0], 0)
+    assert list(f) == [0, 1, 0, 0, 0, 0, 0, 0]
+
+
+def test_flux_induction_normal_zero(orc):
+    # the a-component of the induction flux is 0 for every state and axis
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        v = rng.normal(size=3)
+        v *= 0.9 / np.linalg.norm(v)
+        pr = prim(1.0, v, 1.0, rng.normal(size=3))
+        for d in range(3):
+            assert orc.flux_pt(mk(orc), X0, pr, d)[5 + d] == 0.0
+
+
+def test_flux_cp_alfven_exact(orc):
+    # the circularly polarised Alfven wave is an exact nonlinear
+    # solution, U(x - v_A t): F(U) - v_A U is the same at every phase.
+    eta = 0.1
+    va = I.cp_alfven_speed(eta)
+    assert va == pytest.approx(0.407965001183163, rel=1e-13)
+    rows = []
+    for ph in np.linspace(0, 2 * math.pi, 17):
+        B = [1.0, eta * math.cos(ph), eta * math.sin(ph)]
+        v = [0.0, -va * eta * math.cos(ph), -va * eta * math.sin(ph)]
+        pr = prim(1.0, v, 1.0, B)
+        u = orc.prim2cons_pt(mk(orc), X0, pr)
+        f = orc.flux_pt(mk(orc), X0, pr, 0)
+        rows.append(f - va * u)
+    rows = np.array(rows)
+    assert np.max(np.abs(rows - rows[0])) < 1e-14
+
+
+# ------------------------------------------------------------------- HLL
+def test_hll_special_cases(orc):
+    c = mk(orc)
+    rng = np.random.default_rng(6)
+    for _ in range(30):
+        v = rng.normal(size=3) * 0.3
+        pr = prim(rng.uniform(0.1, 2), v, rng.uniform(0.1, 2), rng.normal(size=3))
+        for d in range(3):
+            F = orc.hll_pt(c, X0, pr, pr, d)
+            f = orc.flux_pt(c, X0, pr, d)
+            assert np.allclose(F, f, rtol=4e-16 * 8, atol=1e-15)
+    # supersonic to the right: S_L >= 0 -> F = F_L ; to the left -> F = F_R
+    pl = prim(1.0, [0.99, 0, 0], 0.01, [0, 0, 0])
+    prr = prim(0.5, [0.98, 0, 0], 0.02, [0, 0, 0])
+    assert np.array_equal(orc.hll_pt(c, X0, pl, prr, 0), orc.flux_pt(c, X0, pl, 0))
+    pl2 = prim(1.0, [-0.99, 0, 0], 0.01, [0, 0, 0])
+    pr2 = prim(0.5, [-0.98, 0, 0], 0.02, [0, 0, 0])
+    assert np.array_equal(orc.hll_pt(c, X0, pl2, pr2, 0), orc.flux_pt(c, X0, pr2, 0))
+
+
+# ------------------------------------------------------------- con2prim
+def _random_state(rng):
+    W = rng.uniform(1, 10)
+    vmag = math.sqrt(1 - 1 / W ** 2)
+    d = rng.normal(size=3)
+    v = d / np.linalg.norm(d) * vmag
+    rho = 10 ** rng.uniform(-2, 1)
+    p = rho * 10 ** rng.uniform(-3, 2)
+    beta = 10 ** rng.uniform(-2, 2)
+    Bd = rng.normal(size=3)
+    B = Bd / np.linalg.norm(Bd) * math.sqrt(2 * p / beta)
+    return prim(rho, v, p, B)
+
+
+def test_con2prim_roundtrip(orc):
+    # P9: prim -> cons -> prim on 10^4 random states, 1 % guess
+    c = mk(orc, w_max=1e3)
+    rng = np.random.default_rng(7)
+    worst = 0.0
+    iters = []
+    for _ in range(10000):
+        pr = np.array(_random_state(rng))
+        u = orc.prim2cons_pt(c, X0, pr)
+        guess = pr.copy()
+        guess[0] *= 1.01
+        guess[4] *= 0.99
+        st, out, it = orc.c2p_pt(c, X0, u, guess)
+        assert st == 0
+        iters.append(it)
+        scale_u = max(1.0, np.max(np.abs(pr[1:4])))
+        worst = max(worst, abs(out[0] / pr[0] - 1), abs(out[4] / pr[4] - 1),
+                    np.max(np.abs(out[1:4] - pr[1:4])) / scale_u)
+    assert worst < 1e-11
+    assert np.percentile(iters, 50) <= 5 and max(iters) <= 30
+
+
+def test_con2prim_worked_states(orc):
+    c = mk(orc)
+    for (rho, v, p, B), _ in APP_A_P2C:
+        pr = np.array(prim(rho, v, p, B))
+        u = orc.prim2cons_pt(c, X0, pr)
+        g = pr.copy()
+        g[0] *= 1.01
+        st, out, it = orc.c2p_pt(c, X0, u, g)
+        assert st == 0 and it <= 6
+        np.testing.assert_allclose(out[:5], pr[:5], rtol=2e-15 * 8, atol=1e-15)
+
+
+# ----------------------------------------------------------------- metric
+def ks(orc, M=1.0, a=0.9):
+    return mk(orc, metric=1, M=M, a=a)
+
+
+def test_minkowski_metric(orc):
+    m = orc.metric(mk(orc), X0)
+    assert m["alpha"] == 1 and np.all(m["beta"] == 0) and np.array_equal(m["g"], np.eye(3))
+    assert m["sqrtg"] == 1
+    d = orc.metric_deriv(mk(orc), X0)
+    assert not np.any(d["dalpha"]) and not np.any(d["dbeta"]) and not np.any(d["dg"])
+
+
+@pytest.mark.parametrize("M,a", [(1.0, 0.9), (1.0, 0.0), (0.0, 0.0), (2.0, -0.5)])
+def test_ks_metric_closed_forms(orc, M, a):
+    rng = np.random.default_rng(8)
+    for _ in range(40):
+        r = rng.uniform(1.2, 60)
+        th = rng.uniform(0.1, math.pi - 0.1)
+        x = [math.log(r), th, rng.uniform(0, 2 * math.pi)]
+        m = orc.metric(ks(orc, M, a), x)
+        rho2 = r * r + a * a * math.cos(th) ** 2
+        z = 2 * M * r / rho2
+        assert m["alpha"] == pytest.approx((1 + z) ** -0.5, rel=1e-14)
+        # 4-metric identities of Kerr-Schild: g_tt = -(1-z), g_tr = z, g_tphi = -a z sin^2
+        b = m["beta"]
+        g = m["g"]
+        bl = g @ b
+        assert -m["alpha"] ** 2 + b @ bl == pytest.approx(-(1 - z), rel=1e-13, abs=1e-14)
+        assert bl[0] / r == pytest.approx(z, rel=1e-13, abs=1e-15)
+        assert bl[2] == pytest.approx(-a * z * math.sin(th) ** 2, rel=1e-12, abs=1e-15)
+        # sqrt(gamma) = r * rho_K^2 sin(theta) sqrt(1+z) (log-r Jacobian r)
+        assert m["sqrtg"] == pytest.approx(r * rho2 * math.sin(th) * math.sqrt(1 + z), rel=1e-13)
+        assert np.allclose(m["gi"] @ g, np.eye(3), atol=1e-13)
+        if M == 0 and a == 0:  # flat space in (ln r, theta, phi)
+            np.testing.assert_allclose(g, np.diag([r * r, r * r, r * r * math.sin(th) ** 2]), rtol=1e-15)
+
+
+def test_ks_metric_derivatives_vs_fd(orc):
+    c = ks(orc)
+    rng = np.random.default_rng(9)
+    for _ in range(30):
+        x = np.array([math.log(rng.uniform(1.3, 50)), rng.uniform(0.2, 2.9), rng.uniform(0, 6)])
+        d = orc.metric_deriv(c, x)
+
+        def flat(xx):
+            m = orc.metric(c, xx)
+            return np.concatenate([[m["alpha"]], m["beta"], m["g"].ravel()])
+        for k in range(3):
+            h = 1e-3
+            e = np.zeros(3)
+            e[k] = h
+            fd = (-flat(x + 2 * e) + 8 * flat(x + e) - 8 * flat(x - e) + flat(x - 2 * e)) / (12 * h)
+            an = np.concatenate([[d["dalpha"][k]], d["dbeta"][k], d["dg"][k].ravel()])
+            scale = np.maximum(1.0, np.abs(flat(x)))
+            assert np.max(np.abs(fd - an) / scale) < 1e-8
+
+
+def test_ks_dlnsqrtg_identity(orc):
+    # d_k ln sqrt(gamma) = 1/2 gamma^ij d_k gamma_ij
+    c = ks(orc)
+    for x in ([0.5, 1.0, 0.0], [2.0, 0.4, 1.0], [3.5, 2.5, 4.0]):
+        m = orc.metric(c, x)
+        d = orc.metric_deriv(c, x)
+        h = 1e-4
+        for k in range(2):
+            e = np.zeros(3)
+            e[k] = h
+            lp = math.log(orc.metric(c, np.add(x, e))["sqrtg"])
+            lm = math.log(orc.metric(c, np.subtract(x, e))["sqrtg"])
+            assert 0.5 * np.sum(m["gi"] * d["dg"][k]) == pytest.approx((lp - lm) / (2 * h), rel=1e-7)
+
+
+# ---------------------------------------------------------------- sources
+def test_sources_minkowski_zero(orc):
+    rng = np.random.default_rng(10)
+    for _ in range(20):
+        s = orc.sources_pt(mk(orc), X0, _random_state(rng))
+        assert not np.any(s)
+
+
+def test_sources_static_gas_flat_spherical(orc):
+    # M = 0: flat space in (ln r, theta, phi).  Static uniform gas, B = 0:
+    # sqrt(g) s(S_i) = p d_i sqrt(g) with sqrt(g) = r^3 sin(theta)  (closed form)
+    c = ks(orc, 0.0, 0.0)
+    for r, th, p in ((2.0, 0.7, 1.3), (10.0, 2.0, 0.2)):
+        x = [math.log(r), th, 0.3]
+        s = orc.sources_pt(c, x, [1.0, 0, 0, 0, p, 0, 0, 0])
+        sg = r ** 3 * math.sin(th)
+        assert sg * s[1] == pytest.approx(p * 3 * r ** 3 * math.sin(th), rel=1e-13)
+        assert sg * s[2] == pytest.approx(p * r ** 3 * math.cos(th), rel=1e-13)
+        assert s[3] == 0 and s[4] == 0 and s[0] == 0
