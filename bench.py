@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the ECHO-3DHPC time-step hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+
+A step = one CFL reduction (echo_max_dt) + one full SSP-RK3 step (echo_step) of
+BASELINE.json config 3 (512^3 periodic multi-mode turbulence, Gamma = 4/3,
+fp64), the configuration the metric is quoted on.  Inputs are resident in HBM
+when the timed region starts; they are ~34 GB >> 126 MB L2, so no flush is
+needed.  Prints ONE JSON line (rank 0).  Under torchrun (N > 1) every rank runs
+an independent replica ("replicas only" — the north star runs on
+one GPU with no sharding), timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import echo_inputs as I  # noqa: E402
+
+METRIC = "zone-updates/sec per RK step (fp64) at 512^3 on 1 B200; % of HBM roofline"
+UNIT = "zone-updates/s"
+BYTES_PER_ZONE_STEP = 752.0      # compulsory traffic per zone-update, DESIGN.md §7
+FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9  # SMs x FP64 lanes x 2 flop/FMA x max clock
+# algorithmic FP64 flops per cell of one sweep launch (Minkowski, DER6, WENO5 point form), DESIGN.md §7
+FLOPS_PER_CELL_SWEEP = 1129.0
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6547.2, "src_hbm": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        peaks["hbm_gbs"] = float(d.get("hbm_gbs", peaks["hbm_gbs"]))
+        peaks["src_hbm"] = "measured (MEASURED_PEAKS.json)"
+    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    peaks["fp64_flops"] = FP64_PEAK_DERIVED
+    peaks["src_fp64"] = "derived: 148 SM x 64 FP64 lanes x 2 x 1.965 GHz"
+    if os.path.exists(fp):
+        with open(fp) as f:
+            d = json.load(f)
+        if d.get("fp64_tflops"):
+            peaks["fp64_flops"] = float(d["fp64_tflops"]) * 1e12
+            peaks["src_fp64"] = "measured DFMA microbenchmark (profiles/fp64_peak.json)"
+    return peaks
+
+
+# ------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------- CPU baseline
+def cpu_baseline(steps: int = 1, n: int = 64):
+    """The oracle as it stands, on the host cores: `steps` SSP-RK3 steps (+CFL) of the
+    config-3 recipe on an n^3 periodic grid (a bounded sample of the 512^3 workload)."""
+    import oracle
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    p = I.problem(3, n=(n, n, n))
+    oc = oracle.Cfg(**p.grid_kwargs(), nthreads=cores)
+    U, P = oracle.set_prims(oc, I.initial_prims(p))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        dt = oracle.max_dt(oc, U, P, p.cfl)
+        U, P, _ = oracle.step(oc, dt, U, P)
+    t = time.perf_counter() - t0
+    zu = p.ncells * steps / t
+    return {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{steps} CFL+SSP-RK3 step(s) of the config-3 recipe (32 modes, k<=8, amp 0.1) on a {n}^3 "
+                      f"periodic grid, {t:.2f} s wall, OpenMP {cores} threads"}
+
+
+# ---------------------------------------------------- distributed glue
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reduce_max(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------- reference
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    n = args.ref_n
+    import oracle
+
+    oracle.build()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    p = I.problem(args.config, n=(n, n, n))
+    oc = oracle.Cfg(**p.grid_kwargs(), nthreads=cores)
+    U, P = oracle.set_prims(oc, I.initial_prims(p))
+    for _ in range(W):
+        dt = oracle.max_dt(oc, U, P, p.cfl)
+        U, P, _ = oracle.step(oc, dt, U, P)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        dt = oracle.max_dt(oc, U, P, p.cfl)
+        U, P, _ = oracle.step(oc, dt, U, P)
+    t = time.perf_counter() - t0
+    zu = p.ncells * K / t
+    sample = (f"each step = CFL + one SSP-RK3 step of the config-{args.config} recipe on a {n}^3 periodic grid "
+              f"(bounded sample of the 512^3 workload; zone-updates/s is per zone)")
+    out = {"impl": "reference", "metric": METRIC, "value": zu, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
+           "warmup": W, "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"cfg{args.config} recipe, {n}^3 sample", "grid": [n, n, n]},
+           "cpu_baseline": {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": zu, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1810_04597_b200 import build
+
+    build.build()
+    from paper_1810_04597_b200 import echo
+
+    K, W = args.steps, args.warmup
+    p = I.problem(args.config, n=args.n)
+    N = p.ncells
+    stream = torch.cuda.current_stream(dev)
+    g = echo.Echo(p)
+    echo.set_stream(g.ctx, stream.cuda_stream)
+    P8 = I.initial_prims(p, device=dev)
+    g.set_prims(P8)
+    for _ in range(W):
+        g.step(g.max_dt(p.cfl))
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K x (CFL + SSP-RK3 step), inputs in HBM
+    clk = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
+    clk.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = echo.launch_count(g.ctx)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    dts = []
+    for _ in range(K):
+        dt = g.max_dt(p.cfl)
+        dts.append(dt)
+        g.step(dt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = clk.stop()
+    launches = echo.launch_count(g.ctx) - l0
+    t_local = e0.elapsed_time(e1) / 1e3
+    t = reduce_max(t_local, world, dev)
+    value = world * N * K / t
+    st = g.stats()
+
+    # ---------------- per-kernel device times (same workload, CUDA events on the ctx stream)
+    echo.profile(g.ctx, True)
+    for _ in range(2):
+        g.step(g.max_dt(p.cfl))
+    prof = echo.profile_read(g.ctx)
+    echo.profile(g.ctx, False)
+    step_ms = sum(ms for ms, n in prof.values()) / 2.0
+    top = max(prof.items(), key=lambda kv: kv[1][0])
+    shares = {k: round(ms / 2.0 / step_ms, 4) for k, (ms, n) in prof.items() if n}
+
+    peaks = load_peaks()
+    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep")}
+    sw_ms = sum(v[0] for v in sweeps.values())
+    sw_n = sum(v[1] for v in sweeps.values())
+    sweep_avg_s = sw_ms / sw_n / 1e3
+    achieved = FLOPS_PER_CELL_SWEEP * N / sweep_avg_s
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    roofline = {"kernel": "sweep_x/y/z (K2, FP64-ALU bound)", "bound": "alu", "achieved": achieved / 1e12,
+                "peak": peaks["fp64_flops"] / 1e12, "unit": "TFLOP/s", "frac": achieved / peaks["fp64_flops"],
+                "traffic": traffic, "peak_source": peaks["src_fp64"],
+                "per_launch_flops": FLOPS_PER_CELL_SWEEP * N, "avg_launch_ms": sweep_avg_s * 1e3,
+                "dominant_kernel_by_time": top[0], "kernel_share_of_step": shares}
+    hbm_rate = peaks["hbm_gbs"] * 1e9 / BYTES_PER_ZONE_STEP
+    hbm = {"bytes_per_zone_step": BYTES_PER_ZONE_STEP, "achieved_gbs": value / world * BYTES_PER_ZONE_STEP / 1e9,
+           "peak_gbs": peaks["hbm_gbs"], "frac": value / world / hbm_rate, "peak_source": peaks["src_hbm"]}
+
+    # ---------------- end to end through the C-ABI with HOST buffers
+    host_in = torch.empty(P8.shape, dtype=torch.float64, pin_memory=True)
+    host_in.copy_(P8)
+    host_out = torch.empty(P8.shape, dtype=torch.float64, pin_memory=True)
+    del P8
+    torch.cuda.empty_cache()
+    hin = host_in.numpy()
+    hout = host_out.numpy()
+    barrier(world)
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    echo.set_prims(g.ctx, hin)          # H2D of the inputs (pinned) + prim2cons
+    for _ in range(K):
+        g.step(g.max_dt(p.cfl))         # each step reads its dt back (8 B D2H)
+    echo.get_prims(g.ctx, hout)         # D2H of the result
+    f1.record(stream)
+    torch.cuda.synchronize()
+    te2e = reduce_max(f0.elapsed_time(f1) / 1e3, world, dev)
+    e2e = {"value": world * N * K / te2e, "unit": UNIT,
+           "h2d_bytes_per_step": int(8 * N * 8 / K) + 0, "d2h_bytes_per_step": int(8 * N * 8 / K) + 8,
+           "what": "echo_set_prims(pinned host) + K x (echo_max_dt + echo_step) + echo_get_prims(pinned host)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(steps=args.cpu_steps, n=args.cpu_n)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
+                                   f"CFL {p.cfl}, Gamma 4/3, WENO5+HLL+DER6+field-CD, SSP-RK3",
+                       "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
+                       "step": "echo_max_dt + echo_step (3 stages x [3 sweeps + update])"},
+            "hbm_roofline": hbm, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks,
+            "counters": {"floor_events": st["floor_events"], "c2p_failures": st["c2p_failures"]},
+            "dt_first_last": [dts[0], dts[-1]],
+        }
+        print(json.dumps(out), flush=True)
+    g.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")
+    ap.add_argument("--ref-n", type=int, default=64)
+    ap.add_argument("--cpu-n", type=int, default=64)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

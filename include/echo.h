@@ -1,0 +1,171 @@
+/*
+ * echo.h — C-ABI of the B200-native ECHO-3DHPC time-step library (libecho_b200.so).
+ *
+ * The paper (arXiv 1810.04597) studies the time step of ECHO-3DHPC, "a Fortran
+ * application developed to solve the equations of magneto-hydrodynamic in
+ * General Relativity, using 3D finite-differences method and high-order
+ * reconstruction algorithms", timed per iteration on 512^3 and
+ * 1024^3 grids (Table 1).  This library evaluates exactly that
+ * step on one B200: per SSP-RK3 stage a ghost fill, per-axis WENO5
+ * reconstruction + HLL flux + DER6 flux derivative, metric sources, a field-CD
+ * divergence-preserving B update, the RK combine and a per-cell Newton
+ * con2prim with floors; plus the CFL max-speed reduction.  The formulas are
+ * DESIGN.md §2 and readings A1-A30 (the paper prints none).
+ *
+ * Conventions shared by every entry point
+ *  - Arrays are fp64, row-major [var][n3][n2][n1] (x1 fastest), owned cells
+ *    only (no ghost cells), N = n1*n2*n3 cells per variable.
+ *      user prims  P8 : rho, v^1, v^2, v^3, p, B^1, B^2, B^3   (v contravariant
+ *                       Eulerian 3-velocity, B non-densitised)       [A29]
+ *      state prims P5 : rho, u~^1, u~^2, u~^3, p with u~ = W v
+ *      conserved   U8 : sqrt(gamma) * (D, S_1, S_2, S_3, tau, B^1, B^2, B^3) [A10]
+ *  - `on_device` = 1: the pointer is device memory (e.g. torch tensor
+ *    data_ptr()); the copy is stream-ordered on the context stream and the call
+ *    returns without synchronising.  `on_device` = 0: host memory; the call
+ *    copies and synchronises before returning.
+ *  - Ownership: the context owns every device allocation (made in
+ *    echo_create, freed in echo_destroy).  Caller buffers are never retained.
+ *  - Errors: every int-returning call returns ECHO_OK (0) or a negative
+ *    echo_status; echo_last_error() then names the violated rule and, for
+ *    unphysical states, the first bad cell and its values (SPEC.md:110 idea).
+ *    Asynchronous kernel faults surface at the next synchronising call.
+ *  - Threading: one control thread per context; several
+ *    contexts may share a device.
+ *  - There is no CPU fallback: every step runs in the sm_100a kernels of this
+ *    library; a missing device is ECHO_E_CUDA at echo_create.
+ */
+#ifndef ECHO_B200_H
+#define ECHO_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct echo_ctx echo_ctx;
+
+typedef enum {
+  ECHO_OK = 0,
+  ECHO_E_ARG = -1,         /* invalid argument (rule named in echo_last_error) */
+  ECHO_E_CUDA = -2,        /* CUDA runtime error (no device, launch failure, ...) */
+  ECHO_E_OOM = -3,         /* device allocation failed */
+  ECHO_E_ORDER = -4,       /* call out of order, e.g. echo_step before echo_set_prims */
+  ECHO_E_UNPHYSICAL = -5,  /* rho <= 0, p <= 0 or v^2 >= 1 in echo_set_prims */
+  ECHO_E_NONFINITE = -6    /* all CFL speeds zero / non-finite (echo_max_dt) */
+} echo_status;
+
+typedef enum { ECHO_BC_PERIODIC = 0, ECHO_BC_OUTFLOW = 1 } echo_bc;           /* A13 */
+typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_metric_kind;
+
+/* Grid: n owned cells per axis (n >= 1; periodic n < 5 is allowed, ghosts wrap
+ * modulo n [A12]); [lo, hi) coordinate extent per axis (lo < hi).  Minkowski
+ * uses Cartesian (x, y, z); Kerr-Schild uses (ln r, theta, phi) [A14] and
+ * requires 0 < theta_lo < theta_hi < pi over the whole ghost-extended range.
+ * bc[a][0]/[1] = lower/upper boundary of axis a.
+ * rec: 0 = WENO5 point-value form (A2, default), 1 = WENO5 finite-volume form.
+ * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
+ * divb: 0 = field-CD constrained transport (A6, default), 1 = none. */
+typedef struct {
+  int n[3];
+  double lo[3], hi[3];
+  int bc[3][2];
+  int rec;
+  int der;
+  int divb;
+} echo_grid;
+
+/* Stationary background metric (A1, A14): Minkowski, or Kerr-Schild with mass M > 0 and spin |a| < M. */
+typedef struct {
+  int kind; /* echo_metric_kind */
+  double M, a;
+} echo_metric;
+
+/* Ideal-gas EOS and con2prim controls (A8, A9): gamma > 1, floors > 0,
+ * w_max > 1, c2p_max_iter >= 1, c2p_tol > 0. */
+typedef struct {
+  double gamma;
+  double rho_floor, p_floor, w_max;
+  int c2p_max_iter;
+  double c2p_tol;
+} echo_eos;
+
+/* Event counters (A9: floors are applied and counted, never silent). */
+typedef struct {
+  unsigned long long floor_events; /* cells where a floor / W_max rescale fired */
+  unsigned long long c2p_failures; /* cells where Newton failed (previous-stage fallback) */
+  unsigned long long steps;        /* completed echo_step calls */
+  unsigned long long stages;       /* completed RK stages (including those of echo_step) */
+} echo_stats_t;
+
+/* Create a context on the current CUDA device; allocates all device state
+ * (about 32 fp64 fields of N cells).  Validation: see the struct comments;
+ * violations give ECHO_E_ARG.  *out is NULL on failure. */
+int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos* eos, echo_ctx** out);
+
+/* Free every device allocation of ctx (NULL is a no-op). */
+void echo_destroy(echo_ctx* ctx);
+
+/* Launch every kernel of ctx on `cuda_stream` (a cudaStream_t; NULL = legacy default stream). */
+int echo_set_stream(echo_ctx* ctx, void* cuda_stream);
+
+/* Set the state from user prims P8 (layout above): U^n = sqrt(gamma) prim2cons(P)
+ * (DESIGN a0), P5 with u~ = v / sqrt(1 - v^2).  Rejects rho <= 0, p <= 0,
+ * v^2 >= 1 (ECHO_E_UNPHYSICAL, first bad cell named). */
+int echo_set_prims(echo_ctx* ctx, const double* p8, int on_device);
+
+/* Current user prims P8 (B = U_B / sqrt(gamma), v = u~ / W). */
+int echo_get_prims(echo_ctx* ctx, double* p8, int on_device);
+
+/* Replace U^n by u8 and recover P by con2prim + floors (guess: current P).
+ * Requires a prior echo_set_prims (ECHO_E_ORDER). */
+int echo_set_cons(echo_ctx* ctx, const double* u8, int on_device);
+
+/* Current conserved state U8 (U^n after a step; U^s inside a step). */
+int echo_get_cons(echo_ctx* ctx, double* u8, int on_device);
+
+/* Raw stage state: U^n (8 fields), U^s (8 fields, meaningful after stage 1 or 2),
+ * P5 (rho, u~^i, p).  Any pointer may be NULL.  Used by stage-level parity. */
+int echo_get_state(echo_ctx* ctx, double* un8, double* us8, double* p5, int on_device);
+
+/* L(U) of the current state (DESIGN §2 steps 1-4): 8 fields, layout of U8. */
+int echo_rhs(echo_ctx* ctx, double* l8, int on_device);
+
+/* con2prim + floors on the current conserved state (guess: current P);
+ * adds this call's counts to *delta if non-NULL (synchronises). */
+int echo_con2prim(echo_ctx* ctx, echo_stats_t* delta);
+
+/* One SSP-RK3 stage s (1, 2 or 3) with time step dt > 0 (SPEC.md:154 forms, A7):
+ * s=1: U^s = U^n + dt L(U^n); s=2: U^s = 0.75 U^n + 0.25 (U^s + dt L(U^s));
+ * s=3: U^n = (1/3) U^n + (2/3)(U^s + dt L(U^s)); each followed by con2prim.
+ * Stages must be issued in order 1, 2, 3 (ECHO_E_ORDER otherwise).  Asynchronous. */
+int echo_stage(echo_ctx* ctx, int s, double dt);
+
+/* One full SSP-RK3 step (stages 1, 2, 3) with dt > 0.  Asynchronous. */
+int echo_step(echo_ctx* ctx, double dt);
+
+/* CFL (SPEC.md:163 form, A11): *dt_out = cfl / max_cells sum_a max(|lambda+_a|, |lambda-_a|)/Delta_a.
+ * Synchronises (one 8-byte device-to-host copy).  ECHO_E_NONFINITE if the max is 0 or not finite. */
+int echo_max_dt(echo_ctx* ctx, double cfl, double* dt_out);
+
+/* Accumulated counters (synchronises). */
+int echo_stats(echo_ctx* ctx, echo_stats_t* out);
+
+/* Text of the last error of ctx ("" if none); NULL ctx gives the last echo_create error. */
+const char* echo_last_error(const echo_ctx* ctx);
+
+/* Kernel-time profiling on the context stream with CUDA events.
+ * echo_profile(ctx, 1) starts recording (and clears the totals), 0 stops.
+ * echo_profile_read(ctx, id, &ms, &launches) synchronises and returns the summed
+ * device time and launch count of kernel class id (0 <= id < echo_kernel_classes()),
+ * whose name is echo_kernel_name(id). */
+int echo_profile(echo_ctx* ctx, int enable);
+int echo_profile_read(echo_ctx* ctx, int id, double* ms, long long* launches);
+int echo_kernel_classes(void);
+const char* echo_kernel_name(int id);
+
+/* Number of kernels this context has launched so far. */
+long long echo_launch_count(const echo_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

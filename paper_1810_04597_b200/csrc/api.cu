@@ -1,0 +1,490 @@
+// api.cu — the C-ABI of include/echo.h: context, device allocations, stage
+// orchestration on one CUDA stream, CFL readback, counters, profiling.
+// Every step of the path runs in the kernels of sweep.cu / update.cu; this file
+// only allocates, validates, launches and copies.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/echo.h"
+#include "echo_dev.cuh"
+#include "echo_kernels.h"
+#include "metric_tables.h"
+
+using namespace echo;
+
+namespace {
+
+enum KernelClass {
+  kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kNumClasses
+};
+const char* kNames[kNumClasses] = {"sweep_x", "sweep_y", "sweep_z", "update_stage", "update_rhs",
+                                   "con2prim",  "max_speed", "prim2cons", "get_prims"};
+
+std::string g_create_error;
+
+}  // namespace
+
+struct echo_ctx {
+  GridP g;
+  EosP e;
+  bool ks = false;
+  MetTables mt{};
+  double* tables = nullptr;
+  double* Un = nullptr;   // 8N
+  double* Us = nullptr;   // 8N
+  double* P = nullptr;    // 5N
+  double* R = nullptr;    // 8N
+  double* Om = nullptr;   // 3N
+  double* scratch = nullptr;  // 8N, lazily for host-buffer transfers
+  unsigned long long* dcnt = nullptr;  // [0] floors [1] failures [2] max speed bits
+  long long* dbad = nullptr;
+  unsigned long long* hpin = nullptr;  // pinned readback
+  cudaStream_t st = nullptr;
+  bool have_state = false;
+  int next_stage = 1;
+  unsigned long long steps = 0, stages = 0;
+  long long launches = 0;
+  std::string err;
+  // profiling
+  bool prof = false;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  double prof_ms[kNumClasses] = {0};
+  long long prof_n[kNumClasses] = {0};
+};
+
+static int fail(echo_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_create_error = msg;
+  return code;
+}
+static int cuda_fail(echo_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, ECHO_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(call, where)                          \
+  do {                                           \
+    cudaError_t _e = (call);                     \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, where); \
+  } while (0)
+
+// launch bracket: profiling events + launch count
+template <class F>
+static cudaError_t launch(echo_ctx* c, int cls, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->prof) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c->st);
+  }
+  cudaError_t e = f();
+  c->launches++;
+  if (c->prof) {
+    cudaEventRecord(b, c->st);
+    c->recs.push_back({cls, a, b});
+  }
+  return e;
+}
+
+static const double* ucur(echo_ctx* c) { return c->next_stage == 1 ? c->Un : c->Us; }
+static double* ucur_mut(echo_ctx* c) { return c->next_stage == 1 ? c->Un : c->Us; }
+
+static int ensure_scratch(echo_ctx* c) {
+  if (c->scratch) return ECHO_OK;
+  cudaError_t e = cudaMalloc(&c->scratch, sizeof(double) * 8 * c->g.N);
+  if (e != cudaSuccess) return fail(c, ECHO_E_OOM, "echo: scratch allocation failed");
+  return ECHO_OK;
+}
+
+// sweeps x, y, z of the current stage input (P, Ucur) into R, Om
+static int run_sweeps(echo_ctx* c, const double* Ucur) {
+  for (int ax = 0; ax < 3; ax++) {
+    cudaError_t e = launch(c, kSweepX + ax, [&] {
+      return launch_sweep(ax, c->ks, c->g, c->e, c->mt, c->P, Ucur, c->R, c->Om, c->st);
+    });
+    if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
+  }
+  return ECHO_OK;
+}
+
+static int run_stage(echo_ctx* c, int s, double dt) {
+  const double* Uin = (s == 1) ? c->Un : c->Us;
+  int rc = run_sweeps(c, Uin);
+  if (rc) return rc;
+  double* Uout = (s == 3) ? c->Un : c->Us;
+  cudaError_t e = launch(c, kUpdateStage, [&] {
+    return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Om, c->Un, Uin, Uout, c->P,
+                         nullptr, c->dcnt, c->st);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
+  c->stages++;
+  c->next_stage = (s == 3) ? 1 : s + 1;
+  return ECHO_OK;
+}
+
+extern "C" {
+
+int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos* eos, echo_ctx** out) {
+  echo_ctx* c = nullptr;
+  if (out) *out = nullptr;
+  if (!grid || !metric || !eos || !out) return fail(nullptr, ECHO_E_ARG, "echo_create: NULL argument");
+  for (int a = 0; a < 3; a++) {
+    if (grid->n[a] < 1) return fail(nullptr, ECHO_E_ARG, "echo_create: n[a] >= 1 violated");
+    if (!(grid->hi[a] > grid->lo[a])) return fail(nullptr, ECHO_E_ARG, "echo_create: lo < hi violated");
+    for (int s = 0; s < 2; s++)
+      if (grid->bc[a][s] != ECHO_BC_PERIODIC && grid->bc[a][s] != ECHO_BC_OUTFLOW)
+        return fail(nullptr, ECHO_E_ARG, "echo_create: unknown boundary condition");
+    if ((grid->bc[a][0] == ECHO_BC_PERIODIC) != (grid->bc[a][1] == ECHO_BC_PERIODIC))
+      return fail(nullptr, ECHO_E_ARG, "echo_create: periodic must be set on both sides of an axis");
+  }
+  if (grid->rec != 0 && grid->rec != 1) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0 or 1");
+  if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
+  if (grid->divb != 0 && grid->divb != 1) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0 or 1");
+  if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");
+  if (!(eos->rho_floor > 0.0) || !(eos->p_floor > 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: floors > 0 violated");
+  if (!(eos->w_max > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: w_max > 1 violated");
+  if (eos->c2p_max_iter < 1 || !(eos->c2p_tol > 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: c2p controls invalid");
+  if (metric->kind != ECHO_METRIC_MINKOWSKI && metric->kind != ECHO_METRIC_KERR_SCHILD)
+    return fail(nullptr, ECHO_E_ARG, "echo_create: unknown metric kind");
+  const bool ks = metric->kind == ECHO_METRIC_KERR_SCHILD;
+  if (ks) {
+    if (!(metric->M >= 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: Kerr-Schild needs M >= 0");
+    double d2 = (grid->hi[1] - grid->lo[1]) / grid->n[1];
+    if (!(grid->lo[1] - kG * d2 > 0.0) || !(grid->hi[1] + kG * d2 < M_PI))
+      return fail(nullptr, ECHO_E_ARG, "echo_create: Kerr-Schild theta range (with 5 ghost cells) must lie in (0, pi)");
+  }
+  int dev;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return fail(nullptr, ECHO_E_CUDA, std::string("echo_create: no CUDA device: ") + cudaGetErrorString(ce));
+
+  c = new echo_ctx();
+  GridP& g = c->g;
+  g.N = 1;
+  for (int a = 0; a < 3; a++) {
+    g.n[a] = grid->n[a];
+    g.N *= grid->n[a];
+    g.lo[a] = grid->lo[a];
+    g.dx[a] = (grid->hi[a] - grid->lo[a]) / grid->n[a];
+    g.idx[a] = 1.0 / g.dx[a];
+    g.bc[a][0] = grid->bc[a][0];
+    g.bc[a][1] = grid->bc[a][1];
+  }
+  g.rec = grid->rec;
+  g.der = grid->der;
+  g.divb = grid->divb;
+  EosP& e = c->e;
+  e.gamma = eos->gamma;
+  e.gfac = eos->gamma / (eos->gamma - 1.0);
+  e.gm = (eos->gamma - 1.0) / eos->gamma;
+  e.rho_floor = eos->rho_floor;
+  e.p_floor = eos->p_floor;
+  e.w_max = eos->w_max;
+  e.v2max = 1.0 - 1.0 / (eos->w_max * eos->w_max);
+  e.maxit = eos->c2p_max_iter;
+  e.tol = eos->c2p_tol;
+  c->ks = ks;
+
+  const size_t N = (size_t)g.N;
+  auto alloc = [&](double** p, size_t nd) { return cudaMalloc(p, sizeof(double) * nd); };
+  if (alloc(&c->Un, 8 * N) != cudaSuccess || alloc(&c->Us, 8 * N) != cudaSuccess || alloc(&c->P, 5 * N) != cudaSuccess ||
+      alloc(&c->R, 8 * N) != cudaSuccess || alloc(&c->Om, 3 * N) != cudaSuccess ||
+      cudaMalloc(&c->dcnt, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->dbad, sizeof(long long)) != cudaSuccess ||
+      cudaMallocHost(&c->hpin, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    echo_destroy(c);
+    return fail(nullptr, ECHO_E_OOM, "echo_create: device allocation failed");
+  }
+  cudaMemset(c->dcnt, 0, 4 * sizeof(unsigned long long));
+  cudaMemset(c->R, 0, sizeof(double) * 8 * N);
+  cudaMemset(c->Om, 0, sizeof(double) * 3 * N);
+  if (ks) {
+    KsTables t;
+    build_ks_tables(metric->M, metric->a, g.n, g.lo, g.dx, &t);
+    size_t total = t.cen.size() + t.der.size() + t.f0.size() + t.f1.size();
+    if (alloc(&c->tables, total) != cudaSuccess) {
+      echo_destroy(c);
+      return fail(nullptr, ECHO_E_OOM, "echo_create: metric table allocation failed");
+    }
+    double* p = c->tables;
+    cudaMemcpy(p, t.cen.data(), sizeof(double) * t.cen.size(), cudaMemcpyHostToDevice);
+    c->mt.cen = p;
+    p += t.cen.size();
+    cudaMemcpy(p, t.der.data(), sizeof(double) * t.der.size(), cudaMemcpyHostToDevice);
+    c->mt.der = p;
+    p += t.der.size();
+    cudaMemcpy(p, t.f0.data(), sizeof(double) * t.f0.size(), cudaMemcpyHostToDevice);
+    c->mt.f0 = p;
+    p += t.f0.size();
+    cudaMemcpy(p, t.f1.data(), sizeof(double) * t.f1.size(), cudaMemcpyHostToDevice);
+    c->mt.f1 = p;
+    c->mt.w0 = t.w0;
+  }
+  ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    echo_destroy(c);
+    return fail(nullptr, ECHO_E_CUDA, std::string("echo_create: ") + cudaGetErrorString(ce));
+  }
+  *out = c;
+  return ECHO_OK;
+}
+
+void echo_destroy(echo_ctx* c) {
+  if (!c) return;
+  cudaFree(c->Un);
+  cudaFree(c->Us);
+  cudaFree(c->P);
+  cudaFree(c->R);
+  cudaFree(c->Om);
+  cudaFree(c->scratch);
+  cudaFree(c->dcnt);
+  cudaFree(c->dbad);
+  cudaFree(c->tables);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  delete c;
+}
+
+int echo_set_stream(echo_ctx* c, void* stream) {
+  if (!c) return ECHO_E_ARG;
+  c->st = (cudaStream_t)stream;
+  return ECHO_OK;
+}
+
+int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
+  if (!c || !p8) return c ? fail(c, ECHO_E_ARG, "echo_set_prims: NULL buffer") : ECHO_E_ARG;
+  const size_t bytes = sizeof(double) * 8 * c->g.N;
+  const double* src = p8;
+  if (!on_device) {
+    int rc = ensure_scratch(c);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->scratch, p8, bytes, cudaMemcpyHostToDevice, c->st), "echo_set_prims copy");
+    src = c->scratch;
+  }
+  const long long init = LLONG_MAX;
+  CK(cudaMemcpyAsync(c->dbad, &init, sizeof(long long), cudaMemcpyHostToDevice, c->st), "echo_set_prims");
+  cudaError_t e = launch(c, kPrim2Cons, [&] {
+    return launch_prim2cons(c->ks, c->g, c->e, c->mt, src, c->P, c->Un, c->dbad, c->st);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "prim2cons launch");
+  long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->dbad, sizeof(long long), cudaMemcpyDeviceToHost, c->st), "echo_set_prims");
+  CK(cudaStreamSynchronize(c->st), "echo_set_prims");
+  if (bad != LLONG_MAX) {
+    double v[8];
+    const double* base = on_device ? p8 : nullptr;
+    for (int q = 0; q < 8; q++) {
+      if (base) cudaMemcpy(&v[q], base + q * c->g.N + bad, sizeof(double), cudaMemcpyDeviceToHost);
+      else v[q] = p8[q * c->g.N + bad];
+    }
+    long long i = bad % c->g.n[0], j = (bad / c->g.n[0]) % c->g.n[1], k = bad / ((long long)c->g.n[0] * c->g.n[1]);
+    char buf[400];
+    snprintf(buf, sizeof buf,
+             "echo_set_prims: unphysical state (rho > 0, p > 0, v^2 < 1 violated) at cell (%lld,%lld,%lld): "
+             "rho=%.17g v=(%.17g,%.17g,%.17g) p=%.17g B=(%.17g,%.17g,%.17g)",
+             i, j, k, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+    c->have_state = false;
+    return fail(c, ECHO_E_UNPHYSICAL, buf);
+  }
+  c->have_state = true;
+  c->next_stage = 1;
+  return ECHO_OK;
+}
+
+int echo_get_prims(echo_ctx* c, double* p8, int on_device) {
+  if (!c || !p8) return c ? fail(c, ECHO_E_ARG, "echo_get_prims: NULL buffer") : ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_get_prims: no state (call echo_set_prims first)");
+  double* dst = p8;
+  if (!on_device) {
+    int rc = ensure_scratch(c);
+    if (rc) return rc;
+    dst = c->scratch;
+  }
+  cudaError_t e = launch(c, kGetPrims, [&] { return launch_get_prims(c->ks, c->g, c->mt, c->P, ucur(c), dst, c->st); });
+  if (e != cudaSuccess) return cuda_fail(c, e, "get_prims launch");
+  if (!on_device) {
+    CK(cudaMemcpyAsync(p8, c->scratch, sizeof(double) * 8 * c->g.N, cudaMemcpyDeviceToHost, c->st), "echo_get_prims");
+    CK(cudaStreamSynchronize(c->st), "echo_get_prims");
+  }
+  return ECHO_OK;
+}
+
+static int copy_field(echo_ctx* c, double* dst, const double* src, size_t nd, int on_device, const char* where) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * nd, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     c->st), where);
+  if (!on_device) CK(cudaStreamSynchronize(c->st), where);
+  return ECHO_OK;
+}
+
+int echo_get_cons(echo_ctx* c, double* u8, int on_device) {
+  if (!c || !u8) return c ? fail(c, ECHO_E_ARG, "echo_get_cons: NULL buffer") : ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_get_cons: no state");
+  return copy_field(c, u8, ucur(c), 8 * (size_t)c->g.N, on_device, "echo_get_cons");
+}
+
+int echo_get_state(echo_ctx* c, double* un8, double* us8, double* p5, int on_device) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_get_state: no state");
+  int rc = ECHO_OK;
+  if (un8 && !rc) rc = copy_field(c, un8, c->Un, 8 * (size_t)c->g.N, on_device, "echo_get_state");
+  if (us8 && !rc) rc = copy_field(c, us8, c->Us, 8 * (size_t)c->g.N, on_device, "echo_get_state");
+  if (p5 && !rc) rc = copy_field(c, p5, c->P, 5 * (size_t)c->g.N, on_device, "echo_get_state");
+  return rc;
+}
+
+int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
+  if (!c || !u8) return c ? fail(c, ECHO_E_ARG, "echo_set_cons: NULL buffer") : ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_set_cons: needs a prior echo_set_prims (con2prim guess)");
+  CK(cudaMemcpyAsync(c->Un, u8, sizeof(double) * 8 * c->g.N,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st), "echo_set_cons");
+  c->next_stage = 1;
+  return echo_con2prim(c, nullptr);
+}
+
+int echo_rhs(echo_ctx* c, double* l8, int on_device) {
+  if (!c || !l8) return c ? fail(c, ECHO_E_ARG, "echo_rhs: NULL buffer") : ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_rhs: no state");
+  double* dst = l8;
+  if (!on_device) {
+    int rc = ensure_scratch(c);
+    if (rc) return rc;
+    dst = c->scratch;
+  }
+  const double* U = ucur(c);
+  int rc = run_sweeps(c, U);
+  if (rc) return rc;
+  cudaError_t e = launch(c, kUpdateRhs, [&] {
+    return launch_update(kModeRhs, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, c->Om, U, U, nullptr, c->P, dst,
+                         c->dcnt, c->st);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "update(rhs) launch");
+  if (!on_device) return copy_field(c, l8, c->scratch, 8 * (size_t)c->g.N, 0, "echo_rhs");
+  return ECHO_OK;
+}
+
+int echo_con2prim(echo_ctx* c, echo_stats_t* delta) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_con2prim: no state");
+  unsigned long long before[2] = {0, 0}, after[2] = {0, 0};
+  if (delta) {
+    CK(cudaMemcpyAsync(c->hpin, c->dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_con2prim");
+    CK(cudaStreamSynchronize(c->st), "echo_con2prim");
+    before[0] = c->hpin[0];
+    before[1] = c->hpin[1];
+  }
+  double* U = ucur_mut(c);
+  cudaError_t e = launch(c, kC2P, [&] {
+    return launch_update(kModeC2P, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, c->Om, U, U, U, c->P, nullptr, c->dcnt,
+                         c->st);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "con2prim launch");
+  if (delta) {
+    CK(cudaMemcpyAsync(c->hpin, c->dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_con2prim");
+    CK(cudaStreamSynchronize(c->st), "echo_con2prim");
+    after[0] = c->hpin[0];
+    after[1] = c->hpin[1];
+    delta->floor_events = after[0] - before[0];
+    delta->c2p_failures = after[1] - before[1];
+    delta->steps = 0;
+    delta->stages = 0;
+  }
+  return ECHO_OK;
+}
+
+int echo_stage(echo_ctx* c, int s, double dt) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage: no state (call echo_set_prims first)");
+  if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage: s must be 1, 2 or 3");
+  if (s != c->next_stage) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage: dt > 0 violated");
+  return run_stage(c, s, dt);
+}
+
+int echo_step(echo_ctx* c, double dt) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_step: no state (call echo_set_prims first)");
+  if (c->next_stage != 1) return fail(c, ECHO_E_ORDER, "echo_step: a step is in progress (finish its stages)");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_step: dt > 0 violated");
+  for (int s = 1; s <= 3; s++) {
+    int rc = run_stage(c, s, dt);
+    if (rc) return rc;
+  }
+  c->steps++;
+  return ECHO_OK;
+}
+
+int echo_max_dt(echo_ctx* c, double cfl, double* dt_out) {
+  if (!c || !dt_out) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_max_dt: no state");
+  if (!(cfl > 0.0)) return fail(c, ECHO_E_ARG, "echo_max_dt: cfl > 0 violated");
+  CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_max_dt");
+  cudaError_t e = launch(c, kMaxSpeed, [&] {
+    return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, ucur(c), c->dcnt + 2, c->st);
+  });
+  if (e != cudaSuccess) return cuda_fail(c, e, "max_speed launch");
+  CK(cudaMemcpyAsync(c->hpin + 2, c->dcnt + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_max_dt");
+  CK(cudaStreamSynchronize(c->st), "echo_max_dt");
+  double m;
+  std::memcpy(&m, c->hpin + 2, sizeof m);
+  if (!(m > 0.0) || !std::isfinite(m))
+    return fail(c, ECHO_E_NONFINITE, "echo_max_dt: max signal speed is zero or not finite (static field, dt unbounded)");
+  *dt_out = cfl / m;
+  return ECHO_OK;
+}
+
+int echo_stats(echo_ctx* c, echo_stats_t* out) {
+  if (!c || !out) return ECHO_E_ARG;
+  CK(cudaMemcpyAsync(c->hpin, c->dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_stats");
+  CK(cudaStreamSynchronize(c->st), "echo_stats");
+  out->floor_events = c->hpin[0];
+  out->c2p_failures = c->hpin[1];
+  out->steps = c->steps;
+  out->stages = c->stages;
+  return ECHO_OK;
+}
+
+const char* echo_last_error(const echo_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+int echo_profile(echo_ctx* c, int enable) {
+  if (!c) return ECHO_E_ARG;
+  if (enable) {
+    for (int k = 0; k < kNumClasses; k++) {
+      c->prof_ms[k] = 0.0;
+      c->prof_n[k] = 0;
+    }
+  }
+  c->prof = enable != 0;
+  return ECHO_OK;
+}
+
+int echo_profile_read(echo_ctx* c, int id, double* ms, long long* n) {
+  if (!c || id < 0 || id >= kNumClasses) return ECHO_E_ARG;
+  CK(cudaStreamSynchronize(c->st), "echo_profile_read");
+  for (auto& r : c->recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+      c->prof_ms[r.cls] += t;
+      c->prof_n[r.cls] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  c->recs.clear();
+  if (ms) *ms = c->prof_ms[id];
+  if (n) *n = c->prof_n[id];
+  return ECHO_OK;
+}
+
+int echo_kernel_classes(void) { return kNumClasses; }
+const char* echo_kernel_name(int id) { return (id >= 0 && id < kNumClasses) ? kNames[id] : ""; }
+long long echo_launch_count(const echo_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

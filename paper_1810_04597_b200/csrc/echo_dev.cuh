@@ -1,0 +1,268 @@
+// echo_dev.cuh — device-side parameters and point-wise GRMHD physics for the
+// sm_100a kernels.  Formulas: DESIGN.md §2 and readings A1-A30 (the paper,
+// PAPER.md:19, names the equations but prints none).  Written for the FP64
+// pipe: reciprocals computed once, products of the WENO smoothness factors
+// instead of three divisions, the stress written through b^2 (no E field).
+#pragma once
+#include <cstdint>
+
+#define ECHO_HD __host__ __device__ __forceinline__
+#define ECHO_D __device__ __forceinline__
+
+namespace echo {
+
+constexpr int kG = 5;  // halo: WENO5 (3) + DER6 (2), A12
+
+struct GridP {
+  int n[3];
+  long long N;      // cells per field
+  double lo[3];
+  double dx[3];     // (hi - lo) / n
+  double idx[3];    // 1 / dx
+  int bc[3][2];     // 0 periodic, 1 outflow
+  int rec, der, divb;
+};
+
+struct EosP {
+  double gamma;
+  double gfac;      // Gamma / (Gamma - 1)
+  double gm;        // (Gamma - 1) / Gamma
+  double rho_floor, p_floor, w_max, v2max;
+  int maxit;
+  double tol;
+};
+
+// ----------------------------------------------------------- metric types
+// Symmetric 3x3 stored as (00, 01, 02, 11, 12, 22).
+ECHO_HD int sidx(int i, int j) {
+  return (i <= j) ? (i == 0 ? j : (i == 1 ? 2 + j : 5)) : (j == 0 ? i : (j == 1 ? 2 + i : 5));
+}
+
+// Flat (Minkowski, Cartesian): every metric operation compiles away.
+struct FlatMet {
+  ECHO_D double alpha() const { return 1.0; }
+  ECHO_D double beta(int) const { return 0.0; }
+  ECHO_D double sqrtg() const { return 1.0; }
+  ECHO_D double gi_diag(int) const { return 1.0; }
+  ECHO_D void lower(const double* v, double* vl) const { vl[0] = v[0]; vl[1] = v[1]; vl[2] = v[2]; }
+  ECHO_D void raise(const double* v, double* vu) const { vu[0] = v[0]; vu[1] = v[1]; vu[2] = v[2]; }
+  static constexpr bool kFlat = true;
+};
+
+// General stationary 3+1 metric at one point (Kerr-Schild tables).
+struct GenMet {
+  double a, b[3], g[6], gi[6], sg;
+  ECHO_D double alpha() const { return a; }
+  ECHO_D double beta(int i) const { return b[i]; }
+  ECHO_D double sqrtg() const { return sg; }
+  ECHO_D double gi_diag(int j) const { return gi[sidx(j, j)]; }
+  ECHO_D void lower(const double* v, double* vl) const {
+    vl[0] = g[0] * v[0] + g[1] * v[1] + g[2] * v[2];
+    vl[1] = g[1] * v[0] + g[3] * v[1] + g[4] * v[2];
+    vl[2] = g[2] * v[0] + g[4] * v[1] + g[5] * v[2];
+  }
+  ECHO_D void raise(const double* v, double* vu) const {
+    vu[0] = gi[0] * v[0] + gi[1] * v[1] + gi[2] * v[2];
+    vu[1] = gi[1] * v[0] + gi[3] * v[1] + gi[4] * v[2];
+    vu[2] = gi[2] * v[0] + gi[4] * v[1] + gi[5] * v[2];
+  }
+  static constexpr bool kFlat = false;
+};
+
+// Table record sizes (doubles).  Face/centre value record: alpha, beta[3], g[6], gi[6], sqrtg.
+constexpr int kMetRec = 17;
+// Centre derivative record: dalpha[2], dbeta[2][3], dg[2][6]  (d/dx1, d/dx2; d/dx3 = 0).
+constexpr int kDerRec = 20;
+
+ECHO_D GenMet load_met(const double* __restrict__ rec) {
+  GenMet m;
+  m.a = __ldg(rec + 0);
+#pragma unroll
+  for (int i = 0; i < 3; i++) m.b[i] = __ldg(rec + 1 + i);
+#pragma unroll
+  for (int i = 0; i < 6; i++) m.g[i] = __ldg(rec + 4 + i);
+#pragma unroll
+  for (int i = 0; i < 6; i++) m.gi[i] = __ldg(rec + 10 + i);
+  m.sg = __ldg(rec + 16);
+  return m;
+}
+
+// Kerr-Schild tables (device pointers), all phi-independent (2-D in x1, x2),
+// extended by kG ghost layers so that ghost positions are covered.
+struct MetTables {
+  const double* cen;   // [(j+G)*(n1+2G) + (i+G)][kMetRec]       cell centres
+  const double* der;   // [(j+G)*(n1+2G) + (i+G)][kDerRec]       centre derivatives
+  const double* f0;    // [(j+G)*(n1+2G+1) + (i+G)][kMetRec]     x1-face i-1/2, i in [-G, n1+G]
+  const double* f1;    // [(j+G)*(n1+2G) + (i+G)][kMetRec]       x2-face j-1/2, j in [-G, n2+G]
+  int w0;              // n1 + 2G
+};
+
+ECHO_D const double* cen_rec(const MetTables& t, int i, int j) {
+  return t.cen + ((long long)(j + kG) * t.w0 + (i + kG)) * kMetRec;
+}
+ECHO_D const double* der_rec(const MetTables& t, int i, int j) {
+  return t.der + ((long long)(j + kG) * t.w0 + (i + kG)) * kDerRec;
+}
+// face i-1/2 along x1 at row j
+ECHO_D const double* f0_rec(const MetTables& t, int i, int j) {
+  return t.f0 + ((long long)(j + kG) * (t.w0 + 1) + (i + kG)) * kMetRec;
+}
+// face j-1/2 along x2 at column i
+ECHO_D const double* f1_rec(const MetTables& t, int i, int j) {
+  return t.f1 + ((long long)(j + kG) * t.w0 + (i + kG)) * kMetRec;
+}
+
+// --------------------------------------------------------------- indices
+ECHO_D int map_index(int i, int n, int bclo, int bchi) {  // ghost rule A12/A13
+  if (i < 0) return bclo == 0 ? ((i % n) + n) % n : 0;
+  if (i >= n) return bchi == 0 ? (i % n) : n - 1;
+  return i;
+}
+
+// ------------------------------------------------------- one state's physics
+// Everything the flux, conserved vector and speeds of one primitive state need.
+struct State {
+  double W2i;        // 1/W^2
+  double v[3];       // v^i
+  double vl[3];      // v_i
+  double v2;
+  double B[3];       // B^i
+  double Bl[3];      // B_i
+  double B2, vB, b2;
+  double rhoh, ptot;
+  double D, S[3], tau;
+};
+
+template <class M>
+ECHO_D void make_state(const M& m, const EosP& e, const double* pr, State& s) {
+  // pr: rho, u~^1..3, p, B^1..3
+  double ut[3] = {pr[1], pr[2], pr[3]};
+  double ul[3];
+  m.lower(ut, ul);
+  double u2 = ut[0] * ul[0] + ut[1] * ul[1] + ut[2] * ul[2];
+  double W2 = 1.0 + u2;
+  double iW = rsqrt(W2);
+  double W = W2 * iW;
+  s.W2i = iW * iW;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    s.v[i] = ut[i] * iW;
+    s.vl[i] = ul[i] * iW;
+    s.B[i] = pr[5 + i];
+  }
+  s.v2 = u2 * s.W2i;
+  m.lower(s.B, s.Bl);
+  s.B2 = s.B[0] * s.Bl[0] + s.B[1] * s.Bl[1] + s.B[2] * s.Bl[2];
+  s.vB = s.vl[0] * s.B[0] + s.vl[1] * s.B[1] + s.vl[2] * s.B[2];
+  s.b2 = s.B2 * s.W2i + s.vB * s.vB;
+  s.rhoh = pr[0] + e.gfac * pr[4];
+  s.ptot = pr[4] + 0.5 * s.b2;
+  double Z = s.rhoh * W2;
+  s.D = pr[0] * W;
+#pragma unroll
+  for (int i = 0; i < 3; i++) s.S[i] = (Z + s.B2) * s.vl[i] - s.vB * s.Bl[i];
+  // U = Z - p + (E^2 + B^2)/2 = Z + B^2 - p_tot  (E^2 = B^2 - b^2)
+  s.tau = Z + s.B2 - s.ptot - s.D;
+}
+
+// fast-speed bound along axis j (A4)
+template <class M>
+ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, int j, double& lm, double& lp) {
+  double cs2 = e.gamma * pr[4] / s.rhoh;
+  double ca2 = s.b2 / (s.rhoh + s.b2);
+  double a2 = cs2 + ca2 - cs2 * ca2;
+  double vj = s.v[j];
+  double disc = a2 * (1.0 - s.v2) * (m.gi_diag(j) * (1.0 - s.v2 * a2) - vj * vj * (1.0 - a2));
+  double sq = sqrt(fmax(disc, 0.0));
+  double iden = m.alpha() / (1.0 - s.v2 * a2);
+  double c = vj * (1.0 - a2);
+  lp = (c + sq) * iden - m.beta(j);
+  lm = (c - sq) * iden - m.beta(j);
+}
+
+// Non-densitised conserved vector (7 used comps along axis j: D, S_1..3, tau, B^{j+1}, B^{j+2})
+// and flux along j.  Momentum flux through the b^2 identity (E^2 = B^2 - b^2)
+//   W^j_i = v_i S^j + p_tot delta^j_i - B_i (B^j / W^2 + (v.B) v^j),
+//   S^j = (Z + B^2) v^j - (v.B) B^j.
+template <class M>
+ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
+  const double a = m.alpha();
+  const double bj = m.beta(j);
+  const double Vj = a * s.v[j] - bj;
+  const double bbar = s.B[j] * s.W2i + s.vB * s.v[j];
+  // Z + B^2 = tau + D + p_tot
+  const double ZB = s.tau + s.D + s.ptot;
+  const double Sj = ZB * s.v[j] - s.vB * s.B[j];
+  u[0] = s.D;
+  f[0] = Vj * s.D;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    u[1 + i] = s.S[i];
+    f[1 + i] = a * (s.vl[i] * Sj - s.Bl[i] * bbar) - bj * s.S[i] + (i == j ? a * s.ptot : 0.0);
+  }
+  u[4] = s.tau;
+  f[4] = a * (Sj - s.D * s.v[j]) - bj * s.tau;
+  const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+  u[5] = s.B[j1];
+  u[6] = s.B[j2];
+  f[5] = Vj * s.B[j1] - (a * s.v[j1] - m.beta(j1)) * s.B[j];
+  f[6] = Vj * s.B[j2] - (a * s.v[j2] - m.beta(j2)) * s.B[j];
+}
+
+// --------------------------------------------------------------- WENO5 (A2)
+// Left state at i+1/2 and right state at i-1/2 from u[-2..2] of one cell and one
+// variable.  beta_k are shared by both faces; alpha_k = d_k/(eps+beta_k)^2 is
+// evaluated through the products s_l s_m so one division per face remains.
+template <int REC>
+ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
+  const double eps = 1e-6;
+  const double c1312 = 13.0 / 12.0;
+  double t0 = um2 - 2.0 * um1 + u0, t0b = um2 - 4.0 * um1 + 3.0 * u0;
+  double t1 = um1 - 2.0 * u0 + up1, t1b = um1 - up1;
+  double t2 = u0 - 2.0 * up1 + up2, t2b = 3.0 * u0 - 4.0 * up1 + up2;
+  double b0 = c1312 * t0 * t0 + 0.25 * t0b * t0b;
+  double b1 = c1312 * t1 * t1 + 0.25 * t1b * t1b;
+  double b2 = c1312 * t2 * t2 + 0.25 * t2b * t2b;
+  double s0 = (eps + b0) * (eps + b0);
+  double s1 = (eps + b1) * (eps + b1);
+  double s2 = (eps + b2) * (eps + b2);
+  double p01 = s0 * s1, p02 = s0 * s2, p12 = s1 * s2;
+  double q0, q1, q2, r0, r1, r2, d0, d1, d2;
+  if (REC == 0) {
+    const double k = 0.125;
+    q0 = k * (3.0 * um2 - 10.0 * um1 + 15.0 * u0);
+    q1 = k * (-um1 + 6.0 * u0 + 3.0 * up1);
+    q2 = k * (3.0 * u0 + 6.0 * up1 - up2);
+    r0 = k * (3.0 * up2 - 10.0 * up1 + 15.0 * u0);
+    r1 = k * (-up1 + 6.0 * u0 + 3.0 * um1);
+    r2 = k * (3.0 * u0 + 6.0 * um1 - um2);
+    d0 = 1.0; d1 = 10.0; d2 = 5.0;
+  } else {
+    const double k = 1.0 / 6.0;
+    q0 = k * (2.0 * um2 - 7.0 * um1 + 11.0 * u0);
+    q1 = k * (-um1 + 5.0 * u0 + 2.0 * up1);
+    q2 = k * (2.0 * u0 + 5.0 * up1 - up2);
+    r0 = k * (2.0 * up2 - 7.0 * up1 + 11.0 * u0);
+    r1 = k * (-up1 + 5.0 * u0 + 2.0 * um1);
+    r2 = k * (2.0 * u0 + 5.0 * um1 - um2);
+    d0 = 1.0; d1 = 6.0; d2 = 3.0;
+  }
+  // left: weights (d0/s0, d1/s1, d2/s2) ~ (d0 p12, d1 p02, d2 p01)
+  double wl0 = d0 * p12, wl1 = d1 * p02, wl2 = d2 * p01;
+  // right (mirror): r0 uses beta2, r1 beta1, r2 beta0 -> (d0 p01, d1 p02, d2 p12)
+  double wr0 = d0 * p01, wr1 = wl1, wr2 = d2 * p12;
+  qL = (wl0 * q0 + wl1 * q1 + wl2 * q2) / (wl0 + wl1 + wl2);
+  qR = (wr0 * r0 + wr1 * r1 + wr2 * r2) / (wr0 + wr1 + wr2);
+}
+
+// --------------------------------------------------------------- DER (A5)
+template <int DER>
+ECHO_D double der5(double Fm2, double Fm1, double F0, double Fp1, double Fp2) {
+  if (DER == 6)
+    return F0 - (Fm1 - 2.0 * F0 + Fp1) * (1.0 / 24.0) +
+           (Fm2 - 4.0 * Fm1 + 6.0 * F0 - 4.0 * Fp1 + Fp2) * (3.0 / 640.0);
+  if (DER == 4) return F0 - (Fm1 - 2.0 * F0 + Fp1) * (1.0 / 24.0);
+  return F0;
+}
+
+}  // namespace echo

@@ -1,0 +1,248 @@
+"""GPU parity: the C-ABI library (sm_100a kernels) against the oracle on the
+same seeded inputs, element by element, normwise per variable group (A16):
+1e-12 per RK stage, 1e-10 after 10 steps (BASELINE.json north_star).
+Marked gpu: run on a B200 with `pytest -m gpu`."""
+import math
+
+import numpy as np
+import pytest
+
+import echo_inputs as I
+from tests.util import CONS_GROUPS, PRIM5_GROUPS, PRIM8_GROUPS, assert_groups
+
+pytestmark = pytest.mark.gpu
+
+TOL_STAGE = 1e-12
+TOL_10 = 1e-10
+
+
+@pytest.fixture(scope="module")
+def E():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1810_04597_b200 import build
+
+    build.build()
+    from paper_1810_04597_b200 import echo
+
+    return echo
+
+
+def small_problem(cfg, n):
+    p = I.problem(cfg, n=n)
+    return p
+
+
+def ocfg(orc, p):
+    return orc.Cfg(**p.grid_kwargs())
+
+
+# ------------------------------------------------------------ invariants
+def test_uniform_state_gpu(E):
+    n = (70, 9, 6)
+    P8 = I.uniform_prims(n, 0.7, (0.3, -0.2, 0.1), 1.3, (0.4, -0.6, 0.2))
+    g = E.Echo(n=n, lo=(0, 0, 0), hi=(1, 1, 1), bc=((0, 0), (1, 1), (0, 0)))
+    g.set_prims(P8)
+    L = g.rhs()
+    assert not np.any(L)
+    g.step(0.01)
+    U = g.get_cons()
+    for q in range(8):
+        assert np.all(U[q] == U[q].flat[0])
+
+
+# --------------------------------------------------------- stage parity
+CASES = [
+    # (config, grid) — grids span several tiles (64 along the sweep, 4 across) and ragged tails
+    (0, (32, 32, 32)),            # config 0 at its full size
+    (0, (150, 13, 70)),           # multi-tile + ragged in every direction
+    (1, (40, 36, 34)),            # CP Alfven recipe, reduced grid
+    (2, (45, 38, 41)),            # outflow blast, reduced grid
+    (3, (48, 48, 48)),            # config-3 recipe (32 modes, k<=8), reduced grid
+    (4, (72, 36, 24)),            # Kerr-Schild torus, reduced grid
+]
+
+
+@pytest.mark.parametrize("cfg,n", CASES)
+def test_rhs_and_stage_parity(E, orc, cfg, n):
+    p = small_problem(cfg, n)
+    P8 = I.initial_prims(p)
+    oc = ocfg(orc, p)
+    Un, P5 = orc.set_prims(oc, P8)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    gun, _, gp = g.get_state()
+    assert_groups(gun, Un, CONS_GROUPS, 1e-14, what="prim2cons")
+    assert_groups(gp, P5, PRIM5_GROUPS, 1e-14, what="prim2cons P5")
+    # rhs on identical inputs
+    L = orc.rhs(oc, gun, gp)
+    assert_groups(g.rhs(), L, CONS_GROUPS, TOL_STAGE, what=f"rhs cfg{cfg}")
+    # CFL
+    dt_o = orc.max_dt(oc, gun, gp, p.cfl)
+    dt_g = g.max_dt(p.cfl)
+    assert dt_g == pytest.approx(dt_o, rel=1e-14)
+    # stage-chained parity: each oracle stage starts from the GPU's own input state
+    for s in (1, 2, 3):
+        un, us, pp = g.get_state()
+        g.stage(s, dt_o)
+        Uo, Po, cnt = orc.stage(oc, s, dt_o, un, un if s == 1 else us, pp)
+        gn, gs, gP = g.get_state()
+        Ug = gs if s < 3 else gn
+        assert_groups(Ug, Uo, CONS_GROUPS, TOL_STAGE, what=f"stage {s} U cfg{cfg}")
+        assert_groups(gP, Po, PRIM5_GROUPS, TOL_STAGE, what=f"stage {s} P cfg{cfg}")
+
+
+@pytest.mark.parametrize("cfg,n,steps", [(0, (32, 32, 32), 10), (1, (32, 32, 32), 10), (2, (40, 40, 40), 10),
+                                         (3, (40, 40, 40), 5), (4, (64, 32, 16), 10)])
+def test_multistep_parity(E, orc, cfg, n, steps):
+    p = small_problem(cfg, n)
+    P8 = I.initial_prims(p)
+    oc = ocfg(orc, p)
+    U, P = orc.set_prims(oc, P8)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    ocnt = [0, 0]
+    for _ in range(steps):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        U, P, cnt = orc.step(oc, dt, U, P)
+        ocnt[0] += cnt[0]
+        ocnt[1] += cnt[1]
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"{steps} steps U cfg{cfg}")
+    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"{steps} steps P cfg{cfg}")
+    st = g.stats()
+    assert (st["floor_events"], st["c2p_failures"]) == tuple(ocnt)
+    if cfg in (0, 1, 3):
+        assert ocnt == [0, 0]
+    # the user-facing prims agree too
+    assert_groups(g.get_prims(), orc.get_prims(oc, U, P), PRIM8_GROUPS, TOL_10, what="get_prims")
+
+
+def test_con2prim_parity(E, orc):
+    p = small_problem(2, (20, 18, 16))
+    P8 = I.initial_prims(p)
+    oc = ocfg(orc, p)
+    U, P = orc.set_prims(oc, P8)
+    # perturb the conserved state so the Newton solve has work to do, incl. floors
+    rng = np.random.default_rng(3)
+    U2 = U * (1 + 1e-3 * rng.standard_normal(U.shape))
+    U2[4, 0, 0, :5] = -1e-3  # tau < 0: pressure floor
+    g = E.Echo(p)
+    g.set_prims(P8)
+    E.set_cons(g.ctx, np.ascontiguousarray(U2))
+    Uo, Po, cnt = orc.con2prim(oc, U2, P)
+    gn, _, gp = g.get_state()
+    assert_groups(gn, Uo, CONS_GROUPS, TOL_STAGE, what="con2prim U")
+    assert_groups(gp, Po, PRIM5_GROUPS, TOL_STAGE, what="con2prim P")
+    st = g.stats()
+    assert (st["floor_events"], st["c2p_failures"]) == cnt
+    assert cnt[0] + cnt[1] >= 5
+
+
+def test_switches_parity(E, orc):
+    # rec=FV, der=4, divb=none on a multi-tile grid
+    p = small_problem(0, (70, 9, 10))
+    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}):
+        for k, v in kw.items():
+            setattr(p, k, v)
+        P8 = I.initial_prims(p)
+        oc = ocfg(orc, p)
+        U, P = orc.set_prims(oc, P8)
+        g = E.Echo(p)
+        g.set_prims(P8)
+        assert_groups(g.rhs(), orc.rhs(oc, U, P), CONS_GROUPS, TOL_STAGE, what=f"rhs {kw}")
+        p = small_problem(0, (70, 9, 10))
+
+
+# ------------------------------------------------ full-size sampled parity
+FULL = [(1, None), (2, None), (4, None), (3, None)]
+
+
+def _full_state(E, p, device_ic):
+    import torch
+
+    g = E.Echo(p)
+    if device_ic:
+        P8 = I.initial_prims(p, device="cuda")
+        g.set_prims(P8)
+        del P8
+    else:
+        g.set_prims(I.initial_prims(p))
+    return g
+
+
+@pytest.mark.parametrize("cfg,_", FULL)
+def test_full_size_sampled_stage_parity(E, orc, cfg, _):
+    """At BASELINE.json's full sizes, in the bench launch configuration: each RK
+    stage's output at 2000 sampled cells (incl. the 8 corners) against the
+    oracle's per-cell path on the GPU's own input state."""
+    import torch
+
+    p = I.problem(cfg)
+    g = _full_state(E, p, device_ic=(cfg == 3))
+    oc = ocfg(orc, p)
+    cells = I.sample_cells(p.n, 2000, seed=100 + cfg)
+    lin = (cells[:, 2] * p.n[1] + cells[:, 1]) * p.n[0] + cells[:, 0]
+    lin_t = torch.as_tensor(lin, device="cuda")
+    N = p.ncells
+    un = torch.empty((8, N), dtype=torch.float64, device="cuda")
+    us = torch.empty((8, N), dtype=torch.float64, device="cuda")
+    pp = torch.empty((5, N), dtype=torch.float64, device="cuda")
+    E.get_state(g.ctx, un, None, pp)
+    un_h = un.cpu().numpy().reshape(8, *p.n[::-1])
+    pp_h = pp.cpu().numpy().reshape(5, *p.n[::-1])
+    dt = g.max_dt(p.cfl)
+    assert dt == pytest.approx(orc.max_dt(oc, un_h, pp_h, p.cfl), rel=1e-14)
+    us_h = un_h
+    for s in (1, 2, 3):
+        g.stage(s, dt)
+        Uo, Po, _ = orc.stage_cells(oc, s, dt, un_h, us_h, pp_h, cells)
+        E.get_state(g.ctx, un, us, pp)
+        torch.cuda.synchronize()
+        Ug = (us if s < 3 else un)[:, lin_t].cpu().numpy().T
+        Pg = pp[:, lin_t].cpu().numpy().T
+        assert_groups(Ug, Uo, CONS_GROUPS, TOL_STAGE, axis=1, what=f"full cfg{cfg} stage {s} U")
+        assert_groups(Pg, Po, PRIM5_GROUPS, TOL_STAGE, axis=1, what=f"full cfg{cfg} stage {s} P")
+        if s < 3:
+            un_h = un.cpu().numpy().reshape(8, *p.n[::-1])
+            us_h = us.cpu().numpy().reshape(8, *p.n[::-1])
+            pp_h = pp.cpu().numpy().reshape(5, *p.n[::-1])
+    g.close()
+
+
+# ------------------------------------------------------------ robustness
+def test_determinism_bitwise(E):
+    p = small_problem(2, (70, 33, 20))
+    P8 = I.initial_prims(p)
+    outs = []
+    for _ in range(2):
+        g = E.Echo(p)
+        g.set_prims(P8)
+        for _ in range(3):
+            g.step(g.max_dt(0.4))
+        outs.append(g.get_state())
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_errors_are_loud(E):
+    p = small_problem(0, (8, 8, 8))
+    g = E.Echo(p)
+    with pytest.raises(E.EchoError) as ei:
+        g.step(0.01)
+    assert ei.value.code == E.E_ORDER
+    P8 = I.initial_prims(p)
+    P8[4, 3, 2, 1] = -1.0
+    with pytest.raises(E.EchoError) as ei:
+        g.set_prims(P8)
+    assert ei.value.code == E.E_UNPHYSICAL and "(1,2,3)" in str(ei.value)
+    P8[4, 3, 2, 1] = 1.0
+    g.set_prims(P8)
+    with pytest.raises(E.EchoError) as ei:
+        g.stage(2, 0.01)
+    assert ei.value.code == E.E_ORDER
+    with pytest.raises(E.EchoError):
+        E.create(n=(0, 4, 4), lo=(0, 0, 0), hi=(1, 1, 1), bc=((0, 0),) * 3)
