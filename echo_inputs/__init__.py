@@ -75,6 +75,7 @@ class Problem:
     rec: int = 0
     der: int = 6
     divb: int = 0
+    der_jump: float = 0.5
     steps: int = 10
     cfl: float = 0.4
     seed: int = 0
@@ -88,7 +89,7 @@ class Problem:
         return dict(n=tuple(self.n), lo=tuple(self.lo), hi=tuple(self.hi), bc=tuple(tuple(b) for b in self.bc),
                     metric=self.metric, M=self.M, a=self.a, gamma=self.gamma, rho_floor=self.rho_floor,
                     p_floor=self.p_floor, w_max=self.w_max, c2p_max_iter=self.c2p_max_iter,
-                    c2p_tol=self.c2p_tol, rec=self.rec, der=self.der, divb=self.divb)
+                    c2p_tol=self.c2p_tol, rec=self.rec, der=self.der, divb=self.divb, der_jump=self.der_jump)
 
     def centres(self, a: int) -> np.ndarray:
         d = (self.hi[a] - self.lo[a]) / self.n[a]

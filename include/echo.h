@@ -59,11 +59,15 @@ typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_met
 /* Grid: n owned cells per axis (n >= 1; periodic n < 5 is allowed, ghosts wrap
  * modulo n [A12]); [lo, hi) coordinate extent per axis (lo < hi).  Minkowski
  * uses Cartesian (x, y, z); Kerr-Schild uses (ln r, theta, phi) [A14] and
- * requires 0 < theta_lo < theta_hi < pi over the whole ghost-extended range.
+ * requires sin(theta) != 0 at every centre and face of the ghost-extended range.
  * bc[a][0]/[1] = lower/upper boundary of axis a.
  * rec: 0 = WENO5 point-value form (A2, default), 1 = WENO5 finite-volume form.
  * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
- * divb: 0 = field-CD constrained transport (A6, default), 1 = none. */
+ * divb: 0 = field-CD constrained transport (A6, default), 1 = none.
+ * der_jump: DER shock switch (A31): the DER correction at a face is dropped
+ *   (H = F) when one of the 5 faces of its stencil joins two cells whose rho or
+ *   p differ by more than der_jump x the smaller of the two; <= 0 disables it
+ *   (default 0.5). */
 typedef struct {
   int n[3];
   double lo[3], hi[3];
@@ -71,9 +75,11 @@ typedef struct {
   int rec;
   int der;
   int divb;
+  double der_jump;
 } echo_grid;
 
-/* Stationary background metric (A1, A14): Minkowski, or Kerr-Schild with mass M > 0 and spin |a| < M. */
+/* Stationary background metric (A1, A14): Minkowski, or Kerr-Schild with mass M >= 0 and spin a
+ * (M = 0 is flat space in oblate-spheroidal / spherical coordinates; used by the pins). */
 typedef struct {
   int kind; /* echo_metric_kind */
   double M, a;

@@ -58,6 +58,7 @@ class _Cfg(C.Structure):
         ("rec", C.c_int),
         ("der", C.c_int),
         ("divb", C.c_int),
+        ("der_jump", C.c_double),
         ("nthreads", C.c_int),
     ]
 
@@ -90,6 +91,7 @@ class Cfg:
     rec: int = 0
     der: int = 6
     divb: int = 0
+    der_jump: float = 0.5
     nthreads: int = 0
 
     def c(self) -> _Cfg:
@@ -102,7 +104,7 @@ class Cfg:
             s.bc[i][1] = int(self.bc[i][1])
         for k in ("metric", "c2p_max_iter", "rec", "der", "divb", "nthreads"):
             setattr(s, k, int(getattr(self, k)))
-        for k in ("M", "a", "gamma", "rho_floor", "p_floor", "w_max", "c2p_tol"):
+        for k in ("M", "a", "gamma", "rho_floor", "p_floor", "w_max", "c2p_tol", "der_jump"):
             setattr(s, k, float(getattr(self, k)))
         return s
 

@@ -55,6 +55,9 @@ typedef struct {
   int rec;           /* 0 WENO5 point-value form (A2), 1 WENO5 finite-volume form */
   int der;           /* 6 DER6, 4 DER4, 2 plain difference (A5) */
   int divb;          /* 0 field-CD (A6), 1 none: plain flux difference for B */
+  double der_jump;   /* A31 DER switch: the DER correction at a face is dropped (H = F) when a face
+                        of its 5-face stencil joins cells whose rho or p differ by more than
+                        der_jump x the smaller value; <= 0 disables the switch */
   int nthreads;      /* OpenMP threads (<=0: library default) */
 } orc_cfg;
 

@@ -107,9 +107,29 @@ double orc_der(const double F[5], int der) {
   return F[2];
 }
 
+/* A31: does the face between cells with prims pa, pb join a jump in rho or p? */
+static int rough_face(const orc_cfg* c, const double pa[8], const double pb[8]) {
+  if (!(c->der_jump > 0.0)) return 0;
+  return fabs(pb[0] - pa[0]) > c->der_jump * fmin(pa[0], pb[0]) ||
+         fabs(pb[4] - pa[4]) > c->der_jump * fmin(pa[4], pb[4]);
+}
+
+/* DER flux at a face from the 5 face fluxes F5[m][q] (faces i-3/2..i+5/2) and
+ * their roughness flags: the plain flux if any face of the stencil is rough (A31). */
+static void der_face(const orc_cfg* c, const double F5[5][8], const int rough5[5], double H[8]) {
+  int any = 0;
+  for (int m = 0; m < 5; m++) any |= rough5[m];
+  for (int q = 0; q < 8; q++) {
+    double f5[5];
+    for (int m = 0; m < 5; m++) f5[m] = F5[m][q];
+    H[q] = any ? F5[2][q] : orc_der(f5, c->der);
+  }
+}
+
 /* Face flux at face i+1/2 from the stencil st[m][v] = prims of cells i-2+m,
- * m = 0..5, v = 0..7; xf = face coordinates; a = axis.  Shared by both paths. */
-static void face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8]) {
+ * m = 0..5, v = 0..7; xf = face coordinates; a = axis.  Shared by both paths.
+ * Returns the A31 roughness flag of the face. */
+static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8]) {
   double qL[8], qR[8];
   for (int v = 0; v < 8; v++) {
     double l[5], r[5];
@@ -127,6 +147,7 @@ static void face_flux(const orc_cfg* c, const double st[6][8], const double xf[3
   orc_met m;
   orc_met_eval(c, xf, &m);
   orc_hll(&m, c->gamma, qL, qR, a, F);
+  return rough_face(c, st[2], st[3]);
 }
 
 /* prims (8) of an owned cell from the state arrays */
@@ -272,6 +293,7 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
       cell[t1] = line % c->n[t1];
       cell[t2] = line / c->n[t1];
       double* F = (double*)malloc(sizeof(double) * 8 * (na + 5));
+      int* rf = (int*)malloc(sizeof(int) * (na + 5));
       double* H = (double*)malloc(sizeof(double) * 8 * (na + 1));
       for (long long fi = -3; fi < na + 2; fi++) { /* face fi+1/2 */
         double st[6][8];
@@ -284,14 +306,16 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
         xf[a] = face_of(c, a, fi);
         xf[t1] = centre_of(c, t1, cell[t1]);
         xf[t2] = centre_of(c, t2, cell[t2]);
-        face_flux(c, st, xf, a, &F[8 * (fi + 3)]);
+        rf[fi + 3] = face_flux(c, st, xf, a, &F[8 * (fi + 3)]);
       }
       for (long long hi = -1; hi < na; hi++) { /* DER flux at face hi+1/2 */
-        for (int q = 0; q < 8; q++) {
-          double f5[5];
-          for (int m = 0; m < 5; m++) f5[m] = F[8 * (hi - 2 + m + 3) + q];
-          H[8 * (hi + 1) + q] = orc_der(f5, c->der);
+        double F5[5][8];
+        int r5[5];
+        for (int m = 0; m < 5; m++) {
+          for (int q = 0; q < 8; q++) F5[m][q] = F[8 * (hi - 2 + m + 3) + q];
+          r5[m] = rf[hi - 2 + m + 3];
         }
+        der_face(c, F5, r5, &H[8 * (hi + 1)]);
       }
       for (long long i = 0; i < na; i++) {
         long long cc[3] = {cell[0], cell[1], cell[2]};
@@ -305,6 +329,7 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
         for (int q = 0; q < 3; q++) *oget(&O, q, cc[0], cc[1], cc[2]) = Om[q];
       }
       free(F);
+      free(rf);
       free(H);
     }
   }
@@ -370,6 +395,7 @@ static void hhat_at(const orc_cfg* c, const double* U8, const double* P5, int a,
                     double H[8]) {
   int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
   double F[5][8];
+  int r5[5];
   for (int f = 0; f < 5; f++) {
     long long fi = cell[a] - 2 + f;
     double st[6][8];
@@ -382,13 +408,9 @@ static void hhat_at(const orc_cfg* c, const double* U8, const double* P5, int a,
     xf[a] = face_of(c, a, fi);
     xf[t1] = centre_of(c, t1, cell[t1]);
     xf[t2] = centre_of(c, t2, cell[t2]);
-    face_flux(c, st, xf, a, F[f]);
+    r5[f] = face_flux(c, st, xf, a, F[f]);
   }
-  for (int q = 0; q < 8; q++) {
-    double f5[5];
-    for (int m = 0; m < 5; m++) f5[m] = F[m][q];
-    H[q] = orc_der(f5, c->der);
-  }
+  der_face(c, F, r5, H);
 }
 
 /* hydro/divb-none rhs and Omega of an owned cell, sweeps in axis order */

@@ -154,9 +154,13 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   const bool ks = metric->kind == ECHO_METRIC_KERR_SCHILD;
   if (ks) {
     if (!(metric->M >= 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: Kerr-Schild needs M >= 0");
+    // every centre and face of the ghost-extended theta range must avoid the polar axis (sin theta = 0)
     double d2 = (grid->hi[1] - grid->lo[1]) / grid->n[1];
-    if (!(grid->lo[1] - kG * d2 > 0.0) || !(grid->hi[1] + kG * d2 < M_PI))
-      return fail(nullptr, ECHO_E_ARG, "echo_create: Kerr-Schild theta range (with 5 ghost cells) must lie in (0, pi)");
+    for (int h = -2 * kG; h <= 2 * grid->n[1] + 2 * kG; h++) {
+      double th = grid->lo[1] + 0.5 * h * d2;
+      if (!(std::fabs(std::sin(th)) > 1e-12))
+        return fail(nullptr, ECHO_E_ARG, "echo_create: Kerr-Schild theta grid (with 5 ghost cells) touches sin(theta) = 0");
+    }
   }
   int dev;
   cudaError_t ce = cudaGetDevice(&dev);
@@ -177,6 +181,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   g.rec = grid->rec;
   g.der = grid->der;
   g.divb = grid->divb;
+  g.der_jump = grid->der_jump;
   EosP& e = c->e;
   e.gamma = eos->gamma;
   e.gfac = eos->gamma / (eos->gamma - 1.0);

@@ -21,6 +21,7 @@ struct GridP {
   double idx[3];    // 1 / dx
   int bc[3][2];     // 0 periodic, 1 outflow
   int rec, der, divb;
+  double der_jump;  // A31 DER shock switch (<= 0: off)
 };
 
 struct EosP {
@@ -112,6 +113,29 @@ ECHO_D const double* f1_rec(const MetTables& t, int i, int j) {
   return t.f1 + ((long long)(j + kG) * t.w0 + (i + kG)) * kMetRec;
 }
 
+// ------------------------------------------------ FP64 reciprocal / rsqrt
+// MUFU seed (rcp/rsqrt.approx.ftz.f64: high word only, ~20 bits) + two Newton
+// steps: ~full double precision (<= 1-2 ulp), no slow-path branch.  Arguments
+// here are always positive, normal and finite (sums of squares, 1 - v^2 a^2, ...).
+ECHO_D double frcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+ECHO_D double frsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+ECHO_D double fsqrt(double x) { return x > 0.0 ? x * frsqrt(x) : 0.0; }
+
 // --------------------------------------------------------------- indices
 ECHO_D int map_index(int i, int n, int bclo, int bchi) {  // ghost rule A12/A13
   if (i < 0) return bclo == 0 ? ((i % n) + n) % n : 0;
@@ -141,7 +165,7 @@ ECHO_D void make_state(const M& m, const EosP& e, const double* pr, State& s) {
   m.lower(ut, ul);
   double u2 = ut[0] * ul[0] + ut[1] * ul[1] + ut[2] * ul[2];
   double W2 = 1.0 + u2;
-  double iW = rsqrt(W2);
+  double iW = frsqrt(W2);
   double W = W2 * iW;
   s.W2i = iW * iW;
 #pragma unroll
@@ -168,16 +192,42 @@ ECHO_D void make_state(const M& m, const EosP& e, const double* pr, State& s) {
 // fast-speed bound along axis j (A4)
 template <class M>
 ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, int j, double& lm, double& lp) {
-  double cs2 = e.gamma * pr[4] / s.rhoh;
-  double ca2 = s.b2 / (s.rhoh + s.b2);
-  double a2 = cs2 + ca2 - cs2 * ca2;
+  // a^2 = cs^2 + cA^2 - cs^2 cA^2 with cs^2 = Gamma p/(rho h), cA^2 = b^2/(rho h + b^2)
+  //     = (Gamma p + b^2) / (rho h + b^2)   (one division instead of two)
+  double a2 = (e.gamma * pr[4] + s.b2) * frcp(s.rhoh + s.b2);
   double vj = s.v[j];
   double disc = a2 * (1.0 - s.v2) * (m.gi_diag(j) * (1.0 - s.v2 * a2) - vj * vj * (1.0 - a2));
-  double sq = sqrt(fmax(disc, 0.0));
-  double iden = m.alpha() / (1.0 - s.v2 * a2);
+  double sq = fsqrt(disc);
+  double iden = m.alpha() * frcp(1.0 - s.v2 * a2);
   double c = vj * (1.0 - a2);
   lp = (c + sq) * iden - m.beta(j);
   lm = (c - sq) * iden - m.beta(j);
+}
+
+// densitised HLL flux (7 comps) between two reconstructed states at one face (A4)
+template <class M>
+ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* pr, int AX, double* F) {
+  State sl, sr;
+  make_state(m, e, pl, sl);
+  make_state(m, e, pr, sr);
+  double uL[7], fL[7], uR[7], fR[7];
+  cons_flux(m, sl, AX, uL, fL);
+  cons_flux(m, sr, AX, uR, fR);
+  double lmL, lpL, lmR, lpR;
+  speeds(m, e, pl, sl, AX, lmL, lpL);
+  speeds(m, e, pr, sr, AX, lmR, lpR);
+  const double sL = fmin(0.0, fmin(lmL, lmR));
+  const double sR = fmax(0.0, fmax(lpL, lpR));
+  const double den = sR - sL;
+  if (den > 0.0) {
+    const double inv = m.sqrtg() * frcp(den);
+    const double ss = sL * sR;
+#pragma unroll
+    for (int q = 0; q < 7; q++) F[q] = (sR * fL[q] - sL * fR[q] + ss * (uR[q] - uL[q])) * inv;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 7; q++) F[q] = 0.5 * (fL[q] + fR[q]) * m.sqrtg();
+  }
 }
 
 // Non-densitised conserved vector (7 used comps along axis j: D, S_1..3, tau, B^{j+1}, B^{j+2})
@@ -251,8 +301,11 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
   double wl0 = d0 * p12, wl1 = d1 * p02, wl2 = d2 * p01;
   // right (mirror): r0 uses beta2, r1 beta1, r2 beta0 -> (d0 p01, d1 p02, d2 p12)
   double wr0 = d0 * p01, wr1 = wl1, wr2 = d2 * p12;
-  qL = (wl0 * q0 + wl1 * q1 + wl2 * q2) / (wl0 + wl1 + wl2);
-  qR = (wr0 * r0 + wr1 * r1 + wr2 * r2) / (wr0 + wr1 + wr2);
+  // both normalisations through one reciprocal: 1/(SL SR)
+  const double SL = wl0 + wl1 + wl2, SR = wr0 + wr1 + wr2;
+  const double inv = frcp(SL * SR);
+  qL = (wl0 * q0 + wl1 * q1 + wl2 * q2) * (SR * inv);
+  qR = (wr0 * r0 + wr1 * r1 + wr2 * r2) * (SL * inv);
 }
 
 // --------------------------------------------------------------- DER (A5)

@@ -1,14 +1,18 @@
 // sweep.cu — the axis-sweep kernels K2x/K2y/K2z (DESIGN.md §2 step 2, rows a1-a5).
 //
-// One CTA owns a tile of NL lines x TA cells along the sweep axis.  The tile's
-// primitives (8 fields, TA + 2*5 cells per line) are read from HBM once per
-// sweep with coalesced loads into shared memory; the ghost fill (a1) happens
-// in that load as an index map (periodic wrap mod n / outflow clamp), so no
-// padded arrays and no separate ghost pass exist.  Then, all from shared memory:
-//   A  WENO5 per (cell, variable): both faces of the cell, shared beta_k (a2)
-//   B  one thread per face: states, speeds, HLL (a3), densitised
-//   C1 DER6 per (face, component) (a4)
-//   C2 per (cell, component): rhs -= dH/Delta, field-CD EMF contributions (a5)
+// A persistent CTA (2 per SM, 256 threads) walks over tiles of NL = 4 lines x
+// TA = 58 cells along the sweep axis.  Every thread owns one (line, position)
+// slot x in [0, 64) of its line in every phase, so no per-item index division
+// exists and one address computation serves all 8 variables / 7 flux
+// components.  The next tile's primitives (8 fields, TA + 2*5 cells per line)
+// and the rhs/EMF values it will accumulate into are prefetched with cp.async
+// into a second shared-memory buffer while the current tile is computed.  The
+// ghost fill (a1) is an index map inside those loads (periodic wrap mod n /
+// outflow clamp): no padded arrays, no ghost pass.  Per tile, in shared memory:
+//   A  WENO5 of the 8 variables of cell x: both faces, shared beta_k (a2)
+//   B  face x: states, speeds, HLL (a3), densitised
+//   C1 DER6 of the 7 flux components at face x (a4)
+//   C2 cell x: rhs -= dH/Delta, field-CD EMF contributions (a5)
 // Each interface flux is computed by exactly one thread in a fixed operation
 // order, so results are bitwise run-to-run deterministic.
 #include <cuda_runtime.h>
@@ -18,202 +22,253 @@
 
 namespace echo {
 
-constexpr int TA = 64;         // cells along the axis per tile
+constexpr int TA = 58;         // owned cells per line per tile
 constexpr int NL = 4;          // lines per tile
-constexpr int LEN_P = TA + 10; // primitive stencil per line
-constexpr int LEN_Q = TA + 6;  // reconstructed cells per line
-constexpr int NF = TA + 5;     // faces per line
-constexpr int NH = TA + 1;     // DER faces per line
-constexpr int kSweepThreads = NF * NL;  // 276: one face per thread in phase B
-constexpr int SZ_P = 8 * NL * LEN_P;
-constexpr int SZ_Q = 16 * NL * LEN_Q;
-static_assert(7 * NL * NF <= SZ_P, "F must fit in the primitive tile");
-static_assert(7 * NL * NH <= SZ_Q, "H must fit in the state tile");
-constexpr size_t kSweepSmem = sizeof(double) * (SZ_P + SZ_Q);
+constexpr int SLOT = 64;       // slots per line: thread = (line, slot)
+constexpr int LEN_P = TA + 10; // primitive stencil per line (68)
+constexpr int LEN_Q = TA + 6;  // reconstructed cells per line (64 = SLOT)
+constexpr int NF = TA + 5;     // faces per line (63)
+constexpr int NH = TA + 1;     // DER faces per line (59)
+constexpr int kSweepThreads = NL * SLOT;  // 256
+constexpr int kSweepBlocksPerSM = 2;
+static_assert(LEN_Q == SLOT, "one reconstructed cell per thread");
+constexpr int VP = NL * LEN_P;  // variable stride in the primitive buffer
+constexpr int VQ = NL * LEN_Q;  // variable stride in the state buffer
+constexpr int VF = NL * NF;     // component stride of F
+constexpr int VH = NL * NH;     // component stride of H
+constexpr int VA = NL * TA;     // component stride of the accumulation buffer
+constexpr int SZ_P = 8 * VP;    // one primitive buffer (later reused for F)
+constexpr int SZ_Q = 16 * VQ;   // L/R states (later reused for H)
+constexpr int SZ_A = 7 * VA;    // one rhs/EMF accumulation buffer
+static_assert(7 * VF <= SZ_P, "F must fit in the primitive tile");
+static_assert(7 * VH <= SZ_Q, "H must fit in the state tile");
+constexpr int OFF_P0 = 0, OFF_P1 = SZ_P, OFF_Q = 2 * SZ_P, OFF_A0 = OFF_Q + SZ_Q, OFF_A1 = OFF_A0 + SZ_A;
+constexpr size_t kSweepSmem = sizeof(double) * (OFF_A1 + SZ_A);
 
+// conflict-free layout: for the x sweep the along-axis index is fastest, for
+// y/z the line (x) index is fastest — matching the coalesced global direction
 template <int AX, int LEN>
-ECHO_D int soff(int t, int a) {  // conflict-free layout: the coalesced index is fastest
+ECHO_HD int soff(int t, int a) {
   return AX == 0 ? t * LEN + a : a * NL + t;
-}
-template <int AX, int LEN>
-ECHO_D void split(int r, int& t, int& a) {
-  if (AX == 0) { t = r / LEN; a = r - t * LEN; }
-  else { a = r / NL; t = r - a * NL; }
 }
 
 // first axis that writes a given B/Omega component (the others accumulate)
 ECHO_HD int first_axis(int comp) { return comp == 0 ? 1 : 0; }
 
-template <int AX, bool KS, int DER, int REC, bool DIVB_NONE>
-__global__ void __launch_bounds__(kSweepThreads, 2)
-k_sweep(const GridP g, const EosP e, const MetTables mt, const double* __restrict__ P,
-        const double* __restrict__ U, double* __restrict__ R, double* __restrict__ Om) {
-  extern __shared__ double smem[];
-  double* sP = smem;         // [8][...LEN_P], later F [7][...NF]
-  double* sQ = smem + SZ_P;  // [16][...LEN_Q] (L: 0-7, R: 8-15), later H [7][...NH]
-  const int tid = threadIdx.x;
+// does sweep AX accumulate into (rather than overwrite) its output component q?
+template <int AX, bool DN>
+ECHO_HD bool accumulates(int q) {
+  if (q < 5) return AX != 0;
+  const int b1 = (AX + 1) % 3, b2 = (AX + 2) % 3;
+  if (DN) return first_axis(q == 5 ? b1 : b2) != AX;
+  return first_axis(q == 5 ? b2 : b1) != AX;  // q=5 -> Omega_{a+2}, q=6 -> Omega_{a+1}
+}
+// global array holding output component q of sweep AX
+template <int AX, bool DN>
+ECHO_D double* out_ptr(int q, double* R, double* Om, long long N) {
+  if (q < 5) return R + q * N;
+  const int b1 = (AX + 1) % 3, b2 = (AX + 2) % 3;
+  if (DN) return R + (5 + (q == 5 ? b1 : b2)) * N;
+  return Om + (q == 5 ? b2 : b1) * N;
+}
+
+ECHO_D void cp_async8(unsigned saddr, const double* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gsrc));
+}
+ECHO_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+ECHO_D void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+struct TileGeom {
+  int na, nt, ta_tiles, tt_tiles;
+  long long ntiles;
+};
+
+template <int AX>
+ECHO_D void tile_origin(const TileGeom& tg, long long tile, int& a0, int& t0, int& zz) {
+  // AX = 0: x tiles fastest; AX = 1, 2: transverse (x) tiles fastest -> neighbouring CTAs share rows
+  long long r;
+  if (AX == 0) {
+    a0 = (int)(tile % tg.ta_tiles) * TA;
+    r = tile / tg.ta_tiles;
+    t0 = (int)(r % tg.tt_tiles) * NL;
+    zz = (int)(r / tg.tt_tiles);
+  } else {
+    t0 = (int)(tile % tg.tt_tiles) * NL;
+    r = tile / tg.tt_tiles;
+    a0 = (int)(r % tg.ta_tiles) * TA;
+    zz = (int)(r / tg.ta_tiles);
+  }
+}
+
+template <int AX>
+ECHO_D long long lin_of(const GridP& g, int a, int t, int zz) {
+  int i, j, k;
+  if (AX == 0) { i = a; j = t; k = zz; }
+  else if (AX == 1) { i = t; j = a; k = zz; }
+  else { i = t; j = zz; k = a; }
+  return ((long long)k * g.n[1] + j) * g.n[0] + i;
+}
+
+// cp.async loads of one tile: primitives (+ old rhs/EMF values to accumulate into)
+template <int AX, bool DN>
+ECHO_D void issue_tile_loads(const GridP& g, const TileGeom& tg, long long tile, int t, int x,
+                             const double* __restrict__ P, const double* __restrict__ U, double* R, double* Om,
+                             unsigned sP, unsigned sA) {
+  int a0, t0, zz;
+  tile_origin<AX>(tg, tile, a0, t0, zz);
   const long long N = g.N;
-  const int na = g.n[AX];
-  // tile origin
-  const int a0 = (AX == 0 ? blockIdx.x : blockIdx.y) * TA;
-  const int t0 = (AX == 0 ? blockIdx.y : blockIdx.x) * NL;
-  const int TAX = (AX == 0) ? 1 : 0;  // array axis of the transverse (line) index
-  const int nt = g.n[TAX];
-  const int zz = blockIdx.z;          // the remaining axis index
-  // (along a, transverse t) -> (i, j, k)
-  auto cell = [&](int a, int t, int& i, int& j, int& k) {
-    if (AX == 0) { i = a; j = t; k = zz; }
-    else if (AX == 1) { i = t; j = a; k = zz; }
-    else { i = t; j = zz; k = a; }
-  };
-  const int bclo = g.bc[AX][0], bchi = g.bc[AX][1];
-
-  // ---- load: 8 primitives with the ghost rule as an index map (a1) ----
-  for (int it = tid; it < SZ_P; it += kSweepThreads) {
-    int v = it / (NL * LEN_P);
-    int r = it - v * (NL * LEN_P);
-    int t, m;
-    split<AX, LEN_P>(r, t, m);
-    int ag = map_index(a0 - kG + m, na, bclo, bchi);
-    int tg = min(t0 + t, nt - 1);
-    int i, j, k;
-    cell(ag, tg, i, j, k);
-    long long id = ((long long)k * g.n[1] + j) * g.n[0] + i;
-    double val;
-    if (v < 5) {
-      val = __ldg(P + v * N + id);
-    } else {
-      val = __ldg(U + v * N + id);
-      if (KS) val = val / __ldg(cen_rec(mt, i, j) + 16);
-    }
-    sP[v * (NL * LEN_P) + soff<AX, LEN_P>(t, m)] = val;
-  }
-  __syncthreads();
-
-  // ---- A: WENO5, both faces of each cell, per variable (a2) ----
-  for (int it = tid; it < 8 * NL * LEN_Q; it += kSweepThreads) {
-    int v = it / (NL * LEN_Q);
-    int r = it - v * (NL * LEN_Q);
-    int t, c;
-    split<AX, LEN_Q>(r, t, c);
-    const double* row = sP + v * (NL * LEN_P);
-    double um2 = row[soff<AX, LEN_P>(t, c)];
-    double um1 = row[soff<AX, LEN_P>(t, c + 1)];
-    double u0 = row[soff<AX, LEN_P>(t, c + 2)];
-    double up1 = row[soff<AX, LEN_P>(t, c + 3)];
-    double up2 = row[soff<AX, LEN_P>(t, c + 4)];
-    double qL, qR;
-    weno5_both<REC>(um2, um1, u0, up1, up2, qL, qR);
-    if (v == 0 || v == 4) {  // A25 positivity fallback
-      if (!(qL > 0.0)) qL = u0;
-      if (!(qR > 0.0)) qR = u0;
-    }
-    sQ[v * (NL * LEN_Q) + soff<AX, LEN_Q>(t, c)] = qL;
-    sQ[(8 + v) * (NL * LEN_Q) + soff<AX, LEN_Q>(t, c)] = qR;
-  }
-  __syncthreads();
-
-  // ---- B: one face per thread: states, speeds, HLL (a3) ----
-  {
-    int t, fa;
-    split<AX, NF>(tid, t, fa);
-    double pl[8], pr[8];
+  const int tt = min(t0 + t, tg.nt - 1);
 #pragma unroll
-    for (int v = 0; v < 8; v++) {
-      pl[v] = sQ[v * (NL * LEN_Q) + soff<AX, LEN_Q>(t, fa)];
-      pr[v] = sQ[(8 + v) * (NL * LEN_Q) + soff<AX, LEN_Q>(t, fa + 1)];
-    }
-    double F[7];
-    auto hll = [&](const auto& m) {
-      State sl, sr;
-      make_state(m, e, pl, sl);
-      make_state(m, e, pr, sr);
-      double uL[7], fL[7], uR[7], fR[7];
-      cons_flux(m, sl, AX, uL, fL);
-      cons_flux(m, sr, AX, uR, fR);
-      double lmL, lpL, lmR, lpR;
-      speeds(m, e, pl, sl, AX, lmL, lpL);
-      speeds(m, e, pr, sr, AX, lmR, lpR);
-      double sL = fmin(0.0, fmin(lmL, lmR));
-      double sR = fmax(0.0, fmax(lpL, lpR));
-      double den = sR - sL;
-      if (den > 0.0) {
-        double inv = m.sqrtg() / den;
-        double ss = sL * sR;
+  for (int pass = 0; pass < 2; pass++) {
+    const int m = x + pass * SLOT;
+    if (pass == 1 && m >= LEN_P) break;
+    const int ag = map_index(a0 - kG + m, tg.na, g.bc[AX][0], g.bc[AX][1]);
+    const long long id = lin_of<AX>(g, ag, tt, zz);
+    const unsigned s = sP + 8u * soff<AX, LEN_P>(t, m);
 #pragma unroll
-        for (int q = 0; q < 7; q++) F[q] = (sR * fL[q] - sL * fR[q] + ss * (uR[q] - uL[q])) * inv;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 7; q++) F[q] = 0.5 * (fL[q] + fR[q]) * m.sqrtg();
-      }
-    };
-    if (KS) {
-      int af = a0 - 3 + fa + 1;  // face af - 1/2
-      af = max(-kG, min(af, na + kG));
-      int tg = min(t0 + t, nt - 1);
-      const double* rec;
-      if (AX == 0) rec = f0_rec(mt, af, tg);
-      else if (AX == 1) rec = f1_rec(mt, tg, af);
-      else rec = cen_rec(mt, tg, zz);
-      hll(load_met(rec));
-    } else {
-      hll(FlatMet());
-    }
-    // sP is free since phase A (synchronised above); phase B reads only sQ
-#pragma unroll
-    for (int q = 0; q < 7; q++) sP[q * (NL * NF) + soff<AX, NF>(t, fa)] = F[q];
+    for (int v = 0; v < 8; v++) cp_async8(s + 8u * v * VP, (v < 5 ? P : U) + v * N + id);
   }
-  __syncthreads();
-
-  // ---- C1: DER flux derivative at faces a0-1/2 .. a0+TA-1/2 (a4) ----
-  for (int it = tid; it < 7 * NL * NH; it += kSweepThreads) {
-    int q = it / (NL * NH);
-    int r = it - q * (NL * NH);
-    int t, h;
-    split<AX, NH>(r, t, h);
-    const double* Fq = sP + q * (NL * NF);
-    double Hv = der5<DER>(Fq[soff<AX, NF>(t, h)], Fq[soff<AX, NF>(t, h + 1)], Fq[soff<AX, NF>(t, h + 2)],
-                          Fq[soff<AX, NF>(t, h + 3)], Fq[soff<AX, NF>(t, h + 4)]);
-    sQ[q * (NL * NH) + soff<AX, NH>(t, h)] = Hv;
+  if (AX != 0 && x < TA) {
+    const int a = min(a0 + x, tg.na - 1);
+    const long long id = lin_of<AX>(g, a, tt, zz);
+    const unsigned s = sA + 8u * soff<AX, TA>(t, x);
+#pragma unroll
+    for (int q = 0; q < 7; q++)
+      if (accumulates<AX, DN>(q)) cp_async8(s + 8u * q * VA, out_ptr<AX, DN>(q, R, Om, N) + id);
   }
-  __syncthreads();
+}
 
-  // ---- C2: flux differences into rhs; field-CD EMF (a5) ----
+template <int AX, bool KS, int DER, int REC, bool DN>
+__global__ void __launch_bounds__(kSweepThreads, kSweepBlocksPerSM)
+k_sweep(const GridP g, const EosP e, const MetTables mt, const TileGeom tg, const double* __restrict__ P,
+        const double* __restrict__ U, double* R, double* Om) {
+  extern __shared__ double smem[];
+  __shared__ unsigned char sRough[kSweepThreads];  // A31 flag of face x of line t
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const int tid = threadIdx.x;
+  const int t = (AX == 0) ? (tid >> 6) : (tid & 3);   // line
+  const int x = (AX == 0) ? (tid & 63) : (tid >> 2);  // slot along the line
+  const long long N = g.N;
   const double idxa = g.idx[AX];
-  for (int it = tid; it < 7 * NL * TA; it += kSweepThreads) {
-    int q = it / (NL * TA);
-    int r = it - q * (NL * TA);
-    int t, c;
-    split<AX, TA>(r, t, c);
-    int a = a0 + c, tg = t0 + t;
-    if (a >= na || tg >= nt) continue;
-    int i, j, k;
-    cell(a, tg, i, j, k);
-    long long id = ((long long)k * g.n[1] + j) * g.n[0] + i;
-    const double* Hq = sQ + q * (NL * NH);
-    double Hp = Hq[soff<AX, NH>(t, c + 1)], Hm = Hq[soff<AX, NH>(t, c)];
-    if (q < 5) {
-      double d = -(Hp - Hm) * idxa;
-      double* dst = R + q * N + id;
-      *dst = (AX == 0) ? d : (*dst + d);
-    } else {
-      const int b1 = (AX + 1) % 3, b2 = (AX + 2) % 3;
-      const int bc = (q == 5) ? b1 : b2;  // which B component this flux transports
-      if (DIVB_NONE) {
-        double d = -(Hp - Hm) * idxa;
-        double* dst = R + (5 + bc) * N + id;
-        *dst = (first_axis(bc) == AX) ? d : (*dst + d);
-      } else {
-        double hs = 0.25 * (Hp + Hm);
-        if (q == 5) {  // flux of B^{a+1} -> -1/4 into Omega_{a+2}
-          double* dst = Om + b2 * N + id;
-          *dst = (first_axis(b2) == AX) ? -hs : (*dst - hs);
-        } else {       // flux of B^{a+2} -> +1/4 into Omega_{a+1}
-          double* dst = Om + b1 * N + id;
-          *dst = (first_axis(b1) == AX) ? hs : (*dst + hs);
+
+  long long tile = blockIdx.x;
+  if (tile < tg.ntiles)
+    issue_tile_loads<AX, DN>(g, tg, tile, t, x, P, U, R, Om, sbase + 8u * OFF_P0, sbase + 8u * OFF_A0);
+  cp_async_commit();
+  for (int iter = 0; tile < tg.ntiles; iter++, tile += gridDim.x) {
+    const int cur = iter & 1;
+    const int offP = cur ? OFF_P1 : OFF_P0;
+    const int offA = cur ? OFF_A1 : OFF_A0;
+    const long long nxt = tile + gridDim.x;
+    if (nxt < tg.ntiles)
+      issue_tile_loads<AX, DN>(g, tg, nxt, t, x, P, U, R, Om, sbase + 8u * (cur ? OFF_P0 : OFF_P1),
+                               sbase + 8u * (cur ? OFF_A0 : OFF_A1));
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+
+    int a0, t0, zz;
+    tile_origin<AX>(tg, tile, a0, t0, zz);
+    const int tt = min(t0 + t, tg.nt - 1);
+
+    // ---- A: WENO5 of the 8 variables of reconstructed cell x (a2) ----
+    {
+      const double* row = smem + offP;
+      double isg[5];
+      if (KS) {  // B^i = (sqrt(g) B^i) / sqrt(g) of the (mapped) owned cell
+#pragma unroll
+        for (int m = 0; m < 5; m++) {
+          int ag = map_index(a0 - kG + x + m, tg.na, g.bc[AX][0], g.bc[AX][1]);
+          int ci = (AX == 0) ? ag : tt, cj = (AX == 0) ? tt : (AX == 1 ? ag : zz);
+          isg[m] = frcp(__ldg(cen_rec(mt, ci, cj) + 16));
         }
       }
+      bool rough = false;
+#pragma unroll 2
+      for (int v = 0; v < 8; v++) {
+        const double* r = row + v * VP;
+        double u[5];
+#pragma unroll
+        for (int m = 0; m < 5; m++) u[m] = r[soff<AX, LEN_P>(t, x + m)];
+        if (KS && v >= 5) {
+#pragma unroll
+          for (int m = 0; m < 5; m++) u[m] *= isg[m];
+        }
+        double qL, qR;
+        weno5_both<REC>(u[0], u[1], u[2], u[3], u[4], qL, qR);
+        if (v == 0 || v == 4) {
+          if (!(qL > 0.0)) qL = u[2];  // A25 positivity fallback
+          if (!(qR > 0.0)) qR = u[2];
+          // A31: face x joins cells x and x+1; a jump in rho or p switches DER off nearby
+          rough |= g.der_jump > 0.0 && fabs(u[3] - u[2]) > g.der_jump * fmin(u[2], u[3]);
+        }
+        smem[OFF_Q + v * VQ + soff<AX, LEN_Q>(t, x)] = qL;
+        smem[OFF_Q + (8 + v) * VQ + soff<AX, LEN_Q>(t, x)] = qR;
+      }
+      sRough[t * SLOT + x] = rough;
     }
+    __syncthreads();
+
+    // ---- B: face x (between reconstructed cells x and x+1): HLL (a3) ----
+    if (x < NF) {
+      double pl[8], pr[8];
+#pragma unroll
+      for (int v = 0; v < 8; v++) {
+        pl[v] = smem[OFF_Q + v * VQ + soff<AX, LEN_Q>(t, x)];
+        pr[v] = smem[OFF_Q + (8 + v) * VQ + soff<AX, LEN_Q>(t, x + 1)];
+      }
+      double F[7];
+      if (KS) {
+        int af = a0 - 3 + x + 1;  // face af - 1/2
+        af = max(-kG, min(af, tg.na + kG));
+        const double* rec;
+        if (AX == 0) rec = f0_rec(mt, af, tt);
+        else if (AX == 1) rec = f1_rec(mt, tt, af);
+        else rec = cen_rec(mt, tt, zz);
+        hll_face(load_met(rec), e, pl, pr, AX, F);
+      } else {
+        hll_face(FlatMet(), e, pl, pr, AX, F);
+      }
+      // the primitive buffer of this tile is free since phase A: it takes F
+#pragma unroll
+      for (int q = 0; q < 7; q++) smem[offP + q * VF + soff<AX, NF>(t, x)] = F[q];
+    }
+    __syncthreads();
+
+    // ---- C1: DER flux derivative at face x: faces a0-1/2 .. a0+TA-1/2 (a4) ----
+    if (x < NH) {
+      const unsigned char* rf = sRough + t * SLOT + x;
+      const bool plain = rf[0] | rf[1] | rf[2] | rf[3] | rf[4];  // A31: stencil crosses a jump
+#pragma unroll
+      for (int q = 0; q < 7; q++) {
+        const double* Fq = smem + offP + q * VF;
+        double Hv = plain ? Fq[soff<AX, NF>(t, x + 2)]
+                          : der5<DER>(Fq[soff<AX, NF>(t, x)], Fq[soff<AX, NF>(t, x + 1)], Fq[soff<AX, NF>(t, x + 2)],
+                                      Fq[soff<AX, NF>(t, x + 3)], Fq[soff<AX, NF>(t, x + 4)]);
+        smem[OFF_Q + q * VH + soff<AX, NH>(t, x)] = Hv;
+      }
+    }
+    __syncthreads();
+
+    // ---- C2: cell x: flux differences into rhs; field-CD EMF (a5) ----
+    if (x < TA && a0 + x < tg.na && t0 + t < tg.nt) {
+      const long long id = lin_of<AX>(g, a0 + x, t0 + t, zz);
+#pragma unroll
+      for (int q = 0; q < 7; q++) {
+        const double* Hq = smem + OFF_Q + q * VH;
+        const double Hp = Hq[soff<AX, NH>(t, x + 1)], Hm = Hq[soff<AX, NH>(t, x)];
+        double d;
+        if (q < 5 || DN) {
+          d = -(Hp - Hm) * idxa;
+        } else {
+          const double hs = 0.25 * (Hp + Hm);
+          d = (q == 5) ? -hs : hs;  // flux of B^{a+1} -> -1/4 Omega_{a+2}; of B^{a+2} -> +1/4 Omega_{a+1}
+        }
+        double* dst = out_ptr<AX, DN>(q, R, Om, N) + id;
+        *dst = accumulates<AX, DN>(q) ? (smem[offA + q * VA + soff<AX, TA>(t, x)] + d) : d;
+      }
+    }
+    __syncthreads();  // buffers of this tile are refilled by the next iteration's prefetch
   }
 }
 
@@ -221,17 +276,25 @@ template <int AX, bool KS, int DER, int REC, bool DN>
 static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* U,
                               double* R, double* Om, cudaStream_t st) {
   auto kern = k_sweep<AX, KS, DER, REC, DN>;
-  static bool attr = false;
-  if (!attr) {
+  static int grid_cap = 0;
+  if (!grid_cap) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
     if (err != cudaSuccess) return err;
-    attr = true;
+    int dev, sms, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kSweepThreads, kSweepSmem);
+    grid_cap = sms * (per > 0 ? per : 1);
   }
-  dim3 grid;
-  if (AX == 0) grid = dim3((g.n[0] + TA - 1) / TA, (g.n[1] + NL - 1) / NL, g.n[2]);
-  else if (AX == 1) grid = dim3((g.n[0] + NL - 1) / NL, (g.n[1] + TA - 1) / TA, g.n[2]);
-  else grid = dim3((g.n[0] + NL - 1) / NL, (g.n[2] + TA - 1) / TA, g.n[1]);
-  kern<<<grid, kSweepThreads, kSweepSmem, st>>>(g, e, mt, P, U, R, Om);
+  TileGeom tg;
+  tg.na = g.n[AX];
+  tg.nt = g.n[AX == 0 ? 1 : 0];
+  tg.ta_tiles = (tg.na + TA - 1) / TA;
+  tg.tt_tiles = (tg.nt + NL - 1) / NL;
+  const int nz = (AX == 2) ? g.n[1] : g.n[2];
+  tg.ntiles = (long long)tg.ta_tiles * tg.tt_tiles * nz;
+  unsigned blocks = (unsigned)(tg.ntiles < grid_cap ? tg.ntiles : grid_cap);
+  kern<<<blocks, kSweepThreads, kSweepSmem, st>>>(g, e, mt, tg, P, U, R, Om);
   return cudaGetLastError();
 }
 

@@ -54,20 +54,20 @@ ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* 
   double Z = (guess[0] + e.gfac * guess[4]) * (1.0 + gu[0] * gl[0] + gu[1] * gl[1] + gu[2] * gl[2]);
   bool polish = false, ok = false;
   for (int it = 1; it <= e.maxit; it++) {
-    const double iZ = 1.0 / Z;
+    const double iZ = frcp(Z);
     const double ZB = Z + B2;
-    const double iZB = 1.0 / ZB;
+    const double iZB = frcp(ZB);
     const double iZ2 = iZ * iZ, iZB2 = iZB * iZB;
     double v2 = (Z * Z * S2 + SB2 * (2.0 * Z + B2)) * iZ2 * iZB2;
     bool clamped = false;
     if (v2 > e.v2max) { v2 = e.v2max; clamped = true; }
-    const double sq = sqrt(1.0 - v2);
+    const double sq = fsqrt(1.0 - v2);
     const double p = e.gm * (Z * (1.0 - v2) - D * sq);
     const double f = Z - p + 0.5 * B2 * (1.0 + v2) - 0.5 * SB2 * iZ2 - Ut;
     const double dv2 = clamped ? 0.0 : -2.0 * iZB2 * iZB * (S2 + SB2 * (3.0 * Z * Z + 3.0 * Z * B2 + B2 * B2) * iZ2 * iZ);
-    const double dp = e.gm * ((1.0 - v2) - Z * dv2 + D * dv2 * (0.5 / sq));
+    const double dp = e.gm * ((1.0 - v2) - Z * dv2 + D * dv2 * (0.5 * frcp(sq)));
     const double df = 1.0 - dp + 0.5 * B2 * dv2 + SB2 * iZ2 * iZ;
-    double Zn = Z - f / df;
+    double Zn = Z - f * frcp(df);
     if (!(Zn > 0.0)) Zn = 0.5 * Z;
     const double dZ = fabs(Zn - Z);
     Z = Zn;
@@ -79,13 +79,13 @@ ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* 
     }
   }
   if (!ok) return 1;
-  const double iZ = 1.0 / Z;
+  const double iZ = frcp(Z);
   const double ZB = Z + B2;
-  const double iZB = 1.0 / ZB;
+  const double iZB = frcp(ZB);
   double v2 = (Z * Z * S2 + SB2 * (2.0 * Z + B2)) * (iZ * iZ) * (iZB * iZB);
   if (v2 > e.v2max) v2 = e.v2max;
-  const double sq = sqrt(1.0 - v2);
-  const double W = 1.0 / sq;
+  const double sq = fsqrt(1.0 - v2);
+  const double W = frcp(sq);
   out[0] = D * sq;
   out[4] = e.gm * (Z * (1.0 - v2) - D * sq);
   double vl[3], vu[3];
@@ -201,7 +201,7 @@ ECHO_D void add_sources(const GenMet& m, const double* __restrict__ dr, const Eo
 
 // -------------------------------------------------------------- K3 kernel
 template <bool KS, int MODE, bool DIVB_NONE>
-__global__ void __launch_bounds__(kCellThreads)
+__global__ void __launch_bounds__(kCellThreads, 3)
 k_update(const GridP g, const EosP e, const MetTables mt, const int s, const double dt, const double* __restrict__ R,
          const double* __restrict__ Om, const double* Un, const double* Us, double* Uout, double* P,
          double* __restrict__ Lout, unsigned long long* counters) {

@@ -30,7 +30,7 @@ METRIC_MINKOWSKI, METRIC_KERR_SCHILD = 0, 1
 
 class Grid(C.Structure):
     _fields_ = [("n", C.c_int * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("bc", (C.c_int * 2) * 3),
-                ("rec", C.c_int), ("der", C.c_int), ("divb", C.c_int)]
+                ("rec", C.c_int), ("der", C.c_int), ("divb", C.c_int), ("der_jump", C.c_double)]
 
 
 class Metric(C.Structure):
@@ -104,7 +104,7 @@ def _buf(a, writable=False):
     return a.data_ptr(), 1
 
 
-def _grid(n, lo, hi, bc, rec=0, der=6, divb=0) -> Grid:
+def _grid(n, lo, hi, bc, rec=0, der=6, divb=0, der_jump=0.5) -> Grid:
     g = Grid()
     for i in range(3):
         g.n[i] = int(n[i])
@@ -113,13 +113,14 @@ def _grid(n, lo, hi, bc, rec=0, der=6, divb=0) -> Grid:
         g.bc[i][0] = int(bc[i][0])
         g.bc[i][1] = int(bc[i][1])
     g.rec, g.der, g.divb = int(rec), int(der), int(divb)
+    g.der_jump = float(der_jump)
     return g
 
 
 # ------------------------------------------------------------- C names
 def create(n, lo, hi, bc, metric=METRIC_MINKOWSKI, M=1.0, a=0.0, gamma=4.0 / 3.0, rho_floor=1e-8, p_floor=1e-10,
-           w_max=50.0, c2p_max_iter=30, c2p_tol=1e-13, rec=0, der=6, divb=0):
-    g = _grid(n, lo, hi, bc, rec, der, divb)
+           w_max=50.0, c2p_max_iter=30, c2p_tol=1e-13, rec=0, der=6, divb=0, der_jump=0.5):
+    g = _grid(n, lo, hi, bc, rec, der, divb, der_jump)
     m = Metric(int(metric), float(M), float(a))
     e = Eos(float(gamma), float(rho_floor), float(p_floor), float(w_max), int(c2p_max_iter), float(c2p_tol))
     out = _P()

@@ -15,7 +15,8 @@ mp.mp.dps = 50
 
 
 class Grid:
-    def __init__(self, n, lo, hi, bc, metric=0, M=1, a=0, gamma=mp.mpf(4) / 3, rec=0, der=6, divb=0):
+    def __init__(self, n, lo, hi, bc, metric=0, M=1, a=0, gamma=mp.mpf(4) / 3, rec=0, der=6, divb=0, der_jump=0.5):
+        self.der_jump = der_jump
         self.n = list(n)
         self.lo = [mp.mpf(v) for v in lo]
         self.hi = [mp.mpf(v) for v in hi]
@@ -259,8 +260,12 @@ class Scheme:
         x = [G.centre(b, cell[b]) for b in range(3)]
         x[ax] = G.face(ax, cell[ax])
         F = hll(Met(G, x), G.gamma, qL, qR, ax)
-        self._face[key] = F
-        return F
+        # A31 jump flag of this face from the two cell-centre states it joins (fp64 inputs)
+        a, b = st[2], st[3]
+        dj = G.der_jump
+        rough = dj > 0 and (abs(b[0] - a[0]) > dj * min(a[0], b[0]) or abs(b[4] - a[4]) > dj * min(a[4], b[4]))
+        self._face[key] = (F, rough)
+        return self._face[key]
 
     def H(self, ax, cell):
         key = (ax, tuple(cell))
@@ -270,7 +275,10 @@ class Scheme:
                 cc = list(cell)
                 cc[ax] = cell[ax] - 2 + mm
                 Fs.append(self.face_flux(ax, cc))
-            self._H[key] = [derf([Fs[mm][q] for mm in range(5)], self.G.der) for q in range(8)]
+            if any(r for _, r in Fs):
+                self._H[key] = list(Fs[2][0])
+            else:
+                self._H[key] = [derf([Fs[mm][0][q] for mm in range(5)], self.G.der) for q in range(8)]
         return self._H[key]
 
     def axes(self, cell):

@@ -27,3 +27,18 @@ def assert_groups(got, ref, groups, tol, axis=0, what=""):
     bad = {k: v for k, v in errs.items() if not v <= tol}
     assert not bad, f"{what}: normwise group error above {tol:g}: {errs}"
     return errs
+
+
+def assert_rhs_groups(got, ref, U, dt, groups, tol, what=""):
+    """L comparisons (A16 for residuals): the group scale is max(max|L|, max|U|/dt), because
+    the L of a group near equilibrium is a truncation-level residual of cancelling flux
+    differences whose rounding scales with |U|/dt, not with |L|."""
+    got, ref, U = np.asarray(got), np.asarray(ref), np.asarray(U)
+    errs = {}
+    for name, idx in groups.items():
+        g, r, u = got[idx], ref[idx], U[idx]
+        scale = max(float(np.max(np.abs(r))), float(np.max(np.abs(u))) / dt)
+        errs[name] = float(np.max(np.abs(g - r))) / scale if scale > 0 else float(np.max(np.abs(g - r)))
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, f"{what}: rhs group error above {tol:g}: {errs}"
+    return errs
