@@ -21,10 +21,11 @@ using namespace echo;
 namespace {
 
 enum KernelClass {
-  kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kNumClasses
+  kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kLayout,
+  kNumClasses
 };
-const char* kNames[kNumClasses] = {"sweep_x", "sweep_y", "sweep_z", "update_stage", "update_rhs",
-                                   "con2prim",  "max_speed", "prim2cons", "get_prims"};
+const char* kNames[kNumClasses] = {"sweep_x", "sweep_y",   "sweep_z",   "update_stage", "update_rhs",
+                                   "con2prim", "max_speed", "prim2cons", "get_prims",    "layout"};
 
 std::string g_create_error;
 
@@ -36,12 +37,12 @@ struct echo_ctx {
   bool ks = false;
   MetTables mt{};
   double* tables = nullptr;
-  double* Un = nullptr;   // 8N
-  double* Us = nullptr;   // 8N
-  double* P = nullptr;    // 5N
-  double* R = nullptr;    // 8N
-  double* Om = nullptr;   // 3N
-  double* scratch = nullptr;  // 8N, lazily for host-buffer transfers
+  // cell-interleaved device state (echo_kernels.h): 8 doubles per cell each
+  double* Un = nullptr;   // U^n
+  double* Us = nullptr;   // U^s
+  double* P = nullptr;    // rho, u~, p, B
+  double* R = nullptr;    // rhs + EMF accumulator
+  double* scratch = nullptr;  // 8N, lazily for layout conversions / host-buffer transfers
   unsigned long long* dcnt = nullptr;  // [0] floors [1] failures [2] max speed bits
   long long* dbad = nullptr;
   unsigned long long* hpin = nullptr;  // pinned readback
@@ -101,11 +102,11 @@ static int ensure_scratch(echo_ctx* c) {
   return ECHO_OK;
 }
 
-// sweeps x, y, z of the current stage input (P, Ucur) into R, Om
-static int run_sweeps(echo_ctx* c, const double* Ucur) {
+// sweeps x, y, z of the current stage input P (B included) into R
+static int run_sweeps(echo_ctx* c) {
   for (int ax = 0; ax < 3; ax++) {
     cudaError_t e = launch(c, kSweepX + ax, [&] {
-      return launch_sweep(ax, c->ks, c->g, c->e, c->mt, c->P, Ucur, c->R, c->Om, c->st);
+      return launch_sweep(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
   }
@@ -114,12 +115,12 @@ static int run_sweeps(echo_ctx* c, const double* Ucur) {
 
 static int run_stage(echo_ctx* c, int s, double dt) {
   const double* Uin = (s == 1) ? c->Un : c->Us;
-  int rc = run_sweeps(c, Uin);
+  int rc = run_sweeps(c);
   if (rc) return rc;
   double* Uout = (s == 3) ? c->Un : c->Us;
   cudaError_t e = launch(c, kUpdateStage, [&] {
-    return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Om, c->Un, Uin, Uout, c->P,
-                         nullptr, c->dcnt, c->st);
+    return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Un, Uin, Uout, c->P, nullptr,
+                         c->dcnt, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
   c->stages++;
@@ -194,10 +195,13 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   e.tol = eos->c2p_tol;
   c->ks = ks;
 
-  const size_t N = (size_t)g.N;
+  // record rows: 8 n1 doubles + 8 (64 B) padding, so that row and plane strides
+  // are not powers of two (DRAM channel spread of the y/z pencils)
+  g.pitch = 8LL * g.n[0] + 8;
+  const size_t rec = (size_t)g.pitch * g.n[1] * g.n[2];  // doubles per record array
   auto alloc = [&](double** p, size_t nd) { return cudaMalloc(p, sizeof(double) * nd); };
-  if (alloc(&c->Un, 8 * N) != cudaSuccess || alloc(&c->Us, 8 * N) != cudaSuccess || alloc(&c->P, 5 * N) != cudaSuccess ||
-      alloc(&c->R, 8 * N) != cudaSuccess || alloc(&c->Om, 3 * N) != cudaSuccess ||
+  if (alloc(&c->Un, rec) != cudaSuccess || alloc(&c->Us, rec) != cudaSuccess || alloc(&c->P, rec) != cudaSuccess ||
+      alloc(&c->R, rec) != cudaSuccess ||
       cudaMalloc(&c->dcnt, 4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&c->dbad, sizeof(long long)) != cudaSuccess ||
       cudaMallocHost(&c->hpin, 4 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -206,8 +210,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     return fail(nullptr, ECHO_E_OOM, "echo_create: device allocation failed");
   }
   cudaMemset(c->dcnt, 0, 4 * sizeof(unsigned long long));
-  cudaMemset(c->R, 0, sizeof(double) * 8 * N);
-  cudaMemset(c->Om, 0, sizeof(double) * 3 * N);
+  cudaMemset(c->R, 0, sizeof(double) * rec);
   if (ks) {
     KsTables t;
     build_ks_tables(metric->M, metric->a, g.n, g.lo, g.dx, &t);
@@ -245,7 +248,6 @@ void echo_destroy(echo_ctx* c) {
   cudaFree(c->Us);
   cudaFree(c->P);
   cudaFree(c->R);
-  cudaFree(c->Om);
   cudaFree(c->scratch);
   cudaFree(c->dcnt);
   cudaFree(c->dbad);
@@ -313,7 +315,7 @@ int echo_get_prims(echo_ctx* c, double* p8, int on_device) {
     if (rc) return rc;
     dst = c->scratch;
   }
-  cudaError_t e = launch(c, kGetPrims, [&] { return launch_get_prims(c->ks, c->g, c->mt, c->P, ucur(c), dst, c->st); });
+  cudaError_t e = launch(c, kGetPrims, [&] { return launch_get_prims(c->ks, c->g, c->mt, c->P, dst, c->st); });
   if (e != cudaSuccess) return cuda_fail(c, e, "get_prims launch");
   if (!on_device) {
     CK(cudaMemcpyAsync(p8, c->scratch, sizeof(double) * 8 * c->g.N, cudaMemcpyDeviceToHost, c->st), "echo_get_prims");
@@ -322,34 +324,49 @@ int echo_get_prims(echo_ctx* c, double* p8, int on_device) {
   return ECHO_OK;
 }
 
-static int copy_field(echo_ctx* c, double* dst, const double* src, size_t nd, int on_device, const char* where) {
-  CK(cudaMemcpyAsync(dst, src, sizeof(double) * nd, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                     c->st), where);
-  if (!on_device) CK(cudaStreamSynchronize(c->st), where);
+// device record array [cell][8] -> caller array [q][cell] (first nq slots)
+static int export_field(echo_ctx* c, double* dst, const double* src, int nq, int on_device, const char* where) {
+  double* d = dst;
+  if (!on_device) {
+    int rc = ensure_scratch(c);
+    if (rc) return rc;
+    d = c->scratch;
+  }
+  CK(launch(c, kLayout, [&] { return launch_layout(c->g, src, d, nq, true, c->st); }), where);
+  if (!on_device) {
+    CK(cudaMemcpyAsync(dst, c->scratch, sizeof(double) * nq * c->g.N, cudaMemcpyDeviceToHost, c->st), where);
+    CK(cudaStreamSynchronize(c->st), where);
+  }
   return ECHO_OK;
 }
 
 int echo_get_cons(echo_ctx* c, double* u8, int on_device) {
   if (!c || !u8) return c ? fail(c, ECHO_E_ARG, "echo_get_cons: NULL buffer") : ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_get_cons: no state");
-  return copy_field(c, u8, ucur(c), 8 * (size_t)c->g.N, on_device, "echo_get_cons");
+  return export_field(c, u8, ucur(c), 8, on_device, "echo_get_cons");
 }
 
 int echo_get_state(echo_ctx* c, double* un8, double* us8, double* p5, int on_device) {
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_get_state: no state");
   int rc = ECHO_OK;
-  if (un8 && !rc) rc = copy_field(c, un8, c->Un, 8 * (size_t)c->g.N, on_device, "echo_get_state");
-  if (us8 && !rc) rc = copy_field(c, us8, c->Us, 8 * (size_t)c->g.N, on_device, "echo_get_state");
-  if (p5 && !rc) rc = copy_field(c, p5, c->P, 5 * (size_t)c->g.N, on_device, "echo_get_state");
+  if (un8 && !rc) rc = export_field(c, un8, c->Un, 8, on_device, "echo_get_state");
+  if (us8 && !rc) rc = export_field(c, us8, c->Us, 8, on_device, "echo_get_state");
+  if (p5 && !rc) rc = export_field(c, p5, c->P, 5, on_device, "echo_get_state");
   return rc;
 }
 
 int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
   if (!c || !u8) return c ? fail(c, ECHO_E_ARG, "echo_set_cons: NULL buffer") : ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_set_cons: needs a prior echo_set_prims (con2prim guess)");
-  CK(cudaMemcpyAsync(c->Un, u8, sizeof(double) * 8 * c->g.N,
-                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st), "echo_set_cons");
+  const double* src = u8;
+  if (!on_device) {
+    int rc = ensure_scratch(c);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->scratch, u8, sizeof(double) * 8 * c->g.N, cudaMemcpyHostToDevice, c->st), "echo_set_cons");
+    src = c->scratch;
+  }
+  CK(launch(c, kLayout, [&] { return launch_layout(c->g, src, c->Un, 8, false, c->st); }), "echo_set_cons");
   c->next_stage = 1;
   return echo_con2prim(c, nullptr);
 }
@@ -364,14 +381,17 @@ int echo_rhs(echo_ctx* c, double* l8, int on_device) {
     dst = c->scratch;
   }
   const double* U = ucur(c);
-  int rc = run_sweeps(c, U);
+  int rc = run_sweeps(c);
   if (rc) return rc;
   cudaError_t e = launch(c, kUpdateRhs, [&] {
-    return launch_update(kModeRhs, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, c->Om, U, U, nullptr, c->P, dst,
-                         c->dcnt, c->st);
+    return launch_update(kModeRhs, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, nullptr, c->P, dst, c->dcnt,
+                         c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update(rhs) launch");
-  if (!on_device) return copy_field(c, l8, c->scratch, 8 * (size_t)c->g.N, 0, "echo_rhs");
+  if (!on_device) {
+    CK(cudaMemcpyAsync(l8, c->scratch, sizeof(double) * 8 * c->g.N, cudaMemcpyDeviceToHost, c->st), "echo_rhs");
+    CK(cudaStreamSynchronize(c->st), "echo_rhs");
+  }
   return ECHO_OK;
 }
 
@@ -387,8 +407,7 @@ int echo_con2prim(echo_ctx* c, echo_stats_t* delta) {
   }
   double* U = ucur_mut(c);
   cudaError_t e = launch(c, kC2P, [&] {
-    return launch_update(kModeC2P, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, c->Om, U, U, U, c->P, nullptr, c->dcnt,
-                         c->st);
+    return launch_update(kModeC2P, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, U, c->P, nullptr, c->dcnt, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "con2prim launch");
   if (delta) {
@@ -432,7 +451,7 @@ int echo_max_dt(echo_ctx* c, double cfl, double* dt_out) {
   if (!(cfl > 0.0)) return fail(c, ECHO_E_ARG, "echo_max_dt: cfl > 0 violated");
   CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_max_dt");
   cudaError_t e = launch(c, kMaxSpeed, [&] {
-    return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, ucur(c), c->dcnt + 2, c->st);
+    return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, c->dcnt + 2, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "max_speed launch");
   CK(cudaMemcpyAsync(c->hpin + 2, c->dcnt + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_max_dt");

@@ -22,6 +22,7 @@ struct GridP {
   int bc[3][2];     // 0 periodic, 1 outflow
   int rec, der, divb;
   double der_jump;  // A31 DER shock switch (<= 0: off)
+  long long pitch;  // doubles per (j, k) row of a record array: 8 n1 + padding
 };
 
 struct EosP {
@@ -135,6 +136,20 @@ ECHO_D double frsqrt(double x) {
   return fma(y, e, y);
 }
 ECHO_D double fsqrt(double x) { return x > 0.0 ? x * frsqrt(x) : 0.0; }
+
+// ------------------------------------------------------- device layout
+// Every per-cell record (P, U, R: 8 doubles) is stored row-interleaved,
+// [k][j][var][i]: element (var, i, j, k) at ((k n2 + j) 8 + var) n1 + i.  x stays
+// unit-stride (coalesced, 16-B pairs), and one (j, k) row holds all 8 variables
+// (8 n1 doubles), so a z-pencil touches one 2 MB page per plane instead of 8.
+// Rows are padded to `pitch` doubles (>= 8 n1) so plane strides are not powers of two.
+ECHO_HD long long rec_base(const GridP& g, int i, int j, int k) {
+  return ((long long)k * g.n[1] + j) * g.pitch + i;
+}
+ECHO_HD long long rec_base_id(const GridP& g, long long id) {  // id = linear cell index (x fastest)
+  const long long r = id / g.n[0];
+  return r * g.pitch + (id - r * g.n[0]);
+}
 
 // --------------------------------------------------------------- indices
 ECHO_D int map_index(int i, int n, int bclo, int bchi) {  // ghost rule A12/A13
@@ -263,49 +278,54 @@ ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
 // Left state at i+1/2 and right state at i-1/2 from u[-2..2] of one cell and one
 // variable.  beta_k are shared by both faces; alpha_k = d_k/(eps+beta_k)^2 is
 // evaluated through the products s_l s_m so one division per face remains.
+// Arithmetic rearrangements (all exact in real arithmetic, rounding-level in fp64):
+//  * beta_k scaled by 12 (13 t^2 + 3 tb^2) with eps -> 12 eps: the weights only
+//    depend on ratios of (eps + beta_k)^2, so the common factor 144 cancels;
+//  * the ideal weights d_k and the candidates' 1/8 are folded into the candidate
+//    coefficients (all exact binary fractions for the point-value form).
 template <int REC>
 ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
-  const double eps = 1e-6;
-  const double c1312 = 13.0 / 12.0;
-  double t0 = um2 - 2.0 * um1 + u0, t0b = um2 - 4.0 * um1 + 3.0 * u0;
-  double t1 = um1 - 2.0 * u0 + up1, t1b = um1 - up1;
-  double t2 = u0 - 2.0 * up1 + up2, t2b = 3.0 * u0 - 4.0 * up1 + up2;
-  double b0 = c1312 * t0 * t0 + 0.25 * t0b * t0b;
-  double b1 = c1312 * t1 * t1 + 0.25 * t1b * t1b;
-  double b2 = c1312 * t2 * t2 + 0.25 * t2b * t2b;
-  double s0 = (eps + b0) * (eps + b0);
-  double s1 = (eps + b1) * (eps + b1);
-  double s2 = (eps + b2) * (eps + b2);
-  double p01 = s0 * s1, p02 = s0 * s2, p12 = s1 * s2;
-  double q0, q1, q2, r0, r1, r2, d0, d1, d2;
+  const double eps12 = 12.0e-6;
+  const double t0 = um2 - 2.0 * um1 + u0, t0b = um2 - 4.0 * um1 + 3.0 * u0;
+  const double t1 = um1 - 2.0 * u0 + up1, t1b = um1 - up1;
+  const double t2 = u0 - 2.0 * up1 + up2, t2b = 3.0 * u0 - 4.0 * up1 + up2;
+  double s0 = fma(13.0 * t0, t0, fma(3.0 * t0b, t0b, eps12));
+  double s1 = fma(13.0 * t1, t1, fma(3.0 * t1b, t1b, eps12));
+  double s2 = fma(13.0 * t2, t2, fma(3.0 * t2b, t2b, eps12));
+  s0 *= s0;
+  s1 *= s1;
+  s2 *= s2;
+  const double p01 = s0 * s1, p02 = s0 * s2, p12 = s1 * s2;
+  double Q0, Q1, Q2, R0, R1, R2, SL, SR;
   if (REC == 0) {
-    const double k = 0.125;
-    q0 = k * (3.0 * um2 - 10.0 * um1 + 15.0 * u0);
-    q1 = k * (-um1 + 6.0 * u0 + 3.0 * up1);
-    q2 = k * (3.0 * u0 + 6.0 * up1 - up2);
-    r0 = k * (3.0 * up2 - 10.0 * up1 + 15.0 * u0);
-    r1 = k * (-up1 + 6.0 * u0 + 3.0 * um1);
-    r2 = k * (3.0 * u0 + 6.0 * um1 - um2);
-    d0 = 1.0; d1 = 10.0; d2 = 5.0;
+    // d = (1, 10, 5)/16 on q_k = (3,-10,15)/8, (-1,6,3)/8, (3,6,-1)/8 (16 cancels)
+    Q0 = 0.375 * um2 - 1.25 * um1 + 1.875 * u0;
+    Q1 = -1.25 * um1 + 7.5 * u0 + 3.75 * up1;
+    Q2 = 1.875 * u0 + 3.75 * up1 - 0.625 * up2;
+    R0 = 0.375 * up2 - 1.25 * up1 + 1.875 * u0;
+    R1 = -1.25 * up1 + 7.5 * u0 + 3.75 * um1;
+    R2 = 1.875 * u0 + 3.75 * um1 - 0.625 * um2;
+    SL = fma(5.0, p01, fma(10.0, p02, p12));
+    SR = fma(5.0, p12, fma(10.0, p02, p01));
   } else {
+    // d = (1, 6, 3)/10 on q_k = (2,-7,11)/6, (-1,5,2)/6, (2,5,-1)/6 (10 cancels)
     const double k = 1.0 / 6.0;
-    q0 = k * (2.0 * um2 - 7.0 * um1 + 11.0 * u0);
-    q1 = k * (-um1 + 5.0 * u0 + 2.0 * up1);
-    q2 = k * (2.0 * u0 + 5.0 * up1 - up2);
-    r0 = k * (2.0 * up2 - 7.0 * up1 + 11.0 * u0);
-    r1 = k * (-up1 + 5.0 * u0 + 2.0 * um1);
-    r2 = k * (2.0 * u0 + 5.0 * um1 - um2);
-    d0 = 1.0; d1 = 6.0; d2 = 3.0;
+    Q0 = k * (2.0 * um2 - 7.0 * um1 + 11.0 * u0);
+    Q1 = -um1 + 5.0 * u0 + 2.0 * up1;
+    Q2 = u0 + 2.5 * up1 - 0.5 * up2;
+    R0 = k * (2.0 * up2 - 7.0 * up1 + 11.0 * u0);
+    R1 = -up1 + 5.0 * u0 + 2.0 * um1;
+    R2 = u0 + 2.5 * um1 - 0.5 * um2;
+    SL = fma(3.0, p01, fma(6.0, p02, p12));
+    SR = fma(3.0, p12, fma(6.0, p02, p01));
   }
-  // left: weights (d0/s0, d1/s1, d2/s2) ~ (d0 p12, d1 p02, d2 p01)
-  double wl0 = d0 * p12, wl1 = d1 * p02, wl2 = d2 * p01;
-  // right (mirror): r0 uses beta2, r1 beta1, r2 beta0 -> (d0 p01, d1 p02, d2 p12)
-  double wr0 = d0 * p01, wr1 = wl1, wr2 = d2 * p12;
+  // left: alpha_k ~ d_k / s_k ~ (p12, d1 p02, d2 p01); right (mirror): (p01, d1 p02, d2 p12)
+  const double NL = fma(p01, Q2, fma(p02, Q1, p12 * Q0));
+  const double NR = fma(p12, R2, fma(p02, R1, p01 * R0));
   // both normalisations through one reciprocal: 1/(SL SR)
-  const double SL = wl0 + wl1 + wl2, SR = wr0 + wr1 + wr2;
   const double inv = frcp(SL * SR);
-  qL = (wl0 * q0 + wl1 * q1 + wl2 * q2) * (SR * inv);
-  qR = (wr0 * r0 + wr1 * r1 + wr2 * r2) * (SL * inv);
+  qL = NL * (SR * inv);
+  qR = NR * (SL * inv);
 }
 
 // --------------------------------------------------------------- DER (A5)
