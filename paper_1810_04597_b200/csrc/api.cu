@@ -48,6 +48,7 @@ struct echo_ctx {
   unsigned long long* hpin = nullptr;  // pinned readback
   cudaStream_t st = nullptr;
   bool have_state = false;
+  bool cfl_valid = false;  // dcnt[2] holds the CFL max of the current state (fused into the last update)
   int next_stage = 1;
   unsigned long long steps = 0, stages = 0;
   long long launches = 0;
@@ -118,11 +119,15 @@ static int run_stage(echo_ctx* c, int s, double dt) {
   int rc = run_sweeps(c);
   if (rc) return rc;
   double* Uout = (s == 3) ? c->Un : c->Us;
+  // the last stage also reduces the CFL rate of the new state (a9 fused into K3)
+  unsigned long long* cfl = (s == 3) ? c->dcnt + 2 : nullptr;
+  if (cfl) CK(cudaMemsetAsync(cfl, 0, sizeof(unsigned long long), c->st), "stage");
   cudaError_t e = launch(c, kUpdateStage, [&] {
     return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Un, Uin, Uout, c->P, nullptr,
-                         c->dcnt, c->st);
+                         c->dcnt, cfl, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
+  c->cfl_valid = (s == 3);
   c->stages++;
   c->next_stage = (s == 3) ? 1 : s + 1;
   return ECHO_OK;
@@ -302,6 +307,7 @@ int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
     return fail(c, ECHO_E_UNPHYSICAL, buf);
   }
   c->have_state = true;
+  c->cfl_valid = false;
   c->next_stage = 1;
   return ECHO_OK;
 }
@@ -385,7 +391,7 @@ int echo_rhs(echo_ctx* c, double* l8, int on_device) {
   if (rc) return rc;
   cudaError_t e = launch(c, kUpdateRhs, [&] {
     return launch_update(kModeRhs, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, nullptr, c->P, dst, c->dcnt,
-                         c->st);
+                         nullptr, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update(rhs) launch");
   if (!on_device) {
@@ -406,10 +412,13 @@ int echo_con2prim(echo_ctx* c, echo_stats_t* delta) {
     before[1] = c->hpin[1];
   }
   double* U = ucur_mut(c);
+  CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_con2prim");
   cudaError_t e = launch(c, kC2P, [&] {
-    return launch_update(kModeC2P, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, U, c->P, nullptr, c->dcnt, c->st);
+    return launch_update(kModeC2P, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, U, c->P, nullptr, c->dcnt,
+                         c->dcnt + 2, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "con2prim launch");
+  c->cfl_valid = true;
   if (delta) {
     CK(cudaMemcpyAsync(c->hpin, c->dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_con2prim");
     CK(cudaStreamSynchronize(c->st), "echo_con2prim");
@@ -449,11 +458,14 @@ int echo_max_dt(echo_ctx* c, double cfl, double* dt_out) {
   if (!c || !dt_out) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_max_dt: no state");
   if (!(cfl > 0.0)) return fail(c, ECHO_E_ARG, "echo_max_dt: cfl > 0 violated");
-  CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_max_dt");
-  cudaError_t e = launch(c, kMaxSpeed, [&] {
-    return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, c->dcnt + 2, c->st);
-  });
-  if (e != cudaSuccess) return cuda_fail(c, e, "max_speed launch");
+  if (!c->cfl_valid) {  // otherwise the last update already reduced it for this state
+    CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_max_dt");
+    cudaError_t e = launch(c, kMaxSpeed, [&] {
+      return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, c->dcnt + 2, c->st);
+    });
+    if (e != cudaSuccess) return cuda_fail(c, e, "max_speed launch");
+    c->cfl_valid = true;
+  }
   CK(cudaMemcpyAsync(c->hpin + 2, c->dcnt + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "echo_max_dt");
   CK(cudaStreamSynchronize(c->st), "echo_max_dt");
   double m;

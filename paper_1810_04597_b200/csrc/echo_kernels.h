@@ -20,10 +20,11 @@ enum UpdateMode { kModeStage = 0, kModeRhs = 1, kModeC2P = 2 };
 
 // K3: sources + curl + RK combine + con2prim/floors (stage), or L(U) only into
 // Lout[var][cell] (rhs), or con2prim/floors of Un only (c2p).  counters[0]
-// floors, [1] failures.
+// floors, [1] failures.  cfl_out (may be NULL; zeroed by the caller): the CFL
+// max-speed reduction (a9) of the new state, fused into the same pass.
 cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                           const double* R, const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                          unsigned long long* counters, cudaStream_t st);
+                          unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st);
 
 // a9: per-cell sum_a max|lambda_a|/Delta_a, max-reduced into *out (u64 bit pattern, zeroed by caller)
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,

@@ -39,7 +39,7 @@ struct Geo {
   static constexpr int NL = (AX == 0) ? 4 : 8;  // lines per tile (y/z: 8 x-lines = 64 B rows)
   static constexpr int LOG_NL = (AX == 0) ? 2 : 3;
   static constexpr int THREADS = NL * SLOT;
-  static constexpr int BPS = (AX == 0) ? 2 : 1;  // CTAs per SM
+  static constexpr int BPS = (AX == 0) ? 3 : 1;  // CTAs per SM
   static constexpr int VP = NL * LEN_P;  // variable stride in the primitive buffer
   static constexpr int VQ = NL * LEN_Q;  // variable stride in the state buffer
   static constexpr int VF = NL * NF;     // component stride of F
@@ -199,7 +199,7 @@ k_sweep(const GridP g, const EosP e, const MetTables mt, const TileGeom tg, cons
     {
       const double* row = smem + offP;
       bool rough = false;
-#pragma unroll 2
+#pragma unroll 4
       for (int v = 0; v < 8; v++) {
         const double* r = row + v * GE::VP;
         double u[5];

@@ -28,22 +28,59 @@ ECHO_D void st8(double* p, long long vs, const double* o) {
 // MODE stage: U^{s+1} = RK(U^n, U^s, L) then con2prim/floors -> Uout, P.
 // MODE rhs:   L(U) into Lout ([var][cell], the C-ABI layout).
 // MODE c2p:   con2prim/floors of Un in place -> Un, P.
+// per-cell CFL rate sum_a max(|lambda+_a|, |lambda-_a|)/Delta_a (a9, A11) of prims pr (with B)
+template <class M>
+ECHO_D double cfl_rate(const M& m, const GridP& g, const EosP& e, const double* pr) {
+  State s;
+  make_state(m, e, pr, s);
+  double val = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    double lm, lp;
+    speeds(m, e, pr, s, a, lm, lp);
+    val += fmax(fabs(lp), fabs(lm)) * g.idx[a];
+  }
+  if (!(val == val)) val = __longlong_as_double(0x7ff0000000000000LL);  // NaN -> +inf (flagged on host)
+  return val;
+}
+
+// block max of v (all threads of the block call it) -> one atomicMax on the u64 bit pattern
+ECHO_D void block_max_atomic(double v, unsigned long long* out) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __shared__ double red[kCellThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bm = red[0];
+#pragma unroll
+    for (int w = 1; w < kCellThreads / 32; w++) bm = fmax(bm, red[w]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(bm));  // non-negative doubles order as u64
+  }
+}
+
 template <bool KS, int MODE, bool DIVB_NONE>
 __global__ void __launch_bounds__(kCellThreads, 3)
 k_update(const GridP g, const EosP e, const MetTables mt, const int s, const double dt, const double* __restrict__ R,
          const double* Un, const double* Us, double* Uout, double* P, double* __restrict__ Lout,
-         unsigned long long* counters) {
+         unsigned long long* counters, unsigned long long* cfl_out) {
   const long long N = g.N;
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = id < N;
   int ev = 0;
+  double rate = 0.0;
   if (active) {
     int i, j, k;
     cell_ijk(g, id, i, j, k);
     const auto m = MetAt<KS>::get(mt, i, j);
     const long long rb = rec_base(g, i, j, k), vs = g.n[0];
     double Pp[8];
-    ld8(P + rb, vs, Pp);  // rho, u~, p, B of the stage input
+    if (KS) {
+      ld8(P + rb, vs, Pp);  // rho, u~, p, B of the stage input (B for the sources)
+    } else {
+#pragma unroll
+      for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];  // the con2prim guess only
+    }
     double L[8];
     if (MODE != kModeC2P) {
       double Rv[8];
@@ -99,8 +136,10 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
       for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
       st8(Uout + rb, vs, Uo);
       st8(P + rb, vs, Po);
+      if (cfl_out) rate = cfl_rate(m, g, e, Po);  // a9 fused: CFL rate of the new state
     }
   }
+  if (cfl_out) block_max_atomic(rate, cfl_out);
   if (MODE != kModeRhs) {
     unsigned fl = __reduce_add_sync(0xffffffffu, ev == 1 ? 1u : 0u);
     unsigned fa = __reduce_add_sync(0xffffffffu, ev == 2 ? 1u : 0u);
@@ -114,29 +153,29 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
 template <bool KS, int MODE>
 static cudaError_t upd2(const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* R,
                         const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                        unsigned long long* cnt, cudaStream_t st) {
+                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st) {
   unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
   if (g.divb == 1)
-    k_update<KS, MODE, true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt);
+    k_update<KS, MODE, true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl);
   else
-    k_update<KS, MODE, false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt);
+    k_update<KS, MODE, false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl);
   return cudaGetLastError();
 }
 
 template <bool KS>
 static cudaError_t upd1(int mode, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* R,
                         const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                        unsigned long long* cnt, cudaStream_t st) {
-  if (mode == kModeRhs) return upd2<KS, kModeRhs>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, st);
-  if (mode == kModeC2P) return upd2<KS, kModeC2P>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, st);
-  return upd2<KS, kModeStage>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, st);
+                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st) {
+  if (mode == kModeRhs) return upd2<KS, kModeRhs>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, nullptr, st);
+  if (mode == kModeC2P) return upd2<KS, kModeC2P>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st);
+  return upd2<KS, kModeStage>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st);
 }
 
 cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                           const double* R, const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                          unsigned long long* counters, cudaStream_t st) {
-  if (ks) return upd1<true>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, st);
-  return upd1<false>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, st);
+                          unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st) {
+  if (ks) return upd1<true>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st);
+  return upd1<false>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st);
 }
 
 // ------------------------------------------------------ CFL reduction (a9)
@@ -152,27 +191,9 @@ k_max_speed(const GridP g, const EosP e, const MetTables mt, const double* __res
     const auto m = MetAt<KS>::get(mt, i, j);
     double pr[8];
     ld8(P + rec_base(g, i, j, k), g.n[0], pr);
-    State s;
-    make_state(m, e, pr, s);
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-      double lm, lp;
-      speeds(m, e, pr, s, a, lm, lp);
-      val += fmax(fabs(lp), fabs(lm)) * g.idx[a];
-    }
-    if (!(val == val)) val = __longlong_as_double(0x7ff0000000000000LL);  // NaN -> +inf (flagged on host)
+    val = cfl_rate(m, g, e, pr);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) val = fmax(val, __shfl_xor_sync(0xffffffffu, val, o));
-  __shared__ double red[kCellThreads / 32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = val;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double bm = red[0];
-#pragma unroll
-    for (int w = 1; w < kCellThreads / 32; w++) bm = fmax(bm, red[w]);
-    atomicMax(out, (unsigned long long)__double_as_longlong(bm));  // non-negative doubles order as u64
-  }
+  block_max_atomic(val, out);
 }
 
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
