@@ -92,18 +92,34 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
 #pragma unroll
         for (int c = 0; c < 3; c++) L[5 + c] = Rv[5 + c];
       } else {
-        // L(sqrt(g) B^c) = -D_{c+1} Omega_{c+2} + D_{c+2} Omega_{c+1}   (A6, A26)
+        // L(sqrt(g) B^c) = -D_{c+1} Omega_{c+2} + D_{c+2} Omega_{c+1}   (A6, A26).
+        // Neighbour offsets in the record layout with the ghost rule for a +-1
+        // step (periodic: wrap to the other end; outflow: the cell itself), branch free.
         const int ci[3] = {i, j, k};
-        auto om = [&](int comp, int ax, int d) {
-          int cc[3] = {ci[0], ci[1], ci[2]};
-          cc[ax] = map_index(cc[ax] + d, g.n[ax], g.bc[ax][0], g.bc[ax][1]);
-          return R[rec_base(g, cc[0], cc[1], cc[2]) + (5 + comp) * vs];
-        };
+        const long long stride[3] = {1, g.pitch, (long long)g.n[1] * g.pitch};
+        long long om_off[3][2];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          const long long wrap = (long long)(g.n[a] - 1) * stride[a];
+          om_off[a][0] = (ci[a] > 0) ? -stride[a] : (g.bc[a][0] == 0 ? wrap : 0);
+          om_off[a][1] = (ci[a] < g.n[a] - 1) ? stride[a] : (g.bc[a][1] == 0 ? -wrap : 0);
+        }
+        double onb[3][2][2];  // [axis][-/+][which of the two Omega components used along it]
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+          for (int sgn = 0; sgn < 2; sgn++) {
+            const double* base = R + rb + om_off[a][sgn];
+            onb[a][sgn][0] = base[(5 + (a + 1) % 3) * vs];  // Omega_{a+1}
+            onb[a][sgn][1] = base[(5 + (a + 2) % 3) * vs];  // Omega_{a+2}
+          }
 #pragma unroll
         for (int c = 0; c < 3; c++) {
           const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
-          L[5 + c] = -(om(a2, a1, 1) - om(a2, a1, -1)) * (0.5 * g.idx[a1]) +
-                     (om(a1, a2, 1) - om(a1, a2, -1)) * (0.5 * g.idx[a2]);
+          // Omega_{c+2} along a1 = c+1 is component (a1 + 1) % 3 -> index 0 of onb[a1];
+          // Omega_{c+1} along a2 = c+2 is component (a2 + 2) % 3 -> index 1 of onb[a2]
+          L[5 + c] = -(onb[a1][1][0] - onb[a1][0][0]) * (0.5 * g.idx[a1]) +
+                     (onb[a2][1][1] - onb[a2][0][1]) * (0.5 * g.idx[a2]);
         }
       }
     }
