@@ -33,7 +33,7 @@ UNIT = "zone-updates/s"
 BYTES_PER_ZONE_STEP = 752.0      # compulsory traffic per zone-update, DESIGN.md §7
 FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9  # SMs x FP64 lanes x 2 flop/FMA x max clock
 # algorithmic FP64 flops per cell of one sweep launch (Minkowski, DER6, WENO5 point form), DESIGN.md §7
-FLOPS_PER_CELL_SWEEP = 1129.0
+FLOPS_PER_CELL_SWEEP = 901.0
 
 
 def load_peaks():

@@ -236,9 +236,9 @@ ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* 
   const double den = sR - sL;
   if (den > 0.0) {
     const double inv = m.sqrtg() * frcp(den);
-    const double ss = sL * sR;
+    const double a = sR * inv, b = sL * inv, c = sL * sR * inv;
 #pragma unroll
-    for (int q = 0; q < 7; q++) F[q] = (sR * fL[q] - sL * fR[q] + ss * (uR[q] - uL[q])) * inv;
+    for (int q = 0; q < 7; q++) F[q] = fma(c, uR[q] - uL[q], fma(a, fL[q], -b * fR[q]));
   } else {
 #pragma unroll
     for (int q = 0; q < 7; q++) F[q] = 0.5 * (fL[q] + fR[q]) * m.sqrtg();
@@ -283,58 +283,68 @@ ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
 //    depend on ratios of (eps + beta_k)^2, so the common factor 144 cancels;
 //  * the ideal weights d_k and the candidates' 1/8 are folded into the candidate
 //    coefficients (all exact binary fractions for the point-value form).
+//  * everything is written in the first differences dmm = u_{-1}-u_{-2},
+//    dm = u_0-u_{-1}, dp = u_1-u_0, dpp = u_2-u_1: the second differences of the
+//    smoothness indicators are d2m = dm-dmm, d2c = dp-dm, d2p = dpp-dp, and
+//    (u_{-2} - 4u_{-1} + 3u_0) = d2m + 2dm, (u_{-1} - u_1) = -(dm + dp),
+//    (3u_0 - 4u_1 + u_2) = d2p - 2dp; since sum(omega) = 1 each face value is
+//    u_0 + sum_k omega_k (q_k - u_0) with the candidate increments q_k - u_0
+//    linear in the differences (2 flops each instead of 5).
 template <int REC>
 ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
   const double eps12 = 12.0e-6;
-  const double t0 = um2 - 2.0 * um1 + u0, t0b = um2 - 4.0 * um1 + 3.0 * u0;
-  const double t1 = um1 - 2.0 * u0 + up1, t1b = um1 - up1;
-  const double t2 = u0 - 2.0 * up1 + up2, t2b = 3.0 * u0 - 4.0 * up1 + up2;
-  double s0 = fma(13.0 * t0, t0, fma(3.0 * t0b, t0b, eps12));
-  double s1 = fma(13.0 * t1, t1, fma(3.0 * t1b, t1b, eps12));
-  double s2 = fma(13.0 * t2, t2, fma(3.0 * t2b, t2b, eps12));
+  const double dmm = um1 - um2, dm = u0 - um1, dp = up1 - u0, dpp = up2 - up1;
+  const double d2m = dm - dmm, d2c = dp - dm, d2p = dpp - dp;
+  const double t0b = fma(2.0, dm, d2m), t1b = dm + dp, t2b = fma(-2.0, dp, d2p);
+  double s0 = fma(13.0 * d2m, d2m, fma(3.0 * t0b, t0b, eps12));
+  double s1 = fma(13.0 * d2c, d2c, fma(3.0 * t1b, t1b, eps12));
+  double s2 = fma(13.0 * d2p, d2p, fma(3.0 * t2b, t2b, eps12));
   s0 *= s0;
   s1 *= s1;
   s2 *= s2;
   const double p01 = s0 * s1, p02 = s0 * s2, p12 = s1 * s2;
-  double Q0, Q1, Q2, R0, R1, R2, SL, SR;
+  double C0, C1, C2, E0, E1, E2, SL, SR;  // d_k (q_k - u0) for the left / right faces
   if (REC == 0) {
-    // d = (1, 10, 5)/16 on q_k = (3,-10,15)/8, (-1,6,3)/8, (3,6,-1)/8 (16 cancels)
-    Q0 = 0.375 * um2 - 1.25 * um1 + 1.875 * u0;
-    Q1 = -1.25 * um1 + 7.5 * u0 + 3.75 * up1;
-    Q2 = 1.875 * u0 + 3.75 * up1 - 0.625 * up2;
-    R0 = 0.375 * up2 - 1.25 * up1 + 1.875 * u0;
-    R1 = -1.25 * up1 + 7.5 * u0 + 3.75 * um1;
-    R2 = 1.875 * u0 + 3.75 * um1 - 0.625 * um2;
+    // point form, d = (1, 10, 5)/16 (the 16 cancels):
+    //   q0-u0 = (7dm - 3dmm)/8, q1-u0 = (dm + 3dp)/8, q2-u0 = (5dp - dpp)/8, right = mirror
+    C0 = fma(0.875, dm, -0.375 * dmm);
+    C1 = fma(1.25, dm, 3.75 * dp);
+    C2 = fma(3.125, dp, -0.625 * dpp);
+    E0 = fma(0.375, dpp, -0.875 * dp);
+    E1 = fma(-1.25, dp, -3.75 * dm);
+    E2 = fma(0.625, dmm, -3.125 * dm);
     SL = fma(5.0, p01, fma(10.0, p02, p12));
     SR = fma(5.0, p12, fma(10.0, p02, p01));
   } else {
-    // d = (1, 6, 3)/10 on q_k = (2,-7,11)/6, (-1,5,2)/6, (2,5,-1)/6 (10 cancels)
+    // finite-volume form, d = (1, 6, 3)/10 (the 10 cancels):
+    //   q0-u0 = (5dm - 2dmm)/6, q1-u0 = (dm + 2dp)/6, q2-u0 = (4dp - dpp)/6, right = mirror
     const double k = 1.0 / 6.0;
-    Q0 = k * (2.0 * um2 - 7.0 * um1 + 11.0 * u0);
-    Q1 = -um1 + 5.0 * u0 + 2.0 * up1;
-    Q2 = u0 + 2.5 * up1 - 0.5 * up2;
-    R0 = k * (2.0 * up2 - 7.0 * up1 + 11.0 * u0);
-    R1 = -up1 + 5.0 * u0 + 2.0 * um1;
-    R2 = u0 + 2.5 * um1 - 0.5 * um2;
+    C0 = k * fma(5.0, dm, -2.0 * dmm);
+    C1 = fma(1.0, dm, 2.0 * dp);
+    C2 = 0.5 * fma(4.0, dp, -dpp);
+    E0 = k * fma(2.0, dpp, -5.0 * dp);
+    E1 = fma(-1.0, dp, -2.0 * dm);
+    E2 = 0.5 * fma(-4.0, dm, dmm);
     SL = fma(3.0, p01, fma(6.0, p02, p12));
     SR = fma(3.0, p12, fma(6.0, p02, p01));
   }
   // left: alpha_k ~ d_k / s_k ~ (p12, d1 p02, d2 p01); right (mirror): (p01, d1 p02, d2 p12)
-  const double NL = fma(p01, Q2, fma(p02, Q1, p12 * Q0));
-  const double NR = fma(p12, R2, fma(p02, R1, p01 * R0));
+  const double NL = fma(p01, C2, fma(p02, C1, p12 * C0));
+  const double NR = fma(p12, E2, fma(p02, E1, p01 * E0));
   // both normalisations through one reciprocal: 1/(SL SR)
   const double inv = frcp(SL * SR);
-  qL = NL * (SR * inv);
-  qR = NR * (SL * inv);
+  qL = fma(NL, SR * inv, u0);
+  qR = fma(NR, SL * inv, u0);
 }
 
 // --------------------------------------------------------------- DER (A5)
+// H = F0 - d2F/24 + 3 d4F/640 collected by symmetric sums:
+//   H = (1067/960) F0 - (29/480)(F-1 + F+1) + (3/640)(F-2 + F+2)
 template <int DER>
 ECHO_D double der5(double Fm2, double Fm1, double F0, double Fp1, double Fp2) {
   if (DER == 6)
-    return F0 - (Fm1 - 2.0 * F0 + Fp1) * (1.0 / 24.0) +
-           (Fm2 - 4.0 * Fm1 + 6.0 * F0 - 4.0 * Fp1 + Fp2) * (3.0 / 640.0);
-  if (DER == 4) return F0 - (Fm1 - 2.0 * F0 + Fp1) * (1.0 / 24.0);
+    return fma(3.0 / 640.0, Fm2 + Fp2, fma(-29.0 / 480.0, Fm1 + Fp1, (1067.0 / 960.0) * F0));
+  if (DER == 4) return fma(-1.0 / 24.0, Fm1 + Fp1, (13.0 / 12.0) * F0);
   return F0;
 }
 
