@@ -105,9 +105,14 @@ static int ensure_scratch(echo_ctx* c) {
 
 // sweeps x, y, z of the current stage input P (B included) into R
 static int run_sweeps(echo_ctx* c) {
+  static const bool tiles = [] {
+    const char* s = getenv("ECHO_SWEEP");
+    return s && std::string(s) == "tile";
+  }();
   for (int ax = 0; ax < 3; ax++) {
     cudaError_t e = launch(c, kSweepX + ax, [&] {
-      return launch_sweep(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st);
+      return tiles ? launch_sweep(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st)
+                   : launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
   }

@@ -15,6 +15,10 @@ namespace echo {
 cudaError_t launch_sweep(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
                          double* R, cudaStream_t st);
 
+// the same sweep as a marching pipeline over whole lines (no tile-halo recomputation)
+cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
+                         double* R, cudaStream_t st);
+
 // K3 modes
 enum UpdateMode { kModeStage = 0, kModeRhs = 1, kModeC2P = 2 };
 

@@ -1,0 +1,376 @@
+// march.cu — the axis-sweep kernels K2x/K2y/K2z as a marching pipeline
+// (DESIGN.md §2 step 2, rows a1-a5; §7).
+//
+// A persistent CTA owns a group of NL lines (x sweep: 4 lines, 256 threads,
+// 3 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows, 512 threads,
+// 1 CTA/SM) and marches along the sweep axis in chunks of 64 cells.  Thread i
+// of a line handles, in chunk c (base B = 64c):
+//   A  WENO5 of reconstructed cell B+3+i (8 variables, both faces; a2) and the
+//      A31 jump flag of face B+3+i
+//   B  HLL flux at face B+2+i (a3): the left state comes from thread i-1
+//      (warp shuffle; across warps and chunks through a small edge buffer)
+//   C1 DER6 at face B+i from the F ring (a4)
+//   C2 flux difference + field-CD EMF of cell B+i (a5)
+// so every reconstruction, every face flux and every DER value is computed
+// exactly once per line: no tile halo is recomputed (the 6 cells / 5 faces /
+// 1 DER value of overlap are carried from the previous chunk), and every lane
+// is busy in every phase.  A prologue chunk c = -1 computes the carried values
+// of the line start.  Primitives stream through a 72-cell ring in shared
+// memory: the next chunk's 64 cells (or the next line group's first window) are
+// prefetched with cp.async as soon as phase A has consumed the current ones; the
+// ghost fill (a1) is the index map of those loads.  Results are bitwise
+// deterministic (fixed per-thread operation order).
+#include <cuda_runtime.h>
+
+#include "echo_dev.cuh"
+#include "echo_kernels.h"
+
+namespace echo {
+namespace march {
+
+constexpr int CH = 64;     // cells per chunk = threads per line
+constexpr int RING = 80;   // ring length for primitives and face fluxes (>= 74 live entries)
+constexpr int HB = CH + 1; // DER fluxes of a chunk (+ the carried one)
+
+template <int AX>
+struct Geo {
+  static constexpr int NL = (AX == 0) ? 4 : 8;
+  static constexpr int LOG_NL = (AX == 0) ? 2 : 3;
+  static constexpr int THREADS = NL * CH;
+  static constexpr int BPS = (AX == 0) ? 3 : 1;
+  static constexpr int DELTA = (AX == 0) ? 1 : NL;           // lane distance between slots i and i+1
+  static constexpr int SLOTS_PER_WARP = 32 / DELTA;           // consecutive slots inside one warp
+  static constexpr int NEDGE = CH / SLOTS_PER_WARP;           // warp-edge slots per line
+  static constexpr int VP = NL * RING;                        // variable stride, primitive ring
+  static constexpr int VF = NL * RING;                        // component stride, F ring
+  static constexpr int VH = NL * HB;                          // component stride, H buffer
+  static constexpr int VA = NL * CH;                          // component stride, accumulation buffer
+  static constexpr int VE = NL * NEDGE;                       // variable stride, edge buffer
+  static constexpr int OFF_P = 0;
+  static constexpr int OFF_F = OFF_P + 8 * VP;
+  static constexpr int OFF_H = OFF_F + 7 * VF;
+  static constexpr int OFF_A = OFF_H + 7 * VH;
+  static constexpr int OFF_E = OFF_A + ((AX == 0) ? 0 : 7 * VA);
+  static constexpr int TOTAL = OFF_E + 2 * 8 * VE;
+  static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RING;  // + A31 flag ring (bytes)
+};
+
+template <int AX, int LEN>
+ECHO_HD int loff(int t, int pos) {  // conflict-free: slot/position fastest for x, line fastest for y/z
+  return AX == 0 ? t * LEN + pos : pos * Geo<AX>::NL + t;
+}
+ECHO_HD int ringpos(int x) { return ((x % RING) + RING) % RING; }
+
+ECHO_HD int first_axis(int comp) { return comp == 0 ? 1 : 0; }
+template <int AX, bool DN>
+ECHO_HD bool accumulates(int q) {
+  if (q < 5) return AX != 0;
+  const int b1 = (AX + 1) % 3, b2 = (AX + 2) % 3;
+  if (DN) return first_axis(q == 5 ? b1 : b2) != AX;
+  return first_axis(q == 5 ? b2 : b1) != AX;
+}
+template <int AX, bool DN>
+ECHO_HD int out_slot(int q) {
+  if (q < 5) return q;
+  const int b1 = (AX + 1) % 3, b2 = (AX + 2) % 3;
+  if (DN) return 5 + (q == 5 ? b1 : b2);
+  return 5 + (q == 5 ? b2 : b1);
+}
+
+ECHO_D void cp_async8(unsigned saddr, const double* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gsrc));
+}
+ECHO_D void cp_async16(unsigned saddr, const double* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gsrc));
+}
+ECHO_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+ECHO_D void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+ECHO_D void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+struct LineGeom {
+  int na, nt, tt_groups, nz, nchunks;
+  int vec16;
+  long long nunits;
+};
+
+template <int AX>
+ECHO_D void unit_origin(const LineGeom& lg, long long unit, int& t0, int& zz) {
+  t0 = (int)(unit % lg.tt_groups) * Geo<AX>::NL;
+  zz = (int)(unit / lg.tt_groups);
+}
+
+template <int AX>
+ECHO_D long long base_of(const GridP& g, int a, int t, int zz) {
+  if (AX == 0) return rec_base(g, a, t, zz);
+  if (AX == 1) return rec_base(g, t, a, zz);
+  return rec_base(g, t, zz, a);
+}
+
+// cp.async of the primitives of cells [x0, x0 + cnt) of line t into the ring
+template <int AX>
+ECHO_D void load_cells(const GridP& g, const LineGeom& lg, int t0, int zz, int t, int x, bool vec,
+                       const double* __restrict__ P, unsigned sbase) {
+  using GE = Geo<AX>;
+  const int ag = map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
+  const int tt = min(t0 + t, lg.nt - 1);
+  const double* src = P + base_of<AX>(g, ag, tt, zz);
+  const long long vs = g.n[0];
+  const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, RING>(t, ringpos(x)));
+#pragma unroll
+  for (int v = 0; v < 8; v++) {
+    if (vec) cp_async16(s + 8u * v * GE::VP, src + v * vs);
+    else cp_async8(s + 8u * v * GE::VP, src + v * vs);
+  }
+}
+
+template <int AX, bool KS, int DER, int REC, bool DN>
+__global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
+k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
+        double* R) {
+  using GE = Geo<AX>;
+  extern __shared__ double smem[];
+  unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RING] face flags
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const int tid = threadIdx.x;
+  const int t = (AX == 0) ? (tid >> 6) : (tid & (GE::NL - 1));  // line in the group
+  const int i = (AX == 0) ? (tid & 63) : (tid >> GE::LOG_NL);    // slot along the line
+  const bool edge_in = (i % GE::SLOTS_PER_WARP) == 0;                            // left neighbour in another warp/chunk
+  const bool edge_out = (i % GE::SLOTS_PER_WARP) == GE::SLOTS_PER_WARP - 1;       // right neighbour in another warp/chunk
+  const double idxa = g.idx[AX];
+  const long long vs = g.n[0];
+
+  long long unit = blockIdx.x;
+  if (unit < lg.nunits) {  // first window [-5, 69) of the first line group
+    int t0, zz;
+    unit_origin<AX>(lg, unit, t0, zz);
+    const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
+    if (!(vec && (t & 1))) {
+      load_cells<AX>(g, lg, t0, zz, t, -kG + i, vec, P, sbase);
+      if (i < 10) load_cells<AX>(g, lg, t0, zz, t, -kG + CH + i, vec, P, sbase);
+    }
+  }
+  cp_async_commit();
+
+  for (; unit < lg.nunits; unit += gridDim.x) {
+    int t0, zz;
+    unit_origin<AX>(lg, unit, t0, zz);
+    const int tt = min(t0 + t, lg.nt - 1);
+    const bool line_ok = t0 + t < lg.nt;
+    const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
+    for (int c = -1; c < lg.nchunks; c++) {
+      const int B = c * CH;
+      const int par = (c + 2) & 1;
+      cp_async_wait0();
+      __syncthreads();  // primitives of this chunk landed; previous chunk fully consumed
+      if (AX != 0 && c >= 0) {  // old rhs/EMF values of the 64 output cells (needed in C2)
+        if (!(vec && (t & 1))) {
+          const int a = min(B + i, lg.na - 1);
+          const double* src = R + base_of<AX>(g, a, tt, zz);
+          const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
+#pragma unroll
+          for (int q = 0; q < 7; q++) {
+            if (!accumulates<AX, DN>(q)) continue;
+            if (vec) cp_async16(s + 8u * q * GE::VA, src + out_slot<AX, DN>(q) * vs);
+            else cp_async8(s + 8u * q * GE::VA, src + out_slot<AX, DN>(q) * vs);
+          }
+        }
+        cp_async_commit();
+      }
+
+      // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) ----
+      const int xr = B + 3 + i;
+      const bool a_on = (c >= 0) || (i >= CH - 6);  // the prologue needs cells -3..2 only
+      double qL[8] = {0, 0, 0, 0, 0, 0, 0, 0}, qR[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (a_on) {
+        bool rgh = false;
+        int pos[5];
+#pragma unroll
+        for (int m = 0; m < 5; m++) pos[m] = loff<AX, RING>(t, ringpos(xr - 2 + m));
+#pragma unroll
+        for (int v = 0; v < 8; v++) {
+          const double* r = smem + GE::OFF_P + v * GE::VP;
+          double u[5];
+#pragma unroll
+          for (int m = 0; m < 5; m++) u[m] = r[pos[m]];
+          weno5_both<REC>(u[0], u[1], u[2], u[3], u[4], qL[v], qR[v]);
+          if (v == 0 || v == 4) {
+            if (!(qL[v] > 0.0)) qL[v] = u[2];  // A25 positivity fallback
+            if (!(qR[v] > 0.0)) qR[v] = u[2];
+            // A31 flag of face xr (joins cells xr and xr+1)
+            rgh |= g.der_jump > 0.0 && fabs(u[3] - u[2]) > g.der_jump * fmin(u[2], u[3]);
+          }
+        }
+        rough[t * RING + ringpos(xr)] = rgh;
+        if (edge_out) {  // publish the left state of cell xr for the slot to the right
+          const int dpar = (i == CH - 1) ? ((c + 3) & 1) : par;
+          const int slot = ((i + 1) % CH) / GE::SLOTS_PER_WARP;
+#pragma unroll
+          for (int v = 0; v < 8; v++) smem[GE::OFF_E + dpar * 8 * GE::VE + v * GE::VE + t * GE::NEDGE + slot] = qL[v];
+        }
+      }
+      __syncthreads();  // A done: primitives of this chunk are dead, edges published
+
+      {  // prefetch: the next chunk's 64 new cells, or the next line group's first window
+         // (the prologue's window already holds chunk 0's cells)
+        if (c < 0) {
+        } else if (c + 1 < lg.nchunks) {
+          if (!(vec && (t & 1))) load_cells<AX>(g, lg, t0, zz, t, B + 69 + i, vec, P, sbase);
+        } else if (unit + gridDim.x < lg.nunits) {
+          int n0, nz;
+          unit_origin<AX>(lg, unit + gridDim.x, n0, nz);
+          const bool nvec = (AX != 0) && lg.vec16 && (n0 + GE::NL <= lg.nt);
+          if (!(nvec && (t & 1))) {
+            load_cells<AX>(g, lg, n0, nz, t, -kG + i, nvec, P, sbase);
+            if (i < 10) load_cells<AX>(g, lg, n0, nz, t, -kG + CH + i, nvec, P, sbase);
+          }
+        }
+        cp_async_commit();
+      }
+
+      // ---- B: face xf = B+2+i between reconstructed cells xf and xf+1 (a3) ----
+      {
+        double pl[8];
+#pragma unroll
+        for (int v = 0; v < 8; v++) pl[v] = __shfl_up_sync(0xffffffffu, qL[v], GE::DELTA);
+        if (edge_in) {
+          const int slot = i / GE::SLOTS_PER_WARP;
+#pragma unroll
+          for (int v = 0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + t * GE::NEDGE + slot];
+        }
+        const int xf = B + 2 + i;
+        const bool b_on = (c >= 0) || (i >= CH - 5);
+        if (b_on) {
+          double F[7];
+          if (KS) {
+            const int af = max(-kG, min(xf + 1, lg.na + kG));  // face af - 1/2
+            const double* rec;
+            if (AX == 0) rec = f0_rec(mt, af, tt);
+            else if (AX == 1) rec = f1_rec(mt, tt, af);
+            else rec = cen_rec(mt, tt, zz);
+            hll_face(load_met(rec), e, pl, qR, AX, F);
+          } else {
+            hll_face(FlatMet(), e, pl, qR, AX, F);
+          }
+          const int fp = loff<AX, RING>(t, ringpos(xf));
+#pragma unroll
+          for (int q = 0; q < 7; q++) smem[GE::OFF_F + q * GE::VF + fp] = F[q];
+        }
+      }
+      __syncthreads();  // F of faces B-2 .. B+65 present
+
+      // ---- C1: DER flux at face xh = B+i (a4); stored at H[i+1] ----
+      {
+        const int xh = B + i;
+        const bool c_on = (c >= 0) || (i == CH - 1);
+        if (c_on) {
+          int fpos[5];
+          bool plain = false;
+#pragma unroll
+          for (int m = 0; m < 5; m++) {
+            const int rp = ringpos(xh - 2 + m);
+            fpos[m] = loff<AX, RING>(t, rp);
+            plain |= rough[t * RING + rp] != 0;  // A31: the DER stencil crosses a jump
+          }
+          const int hp = loff<AX, HB>(t, i + 1);
+#pragma unroll
+          for (int q = 0; q < 7; q++) {
+            const double* Fq = smem + GE::OFF_F + q * GE::VF;
+            smem[GE::OFF_H + q * GE::VH + hp] =
+                plain ? Fq[fpos[2]] : der5<DER>(Fq[fpos[0]], Fq[fpos[1]], Fq[fpos[2]], Fq[fpos[3]], Fq[fpos[4]]);
+          }
+        }
+      }
+      if (AX != 0 && c >= 0) cp_async_wait1();  // the rhs/EMF values (all but the prefetch group)
+      __syncthreads();
+
+      // ---- C2: cell B+i: flux differences into rhs; field-CD EMF (a5) ----
+      if (c >= 0 && B + i < lg.na && line_ok) {
+        double* dst = R + base_of<AX>(g, B + i, t0 + t, zz);
+#pragma unroll
+        for (int q = 0; q < 7; q++) {
+          const double* Hq = smem + GE::OFF_H + q * GE::VH;
+          const double Hp = Hq[loff<AX, HB>(t, i + 1)], Hm = Hq[loff<AX, HB>(t, i)];
+          double d;
+          if (q < 5 || DN) {
+            d = -(Hp - Hm) * idxa;
+          } else {
+            const double hs = 0.25 * (Hp + Hm);
+            d = (q == 5) ? -hs : hs;
+          }
+          dst[out_slot<AX, DN>(q) * vs] =
+              accumulates<AX, DN>(q) ? (smem[GE::OFF_A + q * GE::VA + loff<AX, CH>(t, i)] + d) : d;
+        }
+      }
+      __syncthreads();
+      if (i < 7) {  // carry H(B+63) -> H[0] (the face B+64-1/2 of the next chunk)
+        smem[GE::OFF_H + i * GE::VH + loff<AX, HB>(t, 0)] = smem[GE::OFF_H + i * GE::VH + loff<AX, HB>(t, CH)];
+      }
+    }
+  }
+  cp_async_wait0();
+}
+
+template <int AX, bool KS, int DER, int REC, bool DN>
+static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+                              cudaStream_t st) {
+  using GE = Geo<AX>;
+  auto kern = k_march<AX, KS, DER, REC, DN>;
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GE::SMEM);
+    if (err != cudaSuccess) return err;
+    int dev, sms, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GE::THREADS, GE::SMEM);
+    grid_cap = sms * (per > 0 ? per : 1);
+  }
+  LineGeom lg;
+  lg.na = g.n[AX];
+  lg.nt = g.n[AX == 0 ? 1 : 0];
+  lg.tt_groups = (lg.nt + GE::NL - 1) / GE::NL;
+  lg.nz = (AX == 2) ? g.n[1] : g.n[2];
+  lg.nchunks = (lg.na + CH - 1) / CH;
+  lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
+  lg.nunits = (long long)lg.tt_groups * lg.nz;
+  unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
+  kern<<<blocks, GE::THREADS, GE::SMEM, st>>>(g, e, mt, lg, P, R);
+  return cudaGetLastError();
+}
+
+template <int AX, bool KS, int DER, int REC>
+static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+                             cudaStream_t st) {
+  if (g.divb == 1) return launch_one<AX, KS, DER, REC, true>(g, e, mt, P, R, st);
+  return launch_one<AX, KS, DER, REC, false>(g, e, mt, P, R, st);
+}
+template <int AX, bool KS, int DER>
+static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+                              cudaStream_t st) {
+  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, R, st);
+  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, R, st);
+}
+template <int AX, bool KS>
+static cudaError_t launch_der(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+                              cudaStream_t st) {
+  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, R, st);
+  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, R, st);
+  return launch_rec<AX, KS, 6>(g, e, mt, P, R, st);
+}
+
+}  // namespace march
+
+cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
+                         double* R, cudaStream_t st) {
+  using namespace march;
+  if (ks) {
+    if (axis == 0) return launch_der<0, true>(g, e, mt, P, R, st);
+    if (axis == 1) return launch_der<1, true>(g, e, mt, P, R, st);
+    return launch_der<2, true>(g, e, mt, P, R, st);
+  }
+  if (axis == 0) return launch_der<0, false>(g, e, mt, P, R, st);
+  if (axis == 1) return launch_der<1, false>(g, e, mt, P, R, st);
+  return launch_der<2, false>(g, e, mt, P, R, st);
+}
+
+}  // namespace echo
