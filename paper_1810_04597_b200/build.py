@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libecho_b200.so")
-SOURCES = ["sweep.cu", "march.cu", "update.cu", "api.cu", "metric_tables.cpp"]
+SOURCES = ["march.cu", "update.cu", "api.cu", "metric_tables.cpp"]
 HEADERS = ["echo_dev.cuh", "echo_kernels.h", "metric_tables.h", "cell_physics.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -29,14 +29,14 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src: str, verbose: bool, build_dir: str = BUILD, defines: tuple = ()) -> str:
+    obj = os.path.join(build_dir, os.path.basename(src) + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "echo.h")]
     if not _stale(obj, deps):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(BUILD, os.path.basename(src) + ".ptxas.log")
+    log = os.path.join(build_dir, os.path.basename(src) + ".ptxas.log")
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
@@ -46,22 +46,29 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines: tuple = ()) -> str:
+    """Build libecho_b200.so; a named `variant` (tuning runs only) builds
+    libecho_b200_<variant>.so with extra -D `defines` in its own object dir."""
+    build_dir = BUILD if not variant else BUILD + "_" + variant
+    lib = LIB if not variant else LIB.replace(".so", f"_{variant}.so")
+    os.makedirs(build_dir, exist_ok=True)
     if force:
-        for f in os.listdir(BUILD):
-            os.remove(os.path.join(BUILD, f))
+        for f in os.listdir(build_dir):
+            os.remove(os.path.join(build_dir, f))
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda s: _compile(s, verbose, build_dir, tuple(defines)), SOURCES))
+    if _stale(lib, objs):
+        tmp = lib + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    # python -m paper_1810_04597_b200.build [--force] [--verbose] [--variant NAME -DX=Y ...]
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    defs = tuple(a for a in sys.argv if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, variant=var, defines=defs))

@@ -1,6 +1,6 @@
 // api.cu — the C-ABI of include/echo.h: context, device allocations, stage
 // orchestration on one CUDA stream, CFL readback, counters, profiling.
-// Every step of the path runs in the kernels of sweep.cu / update.cu; this file
+// Every step of the path runs in the kernels of march.cu / update.cu; this file
 // only allocates, validates, launches and copies.
 #include <cuda_runtime.h>
 
@@ -105,14 +105,9 @@ static int ensure_scratch(echo_ctx* c) {
 
 // sweeps x, y, z of the current stage input P (B included) into R
 static int run_sweeps(echo_ctx* c) {
-  static const bool tiles = [] {
-    const char* s = getenv("ECHO_SWEEP");
-    return s && std::string(s) == "tile";
-  }();
   for (int ax = 0; ax < 3; ax++) {
     cudaError_t e = launch(c, kSweepX + ax, [&] {
-      return tiles ? launch_sweep(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st)
-                   : launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st);
+      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
   }

@@ -11,11 +11,8 @@
 
 namespace echo {
 
-// K2x/K2y/K2z: axis sweep (DESIGN §2 step 2): P -> R (x writes, y/z accumulate)
-cudaError_t launch_sweep(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                         double* R, cudaStream_t st);
-
-// the same sweep as a marching pipeline over whole lines (no tile-halo recomputation)
+// K2x/K2y/K2z: axis sweep (DESIGN §2 step 2): P -> R (x writes, y/z accumulate),
+// a marching pipeline over whole lines (no tile-halo recomputation)
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
                          double* R, cudaStream_t st);
 

@@ -1,10 +1,12 @@
 // march.cu — the axis-sweep kernels K2x/K2y/K2z as a marching pipeline
 // (DESIGN.md §2 step 2, rows a1-a5; §7).
 //
-// A persistent CTA owns a group of NL lines (x sweep: 4 lines, 256 threads,
-// 3 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows, 512 threads,
-// 1 CTA/SM) and marches along the sweep axis in chunks of 64 cells.  Thread i
-// of a line handles, in chunk c (base B = 64c):
+// A persistent CTA owns a group of NL lines (x sweep: 2 lines x 64 cells,
+// 128 threads, 6 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows x
+// 32 cells, 256 threads, 2 CTAs/SM — several CTAs per SM so that their phases
+// desynchronise and the FP64 pipe stays fed across the barriers) and marches
+// along the sweep axis in chunks of CH cells.  Thread i
+// of a line handles, in chunk c (base B = CH c):
 //   A  WENO5 of reconstructed cell B+3+i (8 variables, both faces; a2) and the
 //      A31 jump flag of face B+3+i
 //   B  HLL flux at face B+2+i (a3): the left state comes from thread i-1
@@ -15,8 +17,8 @@
 // exactly once per line: no tile halo is recomputed (the 6 cells / 5 faces /
 // 1 DER value of overlap are carried from the previous chunk), and every lane
 // is busy in every phase.  A prologue chunk c = -1 computes the carried values
-// of the line start.  Primitives stream through a 72-cell ring in shared
-// memory: the next chunk's 64 cells (or the next line group's first window) are
+// of the line start.  Primitives stream through a ring of >= CH + 10 cells in
+// shared memory: the next chunk's CH cells (or the next line group's first window) are
 // prefetched with cp.async as soon as phase A has consumed the current ones; the
 // ghost fill (a1) is the index map of those loads.  Results are bitwise
 // deterministic (fixed per-thread operation order).
@@ -28,16 +30,40 @@
 namespace echo {
 namespace march {
 
-constexpr int CH = 64;     // cells per chunk = threads per line
-constexpr int RING = 80;   // ring length for primitives and face fluxes (>= 74 live entries)
-constexpr int HB = CH + 1; // DER fluxes of a chunk (+ the carried one)
+// Line-group geometry per sweep axis: NL lines x CH cells per chunk
+// (THREADS = NL CH), BPS CTAs per SM.  Overridable at build time for tuning
+// runs (-DECHO_YZ_NL=8 -DECHO_YZ_CH=32 -DECHO_YZ_BPS=2, likewise ECHO_X_*).
+#ifndef ECHO_X_NL
+#define ECHO_X_NL 2
+#define ECHO_X_CH 64
+#define ECHO_X_BPS 6
+#endif
+#ifndef ECHO_YZ_NL
+#define ECHO_YZ_NL 8
+#define ECHO_YZ_CH 32
+#define ECHO_YZ_BPS 2
+#endif
+struct GeomSpec {
+  int nl, ch, bps;
+};
+constexpr GeomSpec kGeomX{ECHO_X_NL, ECHO_X_CH, ECHO_X_BPS};
+constexpr GeomSpec kGeomYZ{ECHO_YZ_NL, ECHO_YZ_CH, ECHO_YZ_BPS};
+
+constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+constexpr bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 template <int AX>
 struct Geo {
-  static constexpr int NL = (AX == 0) ? 4 : 8;
-  static constexpr int LOG_NL = (AX == 0) ? 2 : 3;
+  static constexpr GeomSpec S = (AX == 0) ? kGeomX : kGeomYZ;
+  static constexpr int NL = S.nl;
+  static constexpr int CH = S.ch;                             // cells per chunk = threads per line
+  static constexpr int LOG_NL = ilog2(NL);
+  static constexpr int LOG_CH = ilog2(CH);
+  // ring length for primitives and face fluxes: >= CH + 10 live entries (a power of two when cheap)
+  static constexpr int RING = (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
+  static constexpr int HB = CH + 1;                           // DER fluxes of a chunk (+ the carried one)
   static constexpr int THREADS = NL * CH;
-  static constexpr int BPS = (AX == 0) ? 3 : 1;
+  static constexpr int BPS = S.bps;
   static constexpr int DELTA = (AX == 0) ? 1 : NL;           // lane distance between slots i and i+1
   static constexpr int SLOTS_PER_WARP = 32 / DELTA;           // consecutive slots inside one warp
   static constexpr int NEDGE = CH / SLOTS_PER_WARP;           // warp-edge slots per line
@@ -53,13 +79,25 @@ struct Geo {
   static constexpr int OFF_E = OFF_A + ((AX == 0) ? 0 : 7 * VA);
   static constexpr int TOTAL = OFF_E + 2 * 8 * VE;
   static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RING;  // + A31 flag ring (bytes)
+  static_assert(is_pow2(NL) && is_pow2(CH), "NL and CH must be powers of two");
+  static_assert(CH >= 16 && THREADS <= 1024 && (AX == 0 ? CH >= 32 : NL <= 32), "unsupported line geometry");
+  static_assert(AX != 0 || NL * CH <= 1024, "x geometry");
+  // a ring position of cell/face x (x may be negative)
+  static ECHO_HD int ring(int x) {
+    if constexpr (is_pow2(RING)) return x & (RING - 1);
+    else return ((x % RING) + RING) % RING;
+  }
+  // ring position rb + d for a chunk base position rb in [0, RING) and -RING <= d < RING
+  static ECHO_HD int wrap(int p) {
+    if constexpr (is_pow2(RING)) return p & (RING - 1);
+    else return p >= RING ? p - RING : (p < 0 ? p + RING : p);
+  }
 };
 
 template <int AX, int LEN>
 ECHO_HD int loff(int t, int pos) {  // conflict-free: slot/position fastest for x, line fastest for y/z
   return AX == 0 ? t * LEN + pos : pos * Geo<AX>::NL + t;
 }
-ECHO_HD int ringpos(int x) { return ((x % RING) + RING) % RING; }
 
 ECHO_HD int first_axis(int comp) { return comp == 0 ? 1 : 0; }
 template <int AX, bool DN>
@@ -106,7 +144,7 @@ ECHO_D long long base_of(const GridP& g, int a, int t, int zz) {
   return rec_base(g, t, zz, a);
 }
 
-// cp.async of the primitives of cells [x0, x0 + cnt) of line t into the ring
+// cp.async of the primitives of cells x of line t into the ring
 template <int AX>
 ECHO_D void load_cells(const GridP& g, const LineGeom& lg, int t0, int zz, int t, int x, bool vec,
                        const double* __restrict__ P, unsigned sbase) {
@@ -115,7 +153,7 @@ ECHO_D void load_cells(const GridP& g, const LineGeom& lg, int t0, int zz, int t
   const int tt = min(t0 + t, lg.nt - 1);
   const double* src = P + base_of<AX>(g, ag, tt, zz);
   const long long vs = g.n[0];
-  const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, RING>(t, ringpos(x)));
+  const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, GE::RING>(t, GE::ring(x)));
 #pragma unroll
   for (int v = 0; v < 8; v++) {
     if (vec) cp_async16(s + 8u * v * GE::VP, src + v * vs);
@@ -123,32 +161,38 @@ ECHO_D void load_cells(const GridP& g, const LineGeom& lg, int t0, int zz, int t
   }
 }
 
+// the first window [-5, CH + 5) of a line group (cells -5..4 feed the prologue chunk)
+template <int AX>
+ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int t, int i,
+                        const double* __restrict__ P, unsigned sbase) {
+  using GE = Geo<AX>;
+  int t0, zz;
+  unit_origin<AX>(lg, unit, t0, zz);
+  const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
+  if (vec && (t & 1)) return;
+  load_cells<AX>(g, lg, t0, zz, t, -kG + i, vec, P, sbase);
+  if (i < 2 * kG) load_cells<AX>(g, lg, t0, zz, t, -kG + GE::CH + i, vec, P, sbase);
+}
+
 template <int AX, bool KS, int DER, int REC, bool DN>
 __global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         double* R) {
   using GE = Geo<AX>;
+  constexpr int CH = GE::CH, RING = GE::RING, HB = GE::HB;
   extern __shared__ double smem[];
   unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RING] face flags
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const int tid = threadIdx.x;
-  const int t = (AX == 0) ? (tid >> 6) : (tid & (GE::NL - 1));  // line in the group
-  const int i = (AX == 0) ? (tid & 63) : (tid >> GE::LOG_NL);    // slot along the line
+  const int t = (AX == 0) ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));  // line in the group
+  const int i = (AX == 0) ? (tid & (CH - 1)) : (tid >> GE::LOG_NL);      // slot along the line
   const bool edge_in = (i % GE::SLOTS_PER_WARP) == 0;                            // left neighbour in another warp/chunk
   const bool edge_out = (i % GE::SLOTS_PER_WARP) == GE::SLOTS_PER_WARP - 1;       // right neighbour in another warp/chunk
   const double idxa = g.idx[AX];
   const long long vs = g.n[0];
 
   long long unit = blockIdx.x;
-  if (unit < lg.nunits) {  // first window [-5, 69) of the first line group
-    int t0, zz;
-    unit_origin<AX>(lg, unit, t0, zz);
-    const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
-    if (!(vec && (t & 1))) {
-      load_cells<AX>(g, lg, t0, zz, t, -kG + i, vec, P, sbase);
-      if (i < 10) load_cells<AX>(g, lg, t0, zz, t, -kG + CH + i, vec, P, sbase);
-    }
-  }
+  if (unit < lg.nunits) load_window<AX>(g, lg, unit, t, i, P, sbase);
   cp_async_commit();
 
   for (; unit < lg.nunits; unit += gridDim.x) {
@@ -157,12 +201,13 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
     const int tt = min(t0 + t, lg.nt - 1);
     const bool line_ok = t0 + t < lg.nt;
     const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
-    for (int c = -1; c < lg.nchunks; c++) {
+    int rb = GE::ring(-CH);  // ring position of the chunk base B
+    for (int c = -1; c < lg.nchunks; c++, rb = GE::wrap(rb + CH)) {
       const int B = c * CH;
       const int par = (c + 2) & 1;
       cp_async_wait0();
       __syncthreads();  // primitives of this chunk landed; previous chunk fully consumed
-      if (AX != 0 && c >= 0) {  // old rhs/EMF values of the 64 output cells (needed in C2)
+      if (AX != 0 && c >= 0) {  // old rhs/EMF values of the CH output cells (needed in C2)
         if (!(vec && (t & 1))) {
           const int a = min(B + i, lg.na - 1);
           const double* src = R + base_of<AX>(g, a, tt, zz);
@@ -178,14 +223,14 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       }
 
       // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) ----
-      const int xr = B + 3 + i;
+      const int rr = GE::wrap(rb + 3 + i);  // ring position of xr
       const bool a_on = (c >= 0) || (i >= CH - 6);  // the prologue needs cells -3..2 only
       double qL[8] = {0, 0, 0, 0, 0, 0, 0, 0}, qR[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (a_on) {
         bool rgh = false;
         int pos[5];
 #pragma unroll
-        for (int m = 0; m < 5; m++) pos[m] = loff<AX, RING>(t, ringpos(xr - 2 + m));
+        for (int m = 0; m < 5; m++) pos[m] = loff<AX, RING>(t, GE::wrap(rr - 2 + m));
 #pragma unroll
         for (int v = 0; v < 8; v++) {
           const double* r = smem + GE::OFF_P + v * GE::VP;
@@ -200,29 +245,23 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
             rgh |= g.der_jump > 0.0 && fabs(u[3] - u[2]) > g.der_jump * fmin(u[2], u[3]);
           }
         }
-        rough[t * RING + ringpos(xr)] = rgh;
+        rough[t * RING + rr] = rgh;
         if (edge_out) {  // publish the left state of cell xr for the slot to the right
           const int dpar = (i == CH - 1) ? ((c + 3) & 1) : par;
-          const int slot = ((i + 1) % CH) / GE::SLOTS_PER_WARP;
+          const int slot = ((i + 1) & (CH - 1)) / GE::SLOTS_PER_WARP;
 #pragma unroll
           for (int v = 0; v < 8; v++) smem[GE::OFF_E + dpar * 8 * GE::VE + v * GE::VE + t * GE::NEDGE + slot] = qL[v];
         }
       }
       __syncthreads();  // A done: primitives of this chunk are dead, edges published
 
-      {  // prefetch: the next chunk's 64 new cells, or the next line group's first window
+      {  // prefetch: the next chunk's CH new cells, or the next line group's first window
          // (the prologue's window already holds chunk 0's cells)
         if (c < 0) {
         } else if (c + 1 < lg.nchunks) {
-          if (!(vec && (t & 1))) load_cells<AX>(g, lg, t0, zz, t, B + 69 + i, vec, P, sbase);
+          if (!(vec && (t & 1))) load_cells<AX>(g, lg, t0, zz, t, B + CH + kG + i, vec, P, sbase);
         } else if (unit + gridDim.x < lg.nunits) {
-          int n0, nz;
-          unit_origin<AX>(lg, unit + gridDim.x, n0, nz);
-          const bool nvec = (AX != 0) && lg.vec16 && (n0 + GE::NL <= lg.nt);
-          if (!(nvec && (t & 1))) {
-            load_cells<AX>(g, lg, n0, nz, t, -kG + i, nvec, P, sbase);
-            if (i < 10) load_cells<AX>(g, lg, n0, nz, t, -kG + CH + i, nvec, P, sbase);
-          }
+          load_window<AX>(g, lg, unit + gridDim.x, t, i, P, sbase);
         }
         cp_async_commit();
       }
@@ -251,23 +290,22 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           } else {
             hll_face(FlatMet(), e, pl, qR, AX, F);
           }
-          const int fp = loff<AX, RING>(t, ringpos(xf));
+          const int fp = loff<AX, RING>(t, GE::wrap(rr - 1));
 #pragma unroll
           for (int q = 0; q < 7; q++) smem[GE::OFF_F + q * GE::VF + fp] = F[q];
         }
       }
-      __syncthreads();  // F of faces B-2 .. B+65 present
+      __syncthreads();  // F of faces B-2 .. B+CH+1 present
 
       // ---- C1: DER flux at face xh = B+i (a4); stored at H[i+1] ----
       {
-        const int xh = B + i;
         const bool c_on = (c >= 0) || (i == CH - 1);
         if (c_on) {
           int fpos[5];
           bool plain = false;
 #pragma unroll
           for (int m = 0; m < 5; m++) {
-            const int rp = ringpos(xh - 2 + m);
+            const int rp = GE::wrap(rr - 5 + m);  // xh - 2 + m = xr - 5 + m
             fpos[m] = loff<AX, RING>(t, rp);
             plain |= rough[t * RING + rp] != 0;  // A31: the DER stencil crosses a jump
           }
@@ -302,7 +340,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         }
       }
       __syncthreads();
-      if (i < 7) {  // carry H(B+63) -> H[0] (the face B+64-1/2 of the next chunk)
+      if (i < 7) {  // carry H(B+CH-1) -> H[0] (the face B+CH-1/2 of the next chunk)
         smem[GE::OFF_H + i * GE::VH + loff<AX, HB>(t, 0)] = smem[GE::OFF_H + i * GE::VH + loff<AX, HB>(t, CH)];
       }
     }
@@ -330,7 +368,7 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
   lg.nt = g.n[AX == 0 ? 1 : 0];
   lg.tt_groups = (lg.nt + GE::NL - 1) / GE::NL;
   lg.nz = (AX == 2) ? g.n[1] : g.n[2];
-  lg.nchunks = (lg.na + CH - 1) / CH;
+  lg.nchunks = (lg.na + GE::CH - 1) / GE::CH;
   lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
   lg.nunits = (long long)lg.tt_groups * lg.nz;
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);

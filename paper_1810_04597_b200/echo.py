@@ -16,7 +16,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libecho_b200.so")
+# ECHO_LIB_VARIANT=<name> loads libecho_b200_<name>.so (a tuning build, build.py --variant)
+_VAR = os.environ.get("ECHO_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, "libecho_b200.so" if not _VAR else f"libecho_b200_{_VAR}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1810_04597_b200.build` "

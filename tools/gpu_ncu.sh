@@ -5,5 +5,5 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/fp64_peak.cu -o /tmp/fp64
 python -m paper_1810_04597_b200.build > gpurun_out/build.log 2>&1
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu --n 256 256 256"
 $CMD > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_sweep|k_update" -c 4 -o gpurun_out/prof_sweep $CMD > gpurun_out/ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_march|k_update" -c 4 -o gpurun_out/prof_sweep $CMD > gpurun_out/ncu.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu.log

@@ -11,6 +11,6 @@ $CMD > gpurun_out/bench_small.json 2> gpurun_out/bench_small.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD \
   > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?" >> gpurun_out/ncu_launches.log
-ncu --set full --clock-control none --import-source on -k regex:"k_sweep|k_update" -c 4 \
+ncu --set full --clock-control none --import-source on -k regex:"k_march|k_update" -c 4 \
   -o gpurun_out/prof_round $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/ncu_full.log

@@ -64,7 +64,10 @@ def main(tag):
                 "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
                 "smsp__issue_active.avg.pct_of_peak_sustained_active",
                 "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
-                "smsp__inst_executed.sum"]
+                "smsp__inst_executed.sum",
+                "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+                "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                "smsp__thread_inst_executed_per_inst_executed.ratio"]
         sweeps = []
         with open(os.path.join(PROF, f"{tag}_kernels.txt"), "w") as f:
             f.write("ncu --set full --clock-control none, 512^3 config 3 (bench workload), first stage\n")
@@ -82,7 +85,7 @@ def main(tag):
                         except ValueError:
                             pass
                 f.write("   stalls/issue: " + ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:8]) + "\n")
-                if "k_sweep" in name:
+                if "k_sweep" in name or "k_march" in name:
                     def val(k):
                         u = units[ix[k]]
                         v = float(d[ix[k]].replace(",", ""))
