@@ -13,6 +13,14 @@ namespace echo {
 
 constexpr int kG = 5;  // halo: WENO5 (3) + DER6 (2), A12
 
+// FP64 constants that are not exact in a 32-bit-high-word immediate live in the
+// constant bank, so every DFMA takes them as a c[][] operand (otherwise the
+// compiler rebuilds each one with a pair of UMOVs at every use).
+//   [0..2] DER6 symmetric-sum weights 1067/960, -29/480, 3/640; [3..4] DER4 13/12, -1/24
+//   [5] WENO5 eps scaled by 3 (weno5_both), [6] 1/6 (FV candidates)
+static __constant__ double kCst[8] = {1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0, 13.0 / 12.0, -1.0 / 24.0,
+                                      3.0e-6, 1.0 / 6.0, 0.0};
+
 struct GridP {
   int n[3];
   long long N;      // cells per field
@@ -21,7 +29,7 @@ struct GridP {
   double idx[3];    // 1 / dx
   int bc[3][2];     // 0 periodic, 1 outflow
   int rec, der, divb;
-  double der_jump;  // A31 DER shock switch (<= 0: off)
+  double der_jump;  // A31 DER shock switch (+inf: off; the host maps <= 0 to +inf)
   long long pitch;  // doubles per (j, k) row of a record array: 8 n1 + padding
 };
 
@@ -204,17 +212,23 @@ ECHO_D void make_state(const M& m, const EosP& e, const double* pr, State& s) {
   s.tau = Z + s.B2 - s.ptot - s.D;
 }
 
-// fast-speed bound along axis j (A4)
+// fast-speed bound along axis j (A4).  With N = Gamma p + b^2 and Dn = rho h + b^2,
+// a^2 = cs^2 + cA^2 - cs^2 cA^2 = N / Dn, and the reading's
+//   lambda = alpha [v^j (1 - a^2) +- sqrt(a^2 (1 - v^2) [g^jj (1 - v^2 a^2) - v^j v^j (1 - a^2)])] / (1 - v^2 a^2) - beta^j
+// multiplied through by Dn (exact in real arithmetic):
+//   lambda = alpha [v^j (Dn - N) +- sqrt(N (1 - v^2) [g^jj (Dn - v^2 N) - v^j v^j (Dn - N)])] / (Dn - v^2 N) - beta^j
+// (one reciprocal and one square root per state).
 template <class M>
 ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, int j, double& lm, double& lp) {
-  // a^2 = cs^2 + cA^2 - cs^2 cA^2 with cs^2 = Gamma p/(rho h), cA^2 = b^2/(rho h + b^2)
-  //     = (Gamma p + b^2) / (rho h + b^2)   (one division instead of two)
-  double a2 = (e.gamma * pr[4] + s.b2) * frcp(s.rhoh + s.b2);
-  double vj = s.v[j];
-  double disc = a2 * (1.0 - s.v2) * (m.gi_diag(j) * (1.0 - s.v2 * a2) - vj * vj * (1.0 - a2));
-  double sq = fsqrt(disc);
-  double iden = m.alpha() * frcp(1.0 - s.v2 * a2);
-  double c = vj * (1.0 - a2);
+  const double N = fma(e.gamma, pr[4], s.b2);
+  const double Dn = s.rhoh + s.b2;
+  const double vj = s.v[j];
+  const double DmN = Dn - N;
+  const double den = fma(-s.v2, N, Dn);
+  const double Q = N * (1.0 - s.v2) * fma(m.gi_diag(j), den, -vj * vj * DmN);
+  const double sq = fsqrt(Q);
+  const double iden = m.alpha() * frcp(den);
+  const double c = vj * DmN;
   lp = (c + sq) * iden - m.beta(j);
   lm = (c - sq) * iden - m.beta(j);
 }
@@ -279,8 +293,8 @@ ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
 // variable.  beta_k are shared by both faces; alpha_k = d_k/(eps+beta_k)^2 is
 // evaluated through the products s_l s_m so one division per face remains.
 // Arithmetic rearrangements (all exact in real arithmetic, rounding-level in fp64):
-//  * beta_k scaled by 12 (13 t^2 + 3 tb^2) with eps -> 12 eps: the weights only
-//    depend on ratios of (eps + beta_k)^2, so the common factor 144 cancels;
+//  * beta_k scaled by 3 with eps -> 3 eps: the weights only depend on ratios of
+//    (eps + beta_k)^2, so the common factor 9 cancels;
 //  * the ideal weights d_k and the candidates' 1/8 are folded into the candidate
 //    coefficients (all exact binary fractions for the point-value form).
 //  * everything is written in the first differences dmm = u_{-1}-u_{-2},
@@ -292,13 +306,17 @@ ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
 //    linear in the differences (2 flops each instead of 5).
 template <int REC>
 ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
-  const double eps12 = 12.0e-6;
+  const double eps3 = kCst[5];
   const double dmm = um1 - um2, dm = u0 - um1, dp = up1 - u0, dpp = up2 - up1;
-  const double d2m = dm - dmm, d2c = dp - dm, d2p = dpp - dp;
-  const double t0b = fma(2.0, dm, d2m), t1b = dm + dp, t2b = fma(-2.0, dp, d2p);
-  double s0 = fma(13.0 * d2m, d2m, fma(3.0 * t0b, t0b, eps12));
-  double s1 = fma(13.0 * d2c, d2c, fma(3.0 * t1b, t1b, eps12));
-  double s2 = fma(13.0 * d2p, d2p, fma(3.0 * t2b, t2b, eps12));
+  // 3 beta_k as quadratic forms of the first differences (12 beta_k = 13 t^2 + 3 tb^2):
+  //   3 beta_0 = 10 dm^2 - 11 dm dmm + 4 dmm^2
+  //   3 beta_1 =  4 dm^2 -  5 dm dp  + 4 dp^2
+  //   3 beta_2 = 10 dp^2 - 11 dp dpp + 4 dpp^2
+  // (positive definite, so no cancellation beyond a few ulp); eps -> 3 eps.
+  const double m2 = dm * dm, p2 = dp * dp;
+  double s0 = fma(10.0, m2, fma(dmm, fma(4.0, dmm, -11.0 * dm), eps3));
+  double s1 = fma(4.0, m2, fma(4.0, p2, fma(-5.0 * dm, dp, eps3)));
+  double s2 = fma(10.0, p2, fma(dpp, fma(4.0, dpp, -11.0 * dp), eps3));
   s0 *= s0;
   s1 *= s1;
   s2 *= s2;
@@ -318,7 +336,7 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
   } else {
     // finite-volume form, d = (1, 6, 3)/10 (the 10 cancels):
     //   q0-u0 = (5dm - 2dmm)/6, q1-u0 = (dm + 2dp)/6, q2-u0 = (4dp - dpp)/6, right = mirror
-    const double k = 1.0 / 6.0;
+    const double k = kCst[6];
     C0 = k * fma(5.0, dm, -2.0 * dmm);
     C1 = fma(1.0, dm, 2.0 * dp);
     C2 = 0.5 * fma(4.0, dp, -dpp);
@@ -342,9 +360,8 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
 //   H = (1067/960) F0 - (29/480)(F-1 + F+1) + (3/640)(F-2 + F+2)
 template <int DER>
 ECHO_D double der5(double Fm2, double Fm1, double F0, double Fp1, double Fp2) {
-  if (DER == 6)
-    return fma(3.0 / 640.0, Fm2 + Fp2, fma(-29.0 / 480.0, Fm1 + Fp1, (1067.0 / 960.0) * F0));
-  if (DER == 4) return fma(-1.0 / 24.0, Fm1 + Fp1, (13.0 / 12.0) * F0);
+  if (DER == 6) return fma(kCst[2], Fm2 + Fp2, fma(kCst[1], Fm1 + Fp1, kCst[0] * F0));
+  if (DER == 4) return fma(kCst[4], Fm1 + Fp1, kCst[3] * F0);
   return F0;
 }
 

@@ -3,7 +3,7 @@
 //
 // A persistent CTA owns a group of NL lines (x sweep: 2 lines x 64 cells,
 // 128 threads, 6 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows x
-// 32 cells, 256 threads, 2 CTAs/SM — several CTAs per SM so that their phases
+// 16 cells, 128 threads, 4 CTAs/SM — several CTAs per SM so that their phases
 // desynchronise and the FP64 pipe stays fed across the barriers) and marches
 // along the sweep axis in chunks of CH cells.  Thread i
 // of a line handles, in chunk c (base B = CH c):
@@ -40,8 +40,8 @@ namespace march {
 #endif
 #ifndef ECHO_YZ_NL
 #define ECHO_YZ_NL 8
-#define ECHO_YZ_CH 32
-#define ECHO_YZ_BPS 2
+#define ECHO_YZ_CH 16
+#define ECHO_YZ_BPS 4
 #endif
 struct GeomSpec {
   int nl, ch, bps;
@@ -144,14 +144,19 @@ ECHO_D long long base_of(const GridP& g, int a, int t, int zz) {
   return rec_base(g, t, zz, a);
 }
 
-// cp.async of the primitives of cells x of line t into the ring
+// element stride along the sweep axis in the record layout
 template <int AX>
-ECHO_D void load_cells(const GridP& g, const LineGeom& lg, int t0, int zz, int t, int x, bool vec,
+ECHO_D long long axis_stride(const GridP& g) {
+  return AX == 0 ? 1LL : (AX == 1 ? g.pitch : (long long)g.n[1] * g.pitch);
+}
+
+// cp.async of the primitives of cell x of line t (line record base lb) into the ring
+template <int AX>
+ECHO_D void load_cells(const GridP& g, const LineGeom& lg, long long lb, int t, int x, bool vec,
                        const double* __restrict__ P, unsigned sbase) {
   using GE = Geo<AX>;
   const int ag = map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
-  const int tt = min(t0 + t, lg.nt - 1);
-  const double* src = P + base_of<AX>(g, ag, tt, zz);
+  const double* src = P + lb + ag * axis_stride<AX>(g);
   const long long vs = g.n[0];
   const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, GE::RING>(t, GE::ring(x)));
 #pragma unroll
@@ -159,6 +164,12 @@ ECHO_D void load_cells(const GridP& g, const LineGeom& lg, int t0, int zz, int t
     if (vec) cp_async16(s + 8u * v * GE::VP, src + v * vs);
     else cp_async8(s + 8u * v * GE::VP, src + v * vs);
   }
+}
+
+// record base of line t of a unit (cell 0 along the sweep axis)
+template <int AX>
+ECHO_D long long line_base(const GridP& g, const LineGeom& lg, int t0, int zz, int t) {
+  return base_of<AX>(g, 0, min(t0 + t, lg.nt - 1), zz);
 }
 
 // the first window [-5, CH + 5) of a line group (cells -5..4 feed the prologue chunk)
@@ -170,8 +181,9 @@ ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int 
   unit_origin<AX>(lg, unit, t0, zz);
   const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
   if (vec && (t & 1)) return;
-  load_cells<AX>(g, lg, t0, zz, t, -kG + i, vec, P, sbase);
-  if (i < 2 * kG) load_cells<AX>(g, lg, t0, zz, t, -kG + GE::CH + i, vec, P, sbase);
+  const long long lb = line_base<AX>(g, lg, t0, zz, t);
+  load_cells<AX>(g, lg, lb, t, -kG + i, vec, P, sbase);
+  if (i < 2 * kG) load_cells<AX>(g, lg, lb, t, -kG + GE::CH + i, vec, P, sbase);
 }
 
 template <int AX, bool KS, int DER, int REC, bool DN>
@@ -200,6 +212,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
     unit_origin<AX>(lg, unit, t0, zz);
     const int tt = min(t0 + t, lg.nt - 1);
     const bool line_ok = t0 + t < lg.nt;
+    const long long lb = line_base<AX>(g, lg, t0, zz, t);
+    const long long as = axis_stride<AX>(g);
     const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
     int rb = GE::ring(-CH);  // ring position of the chunk base B
     for (int c = -1; c < lg.nchunks; c++, rb = GE::wrap(rb + CH)) {
@@ -210,7 +224,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       if (AX != 0 && c >= 0) {  // old rhs/EMF values of the CH output cells (needed in C2)
         if (!(vec && (t & 1))) {
           const int a = min(B + i, lg.na - 1);
-          const double* src = R + base_of<AX>(g, a, tt, zz);
+          const double* src = R + lb + a * as;
           const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
 #pragma unroll
           for (int q = 0; q < 7; q++) {
@@ -225,8 +239,11 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) ----
       const int rr = GE::wrap(rb + 3 + i);  // ring position of xr
       const bool a_on = (c >= 0) || (i >= CH - 6);  // the prologue needs cells -3..2 only
-      double qL[8] = {0, 0, 0, 0, 0, 0, 0, 0}, qR[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (a_on) {
+      double qL[8], qR[8];
+      if (!a_on) {
+#pragma unroll
+        for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
+      } else {
         bool rgh = false;
         int pos[5];
 #pragma unroll
@@ -242,7 +259,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
             if (!(qL[v] > 0.0)) qL[v] = u[2];  // A25 positivity fallback
             if (!(qR[v] > 0.0)) qR[v] = u[2];
             // A31 flag of face xr (joins cells xr and xr+1)
-            rgh |= g.der_jump > 0.0 && fabs(u[3] - u[2]) > g.der_jump * fmin(u[2], u[3]);
+            // (der_jump = +inf when the switch is off: the test is then always false)
+            rgh |= fabs(u[3] - u[2]) > g.der_jump * fmin(u[2], u[3]);
           }
         }
         rough[t * RING + rr] = rgh;
@@ -259,7 +277,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
          // (the prologue's window already holds chunk 0's cells)
         if (c < 0) {
         } else if (c + 1 < lg.nchunks) {
-          if (!(vec && (t & 1))) load_cells<AX>(g, lg, t0, zz, t, B + CH + kG + i, vec, P, sbase);
+          if (!(vec && (t & 1))) load_cells<AX>(g, lg, lb, t, B + CH + kG + i, vec, P, sbase);
         } else if (unit + gridDim.x < lg.nunits) {
           load_window<AX>(g, lg, unit + gridDim.x, t, i, P, sbase);
         }
@@ -313,8 +331,9 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 #pragma unroll
           for (int q = 0; q < 7; q++) {
             const double* Fq = smem + GE::OFF_F + q * GE::VF;
-            smem[GE::OFF_H + q * GE::VH + hp] =
-                plain ? Fq[fpos[2]] : der5<DER>(Fq[fpos[0]], Fq[fpos[1]], Fq[fpos[2]], Fq[fpos[3]], Fq[fpos[4]]);
+            const double F0 = Fq[fpos[2]];
+            const double h = der5<DER>(Fq[fpos[0]], Fq[fpos[1]], F0, Fq[fpos[3]], Fq[fpos[4]]);
+            smem[GE::OFF_H + q * GE::VH + hp] = plain ? F0 : h;  // select, no branch
           }
         }
       }
@@ -323,7 +342,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 
       // ---- C2: cell B+i: flux differences into rhs; field-CD EMF (a5) ----
       if (c >= 0 && B + i < lg.na && line_ok) {
-        double* dst = R + base_of<AX>(g, B + i, t0 + t, zz);
+        double* dst = R + lb + (B + i) * as;
 #pragma unroll
         for (int q = 0; q < 7; q++) {
           const double* Hq = smem + GE::OFF_H + q * GE::VH;
