@@ -47,18 +47,21 @@ ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* 
   double Z = (guess[0] + e.gfac * guess[4]) * (1.0 + gu[0] * gl[0] + gu[1] * gl[1] + gu[2] * gl[2]);
   bool polish = false, ok = false;
   for (int it = 1; it <= e.maxit; it++) {
-    const double iZ = frcp(Z);
+    // 1/Z and 1/(Z + B^2) through one reciprocal; 1/sqrt(1 - v^2) from the rsqrt that gives sqrt(1 - v^2)
     const double ZB = Z + B2;
-    const double iZB = frcp(ZB);
+    const double r = frcp(Z * ZB);
+    const double iZ = ZB * r, iZB = Z * r;
     const double iZ2 = iZ * iZ, iZB2 = iZB * iZB;
     double v2 = (Z * Z * S2 + SB2 * (2.0 * Z + B2)) * iZ2 * iZB2;
     bool clamped = false;
     if (v2 > e.v2max) { v2 = e.v2max; clamped = true; }
-    const double sq = fsqrt(1.0 - v2);
-    const double p = e.gm * (Z * (1.0 - v2) - D * sq);
+    const double omv2 = 1.0 - v2;
+    const double rs = frsqrt(omv2);  // 1 - v^2 >= 1/W_max^2 > 0
+    const double sq = omv2 * rs;
+    const double p = e.gm * (Z * omv2 - D * sq);
     const double f = Z - p + 0.5 * B2 * (1.0 + v2) - 0.5 * SB2 * iZ2 - Ut;
     const double dv2 = clamped ? 0.0 : -2.0 * iZB2 * iZB * (S2 + SB2 * (3.0 * Z * Z + 3.0 * Z * B2 + B2 * B2) * iZ2 * iZ);
-    const double dp = e.gm * ((1.0 - v2) - Z * dv2 + D * dv2 * (0.5 * frcp(sq)));
+    const double dp = e.gm * (omv2 - Z * dv2 + D * dv2 * (0.5 * rs));
     const double df = 1.0 - dp + 0.5 * B2 * dv2 + SB2 * iZ2 * iZ;
     double Zn = Z - f * frcp(df);
     if (!(Zn > 0.0)) Zn = 0.5 * Z;
@@ -72,15 +75,16 @@ ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* 
     }
   }
   if (!ok) return 1;
-  const double iZ = frcp(Z);
   const double ZB = Z + B2;
-  const double iZB = frcp(ZB);
+  const double r = frcp(Z * ZB);
+  const double iZ = ZB * r, iZB = Z * r;
   double v2 = (Z * Z * S2 + SB2 * (2.0 * Z + B2)) * (iZ * iZ) * (iZB * iZB);
   if (v2 > e.v2max) v2 = e.v2max;
-  const double sq = fsqrt(1.0 - v2);
-  const double W = frcp(sq);
+  const double omv2 = 1.0 - v2;
+  const double W = frsqrt(omv2);
+  const double sq = omv2 * W;
   out[0] = D * sq;
-  out[4] = e.gm * (Z * (1.0 - v2) - D * sq);
+  out[4] = e.gm * (Z * omv2 - D * sq);
   double vl[3], vu[3];
 #pragma unroll
   for (int i = 0; i < 3; i++) vl[i] = (S[i] + SB * Bl[i] * iZ) * iZB;
@@ -190,6 +194,127 @@ ECHO_D void add_sources(const GenMet& m, const double* __restrict__ dr, const Eo
     }
   }
   L[4] += sg * (e1 + e2 - e3);
+}
+
+// ------------------------------------------------- K3 per-cell pieces
+// the 8 variables of one cell record (row-interleaved layout, echo_dev.cuh): stride n1
+ECHO_D void ld8(const double* p, long long vs, double* o) {
+#pragma unroll
+  for (int v = 0; v < 8; v++) o[v] = p[v * vs];
+}
+ECHO_D void st8(double* p, long long vs, const double* o) {
+#pragma unroll
+  for (int v = 0; v < 8; v++) p[v * vs] = o[v];
+}
+
+// L(U) of cell (i, j, k) from the sweep accumulator R (rows a5, a6): hydro rhs
+// from R plus the metric sources (KS), and L(sqrt(g) B^c) = -D_{c+1} Omega_{c+2}
+// + D_{c+2} Omega_{c+1} (field-CD, A6, A26) or the B rhs from R (divb none).
+// Pp: stage-input primitives of the cell (all 8 for KS, 5 otherwise).
+template <bool KS, bool DIVB_NONE, class M>
+ECHO_D void cell_L(const GridP& g, const EosP& e, const MetTables& mt, const M& m, const double* __restrict__ R,
+                   long long rb, int i, int j, int k, const double* Pp, double* L) {
+  const long long vs = g.n[0];
+  double Rv[8];
+  ld8(R + rb, vs, Rv);
+#pragma unroll
+  for (int q = 0; q < 5; q++) L[q] = Rv[q];
+  if constexpr (KS) add_sources(m, der_rec(mt, i, j), e, Pp, L);
+  if (DIVB_NONE) {
+#pragma unroll
+    for (int c = 0; c < 3; c++) L[5 + c] = Rv[5 + c];
+  } else {
+    // Neighbour offsets in the record layout with the ghost rule for a +-1
+    // step (periodic: wrap to the other end; outflow: the cell itself), branch free.
+    const int ci[3] = {i, j, k};
+    const long long stride[3] = {1, g.pitch, (long long)g.n[1] * g.pitch};
+    long long om_off[3][2];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const long long wrap = (long long)(g.n[a] - 1) * stride[a];
+      om_off[a][0] = (ci[a] > 0) ? -stride[a] : (g.bc[a][0] == 0 ? wrap : 0);
+      om_off[a][1] = (ci[a] < g.n[a] - 1) ? stride[a] : (g.bc[a][1] == 0 ? -wrap : 0);
+    }
+    double onb[3][2][2];  // [axis][-/+][which of the two Omega components used along it]
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int sgn = 0; sgn < 2; sgn++) {
+        const double* base = R + rb + om_off[a][sgn];
+        onb[a][sgn][0] = base[(5 + (a + 1) % 3) * vs];  // Omega_{a+1}
+        onb[a][sgn][1] = base[(5 + (a + 2) % 3) * vs];  // Omega_{a+2}
+      }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
+      // Omega_{c+2} along a1 = c+1 is component (a1 + 1) % 3 -> index 0 of onb[a1];
+      // Omega_{c+1} along a2 = c+2 is component (a2 + 2) % 3 -> index 1 of onb[a2]
+      L[5 + c] = -(onb[a1][1][0] - onb[a1][0][0]) * (0.5 * g.idx[a1]) +
+                 (onb[a2][1][1] - onb[a2][0][1]) * (0.5 * g.idx[a2]);
+    }
+  }
+}
+
+// per-cell CFL rate sum_a max(|lambda+_a|, |lambda-_a|)/Delta_a (a9, A11) of prims pr (with B)
+template <class M>
+ECHO_D double cfl_rate(const M& m, const GridP& g, const EosP& e, const double* pr) {
+  State s;
+  make_state(m, e, pr, s);
+  double val = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    double lm, lp;
+    speeds(m, e, pr, s, a, lm, lp);
+    val += fmax(fabs(lp), fabs(lm)) * g.idx[a];
+  }
+  if (!(val == val)) val = __longlong_as_double(0x7ff0000000000000LL);  // NaN -> +inf (flagged on host)
+  return val;
+}
+
+// One RK stage of cell (i, j, k) (rows a5-a8, and a9 when want_rate):
+// U^{s+1} = RK_s(U^n, U^s, L) into Uout, then con2prim + floors -> P (in place:
+// the stage-input P of the cell is the Newton guess).  Returns the A9 event
+// code (0 none, 1 floor, 2 failure); rate = CFL rate of the new state.
+template <bool KS, bool DIVB_NONE>
+ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* __restrict__ R,
+                      const double* Un, const double* Us, double* Uout, double* P, int i, int j, int k,
+                      bool want_rate, double& rate) {
+  const auto m = MetAt<KS>::get(mt, i, j);
+  const long long rb = rec_base(g, i, j, k), vs = g.n[0];
+  double Pp[8];
+  if (KS) {
+    ld8(P + rb, vs, Pp);  // rho, u~, p, B of the stage input (B for the sources)
+  } else {
+#pragma unroll
+    for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];  // the con2prim guess only
+  }
+  double L[8];
+  cell_L<KS, DIVB_NONE>(g, e, mt, m, R, rb, i, j, k, Pp, L);
+  double Uo[8];
+  ld8(Un + rb, vs, Uo);
+  if (s == 1) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) Uo[q] = Uo[q] + dt * L[q];
+  } else {
+    double us[8];
+    ld8(Us + rb, vs, us);
+    if (s == 2) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) Uo[q] = 0.75 * Uo[q] + 0.25 * (us[q] + dt * L[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; q++) Uo[q] = (1.0 / 3.0) * Uo[q] + (2.0 / 3.0) * (us[q] + dt * L[q]);
+    }
+  }
+  double Po[8];
+  const int ev = c2p_floors(m, e, Uo, Pp, Po);
+  const double isg = !KS ? 1.0 : frcp(m.sqrtg());
+#pragma unroll
+  for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
+  st8(Uout + rb, vs, Uo);
+  st8(P + rb, vs, Po);
+  if (want_rate) rate = fmax(rate, cfl_rate(m, g, e, Po));  // a9 fused: CFL rate of the new state
+  return ev;
 }
 
 }  // namespace echo

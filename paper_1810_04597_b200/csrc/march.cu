@@ -61,7 +61,9 @@ struct Geo {
   static constexpr int LOG_CH = ilog2(CH);
   // ring length for primitives and face fluxes: >= CH + 10 live entries (a power of two when cheap)
   static constexpr int RING = (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
-  static constexpr int HB = CH + 1;                           // DER fluxes of a chunk (+ the carried one)
+  // ring length (bytes per line) of the A31 face flags: written in A for faces B+3..B+CH+2 while D
+  // reads faces B-CH-2..B+1 in the same barrier interval -> >= 2 CH + 5
+  static constexpr int RR = (2 * CH + 5 <= 64) ? 64 : (2 * CH + 5 <= 128) ? 128 : 256;
   static constexpr int THREADS = NL * CH;
   static constexpr int BPS = S.bps;
   static constexpr int DELTA = (AX == 0) ? 1 : NL;           // lane distance between slots i and i+1
@@ -69,16 +71,15 @@ struct Geo {
   static constexpr int NEDGE = CH / SLOTS_PER_WARP;           // warp-edge slots per line
   static constexpr int VP = NL * RING;                        // variable stride, primitive ring
   static constexpr int VF = NL * RING;                        // component stride, F ring
-  static constexpr int VH = NL * HB;                          // component stride, H buffer
   static constexpr int VA = NL * CH;                          // component stride, accumulation buffer
-  static constexpr int VE = NL * NEDGE;                       // variable stride, edge buffer
+  static constexpr int VE = NL * NEDGE;                       // variable stride, edge buffers
   static constexpr int OFF_P = 0;
   static constexpr int OFF_F = OFF_P + 8 * VP;
-  static constexpr int OFF_H = OFF_F + 7 * VF;
-  static constexpr int OFF_A = OFF_H + 7 * VH;
-  static constexpr int OFF_E = OFF_A + ((AX == 0) ? 0 : 7 * VA);
-  static constexpr int TOTAL = OFF_E + 2 * 8 * VE;
-  static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RING;  // + A31 flag ring (bytes)
+  static constexpr int OFF_A = OFF_F + 7 * VF;
+  static constexpr int OFF_E = OFF_A + ((AX == 0) ? 0 : 7 * VA);   // left states qL at warp edges [2][8]
+  static constexpr int OFF_HE = OFF_E + 2 * 8 * VE;                 // DER fluxes H at warp edges [2][7]
+  static constexpr int TOTAL = OFF_HE + 2 * 7 * VE;
+  static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RR;  // + A31 flag ring (bytes)
   static_assert(is_pow2(NL) && is_pow2(CH), "NL and CH must be powers of two");
   static_assert(CH >= 16 && THREADS <= 1024 && (AX == 0 ? CH >= 32 : NL <= 32), "unsupported line geometry");
   static_assert(AX != 0 || NL * CH <= 1024, "x geometry");
@@ -191,15 +192,17 @@ __global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         double* R) {
   using GE = Geo<AX>;
-  constexpr int CH = GE::CH, RING = GE::RING, HB = GE::HB;
+  constexpr int CH = GE::CH, RING = GE::RING, RR = GE::RR;
   extern __shared__ double smem[];
-  unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RING] face flags
+  unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RR] face flags
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const int tid = threadIdx.x;
   const int t = (AX == 0) ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));  // line in the group
   const int i = (AX == 0) ? (tid & (CH - 1)) : (tid >> GE::LOG_NL);      // slot along the line
   const bool edge_in = (i % GE::SLOTS_PER_WARP) == 0;                            // left neighbour in another warp/chunk
   const bool edge_out = (i % GE::SLOTS_PER_WARP) == GE::SLOTS_PER_WARP - 1;       // right neighbour in another warp/chunk
+  const int eslot_out = ((i + 1) & (CH - 1)) / GE::SLOTS_PER_WARP;               // edge slot this thread publishes
+  const int eslot_in = i / GE::SLOTS_PER_WARP;                                   // edge slot this thread reads
   const double idxa = g.idx[AX];
   const long long vs = g.n[0];
 
@@ -210,20 +213,27 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
   for (; unit < lg.nunits; unit += gridDim.x) {
     int t0, zz;
     unit_origin<AX>(lg, unit, t0, zz);
-    const int tt = min(t0 + t, lg.nt - 1);
     const bool line_ok = t0 + t < lg.nt;
     const long long lb = line_base<AX>(g, lg, t0, zz, t);
     const long long as = axis_stride<AX>(g);
+    const int tt = min(t0 + t, lg.nt - 1);
     const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
     int rb = GE::ring(-CH);  // ring position of the chunk base B
-    for (int c = -1; c < lg.nchunks; c++, rb = GE::wrap(rb + CH)) {
+    // Chunk c (base B = c CH): A = WENO of cells B+3+i, B = HLL at faces B+2+i, D = DER + flux
+    // difference of the cells of chunk c-1 (their faces up to B+1 were written by B(c-1)), so one
+    // chunk needs two barriers.  c = -1 is the prologue (A/B of the line start), c = nchunks the
+    // epilogue (D of the last chunk).
+    for (int c = -1; c <= lg.nchunks; c++, rb = GE::wrap(rb + CH)) {
       const int B = c * CH;
-      const int par = (c + 2) & 1;
+      const int par = c & 1;
+      const bool ab = c < lg.nchunks;       // A and B phases
+      const bool d2 = c >= 1;               // D: outputs cells X0 + i of chunk c-1
+      const int X0 = B - CH;
       cp_async_wait0();
-      __syncthreads();  // primitives of this chunk landed; previous chunk fully consumed
-      if (AX != 0 && c >= 0) {  // old rhs/EMF values of the CH output cells (needed in C2)
+      __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
+      if (AX != 0 && d2) {  // old rhs/EMF values of the output cells (accumulated in D)
         if (!(vec && (t & 1))) {
-          const int a = min(B + i, lg.na - 1);
+          const int a = min(X0 + i, lg.na - 1);
           const double* src = R + lb + a * as;
           const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
 #pragma unroll
@@ -233,14 +243,13 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
             else cp_async8(s + 8u * q * GE::VA, src + out_slot<AX, DN>(q) * vs);
           }
         }
-        cp_async_commit();
       }
+      cp_async_commit();
 
-      // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) ----
+      // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) and the A31 flag of face xr ----
       const int rr = GE::wrap(rb + 3 + i);  // ring position of xr
-      const bool a_on = (c >= 0) || (i >= CH - 6);  // the prologue needs cells -3..2 only
       double qL[8], qR[8];
-      if (!a_on) {
+      if (!(ab && (c >= 0 || i >= CH - 6))) {  // the prologue needs cells -3..2 only
 #pragma unroll
         for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
       } else {
@@ -258,24 +267,50 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           if (v == 0 || v == 4) {
             if (!(qL[v] > 0.0)) qL[v] = u[2];  // A25 positivity fallback
             if (!(qR[v] > 0.0)) qR[v] = u[2];
-            // A31 flag of face xr (joins cells xr and xr+1)
-            // (der_jump = +inf when the switch is off: the test is then always false)
-            rgh |= fabs(u[3] - u[2]) > g.der_jump * fmin(u[2], u[3]);
+            // face xr joins cells xr and xr+1 (der_jump = +inf when the switch is off: never fires)
+            const double lo = u[2] < u[3] ? u[2] : u[3];
+            rgh |= fabs(u[3] - u[2]) > g.der_jump * lo;
           }
         }
-        rough[t * RING + rr] = rgh;
+        rough[t * RR + ((B + 3 + i) & (RR - 1))] = rgh;
         if (edge_out) {  // publish the left state of cell xr for the slot to the right
-          const int dpar = (i == CH - 1) ? ((c + 3) & 1) : par;
-          const int slot = ((i + 1) & (CH - 1)) / GE::SLOTS_PER_WARP;
+          const int dpar = (i == CH - 1) ? ((c + 1) & 1) : par;
 #pragma unroll
-          for (int v = 0; v < 8; v++) smem[GE::OFF_E + dpar * 8 * GE::VE + v * GE::VE + t * GE::NEDGE + slot] = qL[v];
+          for (int v = 0; v < 8; v++) smem[GE::OFF_E + dpar * 8 * GE::VE + v * GE::VE + eslot_out * GE::NL + t] = qL[v];
         }
       }
-      __syncthreads();  // A done: primitives of this chunk are dead, edges published
+
+      // ---- D1: DER flux (a4) at the right face X0+i+1/2 of cell X0+i (faces X0+i-2..X0+i+2) ----
+      double H[7];
+      if (d2 || (c == 0 && i == CH - 1)) {  // c = 0: the left face -1/2 of cell 0, carried to D(1)
+        bool plain = false;
+#pragma unroll
+        for (int m = 0; m < 5; m++) plain |= rough[t * RR + ((X0 + i - 2 + m) & (RR - 1))] != 0;  // A31
+        int fpos[5];
+#pragma unroll
+        for (int m = 0; m < 5; m++) fpos[m] = loff<AX, RING>(t, GE::wrap(rb - CH + i - 2 + m));
+#pragma unroll
+        for (int q = 0; q < 7; q++) {
+          const double* Fq = smem + GE::OFF_F + q * GE::VF;
+          const double F0 = Fq[fpos[2]];
+          const double h = der5<DER>(Fq[fpos[0]], Fq[fpos[1]], F0, Fq[fpos[3]], Fq[fpos[4]]);
+          H[q] = plain ? F0 : h;  // select, no branch
+        }
+        if (edge_out) {  // publish H for the slot to the right (slot CH-1: for slot 0 of the next chunk)
+          const int dpar = (i == CH - 1) ? ((c + 1) & 1) : par;
+#pragma unroll
+          for (int q = 0; q < 7; q++) smem[GE::OFF_HE + dpar * 7 * GE::VE + q * GE::VE + eslot_out * GE::NL + t] = H[q];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 7; q++) H[q] = 0.0;
+      }
+      cp_async_wait0();  // the old rhs/EMF values of this thread's copies
+      __syncthreads();   // (1) A and D1 done: primitives of chunk c dead, edges published, A buffer landed
 
       {  // prefetch: the next chunk's CH new cells, or the next line group's first window
          // (the prologue's window already holds chunk 0's cells)
-        if (c < 0) {
+        if (c < 0 || c >= lg.nchunks) {
         } else if (c + 1 < lg.nchunks) {
           if (!(vec && (t & 1))) load_cells<AX>(g, lg, lb, t, B + CH + kG + i, vec, P, sbase);
         } else if (unit + gridDim.x < lg.nunits) {
@@ -284,19 +319,43 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         cp_async_commit();
       }
 
+      // ---- D2: cell X0+i: flux differences into rhs; field-CD EMF (a5) ----
+      if (d2) {
+        double Hm[7];
+#pragma unroll
+        for (int q = 0; q < 7; q++) Hm[q] = __shfl_up_sync(0xffffffffu, H[q], GE::DELTA);
+        if (edge_in) {
+#pragma unroll
+          for (int q = 0; q < 7; q++) Hm[q] = smem[GE::OFF_HE + par * 7 * GE::VE + q * GE::VE + eslot_in * GE::NL + t];
+        }
+        if (X0 + i < lg.na && line_ok) {
+          double* dst = R + lb + (X0 + i) * as;
+#pragma unroll
+          for (int q = 0; q < 7; q++) {
+            double d;
+            if (q < 5 || DN) {
+              d = -(H[q] - Hm[q]) * idxa;
+            } else {
+              const double hs = 0.25 * (H[q] + Hm[q]);
+              d = (q == 5) ? -hs : hs;
+            }
+            dst[out_slot<AX, DN>(q) * vs] =
+                accumulates<AX, DN>(q) ? (smem[GE::OFF_A + q * GE::VA + loff<AX, CH>(t, i)] + d) : d;
+          }
+        }
+      }
+
       // ---- B: face xf = B+2+i between reconstructed cells xf and xf+1 (a3) ----
-      {
+      if (ab) {
         double pl[8];
 #pragma unroll
         for (int v = 0; v < 8; v++) pl[v] = __shfl_up_sync(0xffffffffu, qL[v], GE::DELTA);
         if (edge_in) {
-          const int slot = i / GE::SLOTS_PER_WARP;
 #pragma unroll
-          for (int v = 0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + t * GE::NEDGE + slot];
+          for (int v = 0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + eslot_in * GE::NL + t];
         }
         const int xf = B + 2 + i;
-        const bool b_on = (c >= 0) || (i >= CH - 5);
-        if (b_on) {
+        if (c >= 0 || i >= CH - 5) {
           double F[7];
           if (KS) {
             const int af = max(-kG, min(xf + 1, lg.na + kG));  // face af - 1/2
@@ -312,55 +371,6 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 #pragma unroll
           for (int q = 0; q < 7; q++) smem[GE::OFF_F + q * GE::VF + fp] = F[q];
         }
-      }
-      __syncthreads();  // F of faces B-2 .. B+CH+1 present
-
-      // ---- C1: DER flux at face xh = B+i (a4); stored at H[i+1] ----
-      {
-        const bool c_on = (c >= 0) || (i == CH - 1);
-        if (c_on) {
-          int fpos[5];
-          bool plain = false;
-#pragma unroll
-          for (int m = 0; m < 5; m++) {
-            const int rp = GE::wrap(rr - 5 + m);  // xh - 2 + m = xr - 5 + m
-            fpos[m] = loff<AX, RING>(t, rp);
-            plain |= rough[t * RING + rp] != 0;  // A31: the DER stencil crosses a jump
-          }
-          const int hp = loff<AX, HB>(t, i + 1);
-#pragma unroll
-          for (int q = 0; q < 7; q++) {
-            const double* Fq = smem + GE::OFF_F + q * GE::VF;
-            const double F0 = Fq[fpos[2]];
-            const double h = der5<DER>(Fq[fpos[0]], Fq[fpos[1]], F0, Fq[fpos[3]], Fq[fpos[4]]);
-            smem[GE::OFF_H + q * GE::VH + hp] = plain ? F0 : h;  // select, no branch
-          }
-        }
-      }
-      if (AX != 0 && c >= 0) cp_async_wait1();  // the rhs/EMF values (all but the prefetch group)
-      __syncthreads();
-
-      // ---- C2: cell B+i: flux differences into rhs; field-CD EMF (a5) ----
-      if (c >= 0 && B + i < lg.na && line_ok) {
-        double* dst = R + lb + (B + i) * as;
-#pragma unroll
-        for (int q = 0; q < 7; q++) {
-          const double* Hq = smem + GE::OFF_H + q * GE::VH;
-          const double Hp = Hq[loff<AX, HB>(t, i + 1)], Hm = Hq[loff<AX, HB>(t, i)];
-          double d;
-          if (q < 5 || DN) {
-            d = -(Hp - Hm) * idxa;
-          } else {
-            const double hs = 0.25 * (Hp + Hm);
-            d = (q == 5) ? -hs : hs;
-          }
-          dst[out_slot<AX, DN>(q) * vs] =
-              accumulates<AX, DN>(q) ? (smem[GE::OFF_A + q * GE::VA + loff<AX, CH>(t, i)] + d) : d;
-        }
-      }
-      __syncthreads();
-      if (i < 7) {  // carry H(B+CH-1) -> H[0] (the face B+CH-1/2 of the next chunk)
-        smem[GE::OFF_H + i * GE::VH + loff<AX, HB>(t, 0)] = smem[GE::OFF_H + i * GE::VH + loff<AX, HB>(t, CH)];
       }
     }
   }

@@ -14,36 +14,10 @@
 
 namespace echo {
 
-// the 8 variables of one cell record (row-interleaved layout, echo_dev.cuh): stride n1
-ECHO_D void ld8(const double* __restrict__ p, long long vs, double* o) {
-#pragma unroll
-  for (int v = 0; v < 8; v++) o[v] = p[v * vs];
-}
-ECHO_D void st8(double* p, long long vs, const double* o) {
-#pragma unroll
-  for (int v = 0; v < 8; v++) p[v * vs] = o[v];
-}
-
 // -------------------------------------------------------------- K3 kernel
-// MODE stage: U^{s+1} = RK(U^n, U^s, L) then con2prim/floors -> Uout, P.
+// MODE stage: U^{s+1} = RK(U^n, U^s, L) then con2prim/floors -> Uout, P (stage_cell).
 // MODE rhs:   L(U) into Lout ([var][cell], the C-ABI layout).
 // MODE c2p:   con2prim/floors of Un in place -> Un, P.
-// per-cell CFL rate sum_a max(|lambda+_a|, |lambda-_a|)/Delta_a (a9, A11) of prims pr (with B)
-template <class M>
-ECHO_D double cfl_rate(const M& m, const GridP& g, const EosP& e, const double* pr) {
-  State s;
-  make_state(m, e, pr, s);
-  double val = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; a++) {
-    double lm, lp;
-    speeds(m, e, pr, s, a, lm, lp);
-    val += fmax(fabs(lp), fabs(lm)) * g.idx[a];
-  }
-  if (!(val == val)) val = __longlong_as_double(0x7ff0000000000000LL);  // NaN -> +inf (flagged on host)
-  return val;
-}
-
 // block max of v (all threads of the block call it) -> one atomicMax on the u64 bit pattern
 ECHO_D void block_max_atomic(double v, unsigned long long* out) {
 #pragma unroll
@@ -72,87 +46,34 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
   if (active) {
     int i, j, k;
     cell_ijk(g, id, i, j, k);
-    const auto m = MetAt<KS>::get(mt, i, j);
-    const long long rb = rec_base(g, i, j, k), vs = g.n[0];
-    double Pp[8];
-    if (KS) {
-      ld8(P + rb, vs, Pp);  // rho, u~, p, B of the stage input (B for the sources)
+    if (MODE == kModeStage) {
+      ev = stage_cell<KS, DIVB_NONE>(g, e, mt, s, dt, R, Un, Us, Uout, P, i, j, k, cfl_out != nullptr, rate);
     } else {
-#pragma unroll
-      for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];  // the con2prim guess only
-    }
-    double L[8];
-    if (MODE != kModeC2P) {
-      double Rv[8];
-      ld8(R + rb, vs, Rv);
-#pragma unroll
-      for (int q = 0; q < 5; q++) L[q] = Rv[q];
-      if constexpr (KS) add_sources(m, der_rec(mt, i, j), e, Pp, L);
-      if (DIVB_NONE) {
-#pragma unroll
-        for (int c = 0; c < 3; c++) L[5 + c] = Rv[5 + c];
+      const auto m = MetAt<KS>::get(mt, i, j);
+      const long long rb = rec_base(g, i, j, k), vs = g.n[0];
+      double Pp[8];
+      if (KS) {
+        ld8(P + rb, vs, Pp);
       } else {
-        // L(sqrt(g) B^c) = -D_{c+1} Omega_{c+2} + D_{c+2} Omega_{c+1}   (A6, A26).
-        // Neighbour offsets in the record layout with the ghost rule for a +-1
-        // step (periodic: wrap to the other end; outflow: the cell itself), branch free.
-        const int ci[3] = {i, j, k};
-        const long long stride[3] = {1, g.pitch, (long long)g.n[1] * g.pitch};
-        long long om_off[3][2];
 #pragma unroll
-        for (int a = 0; a < 3; a++) {
-          const long long wrap = (long long)(g.n[a] - 1) * stride[a];
-          om_off[a][0] = (ci[a] > 0) ? -stride[a] : (g.bc[a][0] == 0 ? wrap : 0);
-          om_off[a][1] = (ci[a] < g.n[a] - 1) ? stride[a] : (g.bc[a][1] == 0 ? -wrap : 0);
-        }
-        double onb[3][2][2];  // [axis][-/+][which of the two Omega components used along it]
-#pragma unroll
-        for (int a = 0; a < 3; a++)
-#pragma unroll
-          for (int sgn = 0; sgn < 2; sgn++) {
-            const double* base = R + rb + om_off[a][sgn];
-            onb[a][sgn][0] = base[(5 + (a + 1) % 3) * vs];  // Omega_{a+1}
-            onb[a][sgn][1] = base[(5 + (a + 2) % 3) * vs];  // Omega_{a+2}
-          }
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
-          // Omega_{c+2} along a1 = c+1 is component (a1 + 1) % 3 -> index 0 of onb[a1];
-          // Omega_{c+1} along a2 = c+2 is component (a2 + 2) % 3 -> index 1 of onb[a2]
-          L[5 + c] = -(onb[a1][1][0] - onb[a1][0][0]) * (0.5 * g.idx[a1]) +
-                     (onb[a2][1][1] - onb[a2][0][1]) * (0.5 * g.idx[a2]);
-        }
+        for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];
       }
-    }
-    if (MODE == kModeRhs) {
+      if (MODE == kModeRhs) {
+        double L[8];
+        cell_L<KS, DIVB_NONE>(g, e, mt, m, R, rb, i, j, k, Pp, L);
 #pragma unroll
-      for (int q = 0; q < 8; q++) Lout[q * N + id] = L[q];
-    } else {
-      double Uo[8];
-      ld8(Un + rb, vs, Uo);
-      if (MODE == kModeStage) {
-        if (s == 1) {
+        for (int q = 0; q < 8; q++) Lout[q * N + id] = L[q];
+      } else {  // c2p
+        double Uo[8], Po[8];
+        ld8(Un + rb, vs, Uo);
+        ev = c2p_floors(m, e, Uo, Pp, Po);
+        const double isg = !KS ? 1.0 : frcp(m.sqrtg());
 #pragma unroll
-          for (int q = 0; q < 8; q++) Uo[q] = Uo[q] + dt * L[q];
-        } else {
-          double us[8];
-          ld8(Us + rb, vs, us);
-          if (s == 2) {
-#pragma unroll
-            for (int q = 0; q < 8; q++) Uo[q] = 0.75 * Uo[q] + 0.25 * (us[q] + dt * L[q]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; q++) Uo[q] = (1.0 / 3.0) * Uo[q] + (2.0 / 3.0) * (us[q] + dt * L[q]);
-          }
-        }
+        for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
+        st8(Uout + rb, vs, Uo);
+        st8(P + rb, vs, Po);
+        if (cfl_out) rate = cfl_rate(m, g, e, Po);
       }
-      double Po[8];
-      ev = c2p_floors(m, e, Uo, Pp, Po);
-      const double isg = !KS ? 1.0 : frcp(m.sqrtg());
-#pragma unroll
-      for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
-      st8(Uout + rb, vs, Uo);
-      st8(P + rb, vs, Po);
-      if (cfl_out) rate = cfl_rate(m, g, e, Po);  // a9 fused: CFL rate of the new state
     }
   }
   if (cfl_out) block_max_atomic(rate, cfl_out);
