@@ -1,8 +1,8 @@
 // march.cu — the axis-sweep kernels K2x/K2y/K2z as a marching pipeline
 // (DESIGN.md §2 step 2, rows a1-a5; §7).
 //
-// A persistent CTA owns a group of NL lines (x sweep: 2 lines x 64 cells,
-// 128 threads, 6 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows x
+// A persistent CTA owns a group of NL lines (x sweep: 4 lines x 32 cells,
+// 128 threads (one warp per line), 6 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows x
 // 16 cells, 128 threads, 4 CTAs/SM — several CTAs per SM so that their phases
 // desynchronise and the FP64 pipe stays fed across the barriers) and marches
 // along the sweep axis in chunks of CH cells.  Thread i
@@ -34,8 +34,8 @@ namespace march {
 // (THREADS = NL CH), BPS CTAs per SM.  Overridable at build time for tuning
 // runs (-DECHO_YZ_NL=8 -DECHO_YZ_CH=32 -DECHO_YZ_BPS=2, likewise ECHO_X_*).
 #ifndef ECHO_X_NL
-#define ECHO_X_NL 2
-#define ECHO_X_CH 64
+#define ECHO_X_NL 4
+#define ECHO_X_CH 32
 #define ECHO_X_BPS 6
 #endif
 #ifndef ECHO_YZ_NL

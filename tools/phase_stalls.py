@@ -32,12 +32,12 @@ def ranges():
     span(dev, r"void speeds", "echo_dev.cuh", "B:hll")
     span(dev, r"void hll_face", "echo_dev.cuh", "B:hll")
     span(dev, r"void cons_flux", "echo_dev.cuh", "B:hll")
-    span(dev, r"double der5", "echo_dev.cuh", "C1:der")
+    span(dev, r"double der5", "echo_dev.cuh", "D1:der")
     span(dev, r"double frcp", "echo_dev.cuh", "rcp/rsqrt")
     span(dev, r"double frsqrt", "echo_dev.cuh", "rcp/rsqrt")
     m = open(root + "march.cu").read().splitlines()
-    marks = [(r"---- A: WENO5", "A:march"), (r"prefetch: the next chunk", "prefetch"), (r"---- B: face", "B:march"),
-             (r"---- C1: DER", "C1:march"), (r"---- C2: cell", "C2:march")]
+    marks = [(r"---- A: WENO5", "A:march"), (r"---- D1: DER", "D1:march"), (r"prefetch: the next chunk", "prefetch"),
+             (r"---- D2: cell", "D2:march"), (r"---- B: face", "B:march")]
     idx = [(next(i for i, l in enumerate(m) if re.search(p, l)), ph) for p, ph in marks]
     kend = next(i for i, l in enumerate(m) if l.startswith("template <int AX, bool KS, int DER, int REC, bool DN>\nstatic") or "static cudaError_t launch_one" in l)
     for (a, ph), nxt in zip(idx, idx[1:] + [(kend, None)]):
