@@ -80,6 +80,9 @@ struct Geo {
   static constexpr int OFF_HE = OFF_E + 2 * 8 * VE;                 // DER fluxes H at warp edges [2][7]
   static constexpr int TOTAL = OFF_HE + 2 * 7 * VE;
   static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RR;  // + A31 flag ring (bytes)
+  // x sweep with one warp per line: every exchange of the march (ring, edges, flags, loads) stays
+  // inside the warp, so the chunk barriers are warp barriers and the warps run decoupled
+  static constexpr bool WARP_LOCAL = (AX == 0 && CH == 32);
   static_assert(is_pow2(NL) && is_pow2(CH), "NL and CH must be powers of two");
   static_assert(CH >= 16 && THREADS <= 1024 && (AX == 0 ? CH >= 32 : NL <= 32), "unsupported line geometry");
   static_assert(AX != 0 || NL * CH <= 1024, "x geometry");
@@ -230,7 +233,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       const bool d2 = c >= 1;               // D: outputs cells X0 + i of chunk c-1
       const int X0 = B - CH;
       cp_async_wait0();
-      __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
+      if constexpr (GE::WARP_LOCAL) __syncwarp();
+      else __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
       if (AX != 0 && d2) {  // old rhs/EMF values of the output cells (accumulated in D)
         if (!(vec && (t & 1))) {
           const int a = min(X0 + i, lg.na - 1);
@@ -306,7 +310,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         for (int q = 0; q < 7; q++) H[q] = 0.0;
       }
       cp_async_wait0();  // the old rhs/EMF values of this thread's copies
-      __syncthreads();   // (1) A and D1 done: primitives of chunk c dead, edges published, A buffer landed
+      if constexpr (GE::WARP_LOCAL) __syncwarp();
+      else __syncthreads();  // (1) A and D1 done: primitives of chunk c dead, edges published, A buffer landed
 
       {  // prefetch: the next chunk's CH new cells, or the next line group's first window
          // (the prologue's window already holds chunk 0's cells)
