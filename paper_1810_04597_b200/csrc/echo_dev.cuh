@@ -123,25 +123,24 @@ ECHO_D const double* f1_rec(const MetTables& t, int i, int j) {
 }
 
 // ------------------------------------------------ FP64 reciprocal / rsqrt
-// MUFU seed (rcp/rsqrt.approx.ftz.f64: high word only, ~20 bits) + two Newton
-// steps: ~full double precision (<= 1-2 ulp), no slow-path branch.  Arguments
-// here are always positive, normal and finite (sums of squares, 1 - v^2 a^2, ...).
+// MUFU seed (rcp/rsqrt.approx.ftz.f64: relative error <= 1e-6, measured in
+// tools/rcp_accuracy.cu) + one higher-order correction: with e = 1 - x y0,
+// 1/x = y0 (1 + e + e^2 + ...) -> y0 + y0 (e + e^2), truncation |e|^3 <= 1e-18;
+// with r = 1 - x y0^2, 1/sqrt(x) = y0 (1 + r/2 + 3 r^2/8 + ...), truncation ~|r|^3.
+// Both are within 1-1.3 ulp of the correctly rounded results over 1.2e9 samples
+// (profiles/rcp_accuracy.json).  Arguments here are always positive, normal and
+// finite (sums of squares, 1 - v^2 a^2, ...).
 ECHO_D double frcp(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
 }
 ECHO_D double frsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  double e = fma(-h * y, y, 0.5);
-  y = fma(y, e, y);
-  e = fma(-h * y, y, 0.5);
-  return fma(y, e, y);
+  const double r = fma(-x * y, y, 1.0);
+  return fma(y * r, fma(0.375, r, 0.5), y);
 }
 ECHO_D double fsqrt(double x) { return x > 0.0 ? x * frsqrt(x) : 0.0; }
 
