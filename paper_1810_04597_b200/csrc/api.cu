@@ -107,7 +107,7 @@ static int ensure_scratch(echo_ctx* c) {
 static int run_sweeps(echo_ctx* c) {
   for (int ax = 0; ax < 3; ax++) {
     cudaError_t e = launch(c, kSweepX + ax, [&] {
-      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->R, c->st);
+      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), c->R, c->st);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
   }
@@ -202,7 +202,8 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
 
   // record rows: 8 n1 doubles + 8 (64 B) padding, so that row and plane strides
   // are not powers of two (DRAM channel spread of the y/z pencils)
-  g.pitch = 8LL * g.n[0] + 8;
+  g.vs = g.n[0] + (g.n[0] & 1);
+  g.pitch = 8LL * g.vs + 8;
   const size_t rec = (size_t)g.pitch * g.n[1] * g.n[2];  // doubles per record array
   auto alloc = [&](double** p, size_t nd) { return cudaMalloc(p, sizeof(double) * nd); };
   if (alloc(&c->Un, rec) != cudaSuccess || alloc(&c->Us, rec) != cudaSuccess || alloc(&c->P, rec) != cudaSuccess ||
@@ -321,7 +322,7 @@ int echo_get_prims(echo_ctx* c, double* p8, int on_device) {
     if (rc) return rc;
     dst = c->scratch;
   }
-  cudaError_t e = launch(c, kGetPrims, [&] { return launch_get_prims(c->ks, c->g, c->mt, c->P, dst, c->st); });
+  cudaError_t e = launch(c, kGetPrims, [&] { return launch_get_prims(c->ks, c->g, c->mt, c->P, ucur(c), dst, c->st); });
   if (e != cudaSuccess) return cuda_fail(c, e, "get_prims launch");
   if (!on_device) {
     CK(cudaMemcpyAsync(p8, c->scratch, sizeof(double) * 8 * c->g.N, cudaMemcpyDeviceToHost, c->st), "echo_get_prims");
@@ -461,7 +462,7 @@ int echo_max_dt(echo_ctx* c, double cfl, double* dt_out) {
   if (!c->cfl_valid) {  // otherwise the last update already reduced it for this state
     CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_max_dt");
     cudaError_t e = launch(c, kMaxSpeed, [&] {
-      return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, c->dcnt + 2, c->st);
+      return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, ucur(c), c->dcnt + 2, c->st);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "max_speed launch");
     c->cfl_valid = true;

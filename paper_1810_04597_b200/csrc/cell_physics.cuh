@@ -206,6 +206,13 @@ ECHO_D void st8(double* p, long long vs, const double* o) {
 #pragma unroll
   for (int v = 0; v < 8; v++) p[v * vs] = o[v];
 }
+// primitives of a cell into P: the 5 hydro ones, plus B^i (= U_B / sqrt(g)) only in a curved
+// metric — in Minkowski B^i = U_B and every reader takes it from U
+template <bool KS>
+ECHO_D void st_prims(double* p, long long vs, const double* o) {
+#pragma unroll
+  for (int v = 0; v < (KS ? 8 : 5); v++) p[v * vs] = o[v];
+}
 
 // L(U) of cell (i, j, k) from the sweep accumulator R (rows a5, a6): hydro rhs
 // from R plus the metric sources (KS), and L(sqrt(g) B^c) = -D_{c+1} Omega_{c+2}
@@ -214,7 +221,7 @@ ECHO_D void st8(double* p, long long vs, const double* o) {
 template <bool KS, bool DIVB_NONE, class M>
 ECHO_D void cell_L(const GridP& g, const EosP& e, const MetTables& mt, const M& m, const double* __restrict__ R,
                    long long rb, int i, int j, int k, const double* Pp, double* L) {
-  const long long vs = g.n[0];
+  const long long vs = g.vs;
   double Rv[8];
   ld8(R + rb, vs, Rv);
 #pragma unroll
@@ -272,7 +279,7 @@ ECHO_D double cfl_rate(const M& m, const GridP& g, const EosP& e, const double* 
 }
 
 // One RK stage of cell (i, j, k) (rows a5-a8, and a9 when want_rate):
-// U^{s+1} = RK_s(U^n, U^s, L) into Uout, then con2prim + floors -> P (in place:
+// U^{s+1} = RK_s(U^n, U^s, L) into Uout, then con2prim + floors -> P (st_prims; in place:
 // the stage-input P of the cell is the Newton guess).  Returns the A9 event
 // code (0 none, 1 floor, 2 failure); rate = CFL rate of the new state.
 template <bool KS, bool DIVB_NONE>
@@ -280,7 +287,7 @@ ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s,
                       const double* Un, const double* Us, double* Uout, double* P, int i, int j, int k,
                       bool want_rate, double& rate) {
   const auto m = MetAt<KS>::get(mt, i, j);
-  const long long rb = rec_base(g, i, j, k), vs = g.n[0];
+  const long long rb = rec_base(g, i, j, k), vs = g.vs;
   double Pp[8];
   if (KS) {
     ld8(P + rb, vs, Pp);  // rho, u~, p, B of the stage input (B for the sources)
@@ -312,7 +319,7 @@ ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s,
 #pragma unroll
   for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
   st8(Uout + rb, vs, Uo);
-  st8(P + rb, vs, Po);
+  st_prims<KS>(P + rb, vs, Po);
   if (want_rate) rate = fmax(rate, cfl_rate(m, g, e, Po));  // a9 fused: CFL rate of the new state
   return ev;
 }

@@ -30,7 +30,8 @@ struct GridP {
   int bc[3][2];     // 0 periodic, 1 outflow
   int rec, der, divb;
   double der_jump;  // A31 DER shock switch (+inf: off; the host maps <= 0 to +inf)
-  long long pitch;  // doubles per (j, k) row of a record array: 8 n1 + padding
+  long long vs;     // variable stride inside a row: n1 rounded up to even (16-byte aligned variables, TMA)
+  long long pitch;  // doubles per (j, k) row of a record array: 8 vs + padding
 };
 
 struct EosP {
@@ -146,10 +147,11 @@ ECHO_D double fsqrt(double x) { return x > 0.0 ? x * frsqrt(x) : 0.0; }
 
 // ------------------------------------------------------- device layout
 // Every per-cell record (P, U, R: 8 doubles) is stored row-interleaved,
-// [k][j][var][i]: element (var, i, j, k) at ((k n2 + j) 8 + var) n1 + i.  x stays
+// [k][j][var][i]: element (var, i, j, k) at (k n2 + j) pitch + var vs + i.  x stays
 // unit-stride (coalesced, 16-B pairs), and one (j, k) row holds all 8 variables
 // (8 n1 doubles), so a z-pencil touches one 2 MB page per plane instead of 8.
-// Rows are padded to `pitch` doubles (>= 8 n1) so plane strides are not powers of two.
+// vs = n1 rounded up to even; rows are padded to `pitch` = 8 vs + 8 doubles so plane
+// strides are not powers of two.
 ECHO_HD long long rec_base(const GridP& g, int i, int j, int k) {
   return ((long long)k * g.n[1] + j) * g.pitch + i;
 }

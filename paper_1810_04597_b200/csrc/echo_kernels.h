@@ -1,7 +1,8 @@
 // echo_kernels.h — host-callable launchers of the sm_100a kernels (internal).
 // Device state: every per-cell record has 8 variables, stored row-interleaved
 // ([k][j][var][i], echo_dev.cuh rec_base):
-//   P = rho, u~^1..3, p, B^1..3        (B non-densitised)
+//   P = rho, u~^1..3, p, B^1..3        (B non-densitised; slots 5..7 kept only in a curved
+//                                      metric: in Minkowski B^i = U_B is read from U)
 //   U = sqrt(g) (D, S_1..3, tau, B^1..3)
 //   R = L_D, L_S1..3, L_tau, Omega_1..3 (field-CD) or L_B1..3 (divb none)
 #pragma once
@@ -13,8 +14,10 @@ namespace echo {
 
 // K2x/K2y/K2z: axis sweep (DESIGN §2 step 2): P -> R (x writes, y/z accumulate),
 // a marching pipeline over whole lines (no tile-halo recomputation)
+// P: stage-input primitives; UB: the array holding B^i in slots 5..7 (P in a curved metric,
+// the stage-input U in Minkowski, where B^i = U_B)
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                         double* R, cudaStream_t st);
+                         const double* UB, double* R, cudaStream_t st);
 
 // K3 modes
 enum UpdateMode { kModeStage = 0, kModeRhs = 1, kModeC2P = 2 };
@@ -29,15 +32,15 @@ cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, cons
 
 // a9: per-cell sum_a max|lambda_a|/Delta_a, max-reduced into *out (u64 bit pattern, zeroed by caller)
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                             unsigned long long* out, cudaStream_t st);
+                             const double* U, unsigned long long* out, cudaStream_t st);
 
 // a0: user prims [8][cell] (rho, v, p, B) -> P, U; first unphysical cell into *bad (init LLONG_MAX)
 cudaError_t launch_prim2cons(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P8, double* P,
                              double* U, long long* bad, cudaStream_t st);
 
 // P -> user prims [8][cell]
-cudaError_t launch_get_prims(bool ks, const GridP& g, const MetTables& mt, const double* P, double* P8,
-                             cudaStream_t st);
+cudaError_t launch_get_prims(bool ks, const GridP& g, const MetTables& mt, const double* P, const double* U,
+                             double* P8, cudaStream_t st);
 
 // device records (first nq variables) <-> caller arrays [q][cell]
 cudaError_t launch_layout(const GridP& g, const double* src, double* dst, int nq, bool to_soa, cudaStream_t st);

@@ -157,16 +157,17 @@ ECHO_D long long axis_stride(const GridP& g) {
 // cp.async of the primitives of cell x of line t (line record base lb) into the ring
 template <int AX>
 ECHO_D void load_cells(const GridP& g, const LineGeom& lg, long long lb, int t, int x, bool vec,
-                       const double* __restrict__ P, unsigned sbase) {
+                       const double* __restrict__ P, const double* __restrict__ UB, unsigned sbase) {
   using GE = Geo<AX>;
   const int ag = map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
-  const double* src = P + lb + ag * axis_stride<AX>(g);
-  const long long vs = g.n[0];
+  const long long off = lb + ag * axis_stride<AX>(g);
+  const long long vs = g.vs;
   const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, GE::RING>(t, GE::ring(x)));
 #pragma unroll
   for (int v = 0; v < 8; v++) {
-    if (vec) cp_async16(s + 8u * v * GE::VP, src + v * vs);
-    else cp_async8(s + 8u * v * GE::VP, src + v * vs);
+    const double* src = (v < 5 ? P : UB) + off + v * vs;
+    if (vec) cp_async16(s + 8u * v * GE::VP, src);
+    else cp_async8(s + 8u * v * GE::VP, src);
   }
 }
 
@@ -179,21 +180,21 @@ ECHO_D long long line_base(const GridP& g, const LineGeom& lg, int t0, int zz, i
 // the first window [-5, CH + 5) of a line group (cells -5..4 feed the prologue chunk)
 template <int AX>
 ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int t, int i,
-                        const double* __restrict__ P, unsigned sbase) {
+                        const double* __restrict__ P, const double* __restrict__ UB, unsigned sbase) {
   using GE = Geo<AX>;
   int t0, zz;
   unit_origin<AX>(lg, unit, t0, zz);
   const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
   if (vec && (t & 1)) return;
   const long long lb = line_base<AX>(g, lg, t0, zz, t);
-  load_cells<AX>(g, lg, lb, t, -kG + i, vec, P, sbase);
-  if (i < 2 * kG) load_cells<AX>(g, lg, lb, t, -kG + GE::CH + i, vec, P, sbase);
+  load_cells<AX>(g, lg, lb, t, -kG + i, vec, P, UB, sbase);
+  if (i < 2 * kG) load_cells<AX>(g, lg, lb, t, -kG + GE::CH + i, vec, P, UB, sbase);
 }
 
 template <int AX, bool KS, int DER, int REC, bool DN>
 __global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
-        double* R) {
+        const double* __restrict__ UB, double* R) {
   using GE = Geo<AX>;
   constexpr int CH = GE::CH, RING = GE::RING, RR = GE::RR;
   extern __shared__ double smem[];
@@ -207,10 +208,10 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
   const int eslot_out = ((i + 1) & (CH - 1)) / GE::SLOTS_PER_WARP;               // edge slot this thread publishes
   const int eslot_in = i / GE::SLOTS_PER_WARP;                                   // edge slot this thread reads
   const double idxa = g.idx[AX];
-  const long long vs = g.n[0];
+  const long long vs = g.vs;
 
   long long unit = blockIdx.x;
-  if (unit < lg.nunits) load_window<AX>(g, lg, unit, t, i, P, sbase);
+  if (unit < lg.nunits) load_window<AX>(g, lg, unit, t, i, P, UB, sbase);
   cp_async_commit();
 
   for (; unit < lg.nunits; unit += gridDim.x) {
@@ -317,9 +318,9 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
          // (the prologue's window already holds chunk 0's cells)
         if (c < 0 || c >= lg.nchunks) {
         } else if (c + 1 < lg.nchunks) {
-          if (!(vec && (t & 1))) load_cells<AX>(g, lg, lb, t, B + CH + kG + i, vec, P, sbase);
+          if (!(vec && (t & 1))) load_cells<AX>(g, lg, lb, t, B + CH + kG + i, vec, P, UB, sbase);
         } else if (unit + gridDim.x < lg.nunits) {
-          load_window<AX>(g, lg, unit + gridDim.x, t, i, P, sbase);
+          load_window<AX>(g, lg, unit + gridDim.x, t, i, P, UB, sbase);
         }
         cp_async_commit();
       }
@@ -383,8 +384,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 }
 
 template <int AX, bool KS, int DER, int REC, bool DN>
-static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
-                              cudaStream_t st) {
+static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB,
+                              double* R, cudaStream_t st) {
   using GE = Geo<AX>;
   auto kern = k_march<AX, KS, DER, REC, DN>;
   static int grid_cap = 0;
@@ -406,43 +407,43 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
   lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
   lg.nunits = (long long)lg.tt_groups * lg.nz;
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
-  kern<<<blocks, GE::THREADS, GE::SMEM, st>>>(g, e, mt, lg, P, R);
+  kern<<<blocks, GE::THREADS, GE::SMEM, st>>>(g, e, mt, lg, P, UB, R);
   return cudaGetLastError();
 }
 
 template <int AX, bool KS, int DER, int REC>
-static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
                              cudaStream_t st) {
-  if (g.divb == 1) return launch_one<AX, KS, DER, REC, true>(g, e, mt, P, R, st);
-  return launch_one<AX, KS, DER, REC, false>(g, e, mt, P, R, st);
+  if (g.divb == 1) return launch_one<AX, KS, DER, REC, true>(g, e, mt, P, UB, R, st);
+  return launch_one<AX, KS, DER, REC, false>(g, e, mt, P, UB, R, st);
 }
 template <int AX, bool KS, int DER>
-static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
                               cudaStream_t st) {
-  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, R, st);
-  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, R, st);
+  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, UB, R, st);
+  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, UB, R, st);
 }
 template <int AX, bool KS>
-static cudaError_t launch_der(const GridP& g, const EosP& e, const MetTables& mt, const double* P, double* R,
+static cudaError_t launch_der(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
                               cudaStream_t st) {
-  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, R, st);
-  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, R, st);
-  return launch_rec<AX, KS, 6>(g, e, mt, P, R, st);
+  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, UB, R, st);
+  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, UB, R, st);
+  return launch_rec<AX, KS, 6>(g, e, mt, P, UB, R, st);
 }
 
 }  // namespace march
 
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                         double* R, cudaStream_t st) {
+                         const double* UB, double* R, cudaStream_t st) {
   using namespace march;
   if (ks) {
-    if (axis == 0) return launch_der<0, true>(g, e, mt, P, R, st);
-    if (axis == 1) return launch_der<1, true>(g, e, mt, P, R, st);
-    return launch_der<2, true>(g, e, mt, P, R, st);
+    if (axis == 0) return launch_der<0, true>(g, e, mt, P, UB, R, st);
+    if (axis == 1) return launch_der<1, true>(g, e, mt, P, UB, R, st);
+    return launch_der<2, true>(g, e, mt, P, UB, R, st);
   }
-  if (axis == 0) return launch_der<0, false>(g, e, mt, P, R, st);
-  if (axis == 1) return launch_der<1, false>(g, e, mt, P, R, st);
-  return launch_der<2, false>(g, e, mt, P, R, st);
+  if (axis == 0) return launch_der<0, false>(g, e, mt, P, UB, R, st);
+  if (axis == 1) return launch_der<1, false>(g, e, mt, P, UB, R, st);
+  return launch_der<2, false>(g, e, mt, P, UB, R, st);
 }
 
 }  // namespace echo

@@ -50,7 +50,7 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
       ev = stage_cell<KS, DIVB_NONE>(g, e, mt, s, dt, R, Un, Us, Uout, P, i, j, k, cfl_out != nullptr, rate);
     } else {
       const auto m = MetAt<KS>::get(mt, i, j);
-      const long long rb = rec_base(g, i, j, k), vs = g.n[0];
+      const long long rb = rec_base(g, i, j, k), vs = g.vs;
       double Pp[8];
       if (KS) {
         ld8(P + rb, vs, Pp);
@@ -71,7 +71,7 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
 #pragma unroll
         for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
         st8(Uout + rb, vs, Uo);
-        st8(P + rb, vs, Po);
+        st_prims<KS>(P + rb, vs, Po);
         if (cfl_out) rate = cfl_rate(m, g, e, Po);
       }
     }
@@ -118,7 +118,8 @@ cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, cons
 // ------------------------------------------------------ CFL reduction (a9)
 template <bool KS>
 __global__ void __launch_bounds__(kCellThreads)
-k_max_speed(const GridP g, const EosP e, const MetTables mt, const double* __restrict__ P, unsigned long long* out) {
+k_max_speed(const GridP g, const EosP e, const MetTables mt, const double* __restrict__ P, const double* __restrict__ U,
+            unsigned long long* out) {
   const long long N = g.N;
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   double val = 0.0;
@@ -127,17 +128,20 @@ k_max_speed(const GridP g, const EosP e, const MetTables mt, const double* __res
     cell_ijk(g, id, i, j, k);
     const auto m = MetAt<KS>::get(mt, i, j);
     double pr[8];
-    ld8(P + rec_base(g, i, j, k), g.n[0], pr);
+    const long long rb = rec_base(g, i, j, k);
+    ld8(P + rb, g.vs, pr);
+    if (!KS)
+      for (int c = 0; c < 3; c++) pr[5 + c] = U[rb + (5 + c) * g.vs];  // B^i = U_B (Minkowski)
     val = cfl_rate(m, g, e, pr);
   }
   block_max_atomic(val, out);
 }
 
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                             unsigned long long* out, cudaStream_t st) {
+                             const double* U, unsigned long long* out, cudaStream_t st) {
   unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
-  if (ks) k_max_speed<true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, out);
-  else k_max_speed<false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, out);
+  if (ks) k_max_speed<true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, U, out);
+  else k_max_speed<false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, U, out);
   return cudaGetLastError();
 }
 
@@ -167,8 +171,8 @@ k_prim2cons(const GridP g, const EosP e, const MetTables mt, const double* __res
   make_state(m, e, pr, s);
   const double sg = m.sqrtg();
   double u[8] = {sg * s.D, sg * s.S[0], sg * s.S[1], sg * s.S[2], sg * s.tau, sg * pr[5], sg * pr[6], sg * pr[7]};
-  st8(U + rec_base(g, i, j, k), g.n[0], u);
-  st8(P + rec_base(g, i, j, k), g.n[0], pr);
+  st8(U + rec_base(g, i, j, k), g.vs, u);
+  st8(P + rec_base(g, i, j, k), g.vs, pr);
 }
 
 cudaError_t launch_prim2cons(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P8, double* P,
@@ -182,7 +186,8 @@ cudaError_t launch_prim2cons(bool ks, const GridP& g, const EosP& e, const MetTa
 // P[cell][8] -> user prims [8][cell] (v = u~ / W)
 template <bool KS>
 __global__ void __launch_bounds__(kCellThreads)
-k_get_prims(const GridP g, const MetTables mt, const double* __restrict__ P, double* __restrict__ P8) {
+k_get_prims(const GridP g, const MetTables mt, const double* __restrict__ P, const double* __restrict__ U,
+            double* __restrict__ P8) {
   const long long N = g.N;
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= N) return;
@@ -190,7 +195,10 @@ k_get_prims(const GridP g, const MetTables mt, const double* __restrict__ P, dou
   cell_ijk(g, id, i, j, k);
   const auto m = MetAt<KS>::get(mt, i, j);
   double pr[8];
-  ld8(P + rec_base(g, i, j, k), g.n[0], pr);
+  const long long rb = rec_base(g, i, j, k);
+  ld8(P + rb, g.vs, pr);
+  if (!KS)
+    for (int c = 0; c < 3; c++) pr[5 + c] = U[rb + (5 + c) * g.vs];  // B^i = U_B (Minkowski)
   double u[3] = {pr[1], pr[2], pr[3]}, ul[3];
   m.lower(u, ul);
   const double iW = frsqrt(1.0 + u[0] * ul[0] + u[1] * ul[1] + u[2] * ul[2]);
@@ -202,11 +210,11 @@ k_get_prims(const GridP g, const MetTables mt, const double* __restrict__ P, dou
   for (int c = 0; c < 3; c++) P8[(5 + c) * N + id] = pr[5 + c];
 }
 
-cudaError_t launch_get_prims(bool ks, const GridP& g, const MetTables& mt, const double* P, double* P8,
-                             cudaStream_t st) {
+cudaError_t launch_get_prims(bool ks, const GridP& g, const MetTables& mt, const double* P, const double* U,
+                             double* P8, cudaStream_t st) {
   unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
-  if (ks) k_get_prims<true><<<blocks, kCellThreads, 0, st>>>(g, mt, P, P8);
-  else k_get_prims<false><<<blocks, kCellThreads, 0, st>>>(g, mt, P, P8);
+  if (ks) k_get_prims<true><<<blocks, kCellThreads, 0, st>>>(g, mt, P, U, P8);
+  else k_get_prims<false><<<blocks, kCellThreads, 0, st>>>(g, mt, P, U, P8);
   return cudaGetLastError();
 }
 
@@ -217,7 +225,7 @@ k_layout(const GridP g, const double* __restrict__ src, double* __restrict__ dst
   const long long N = g.N;
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= N) return;
-  const long long rb = rec_base_id(g, id), vs = g.n[0];
+  const long long rb = rec_base_id(g, id), vs = g.vs;
   if (to_soa) {
     for (int q = 0; q < nq; q++) dst[q * N + id] = src[rb + q * vs];
   } else {
