@@ -7,8 +7,9 @@
  *      g = 5 deep, axis-sequential, ghost(i) = owned(((i mod n)+n) mod n) for
  *      periodic, owned(clamp(i,0,n-1)) for outflow            [A12, A13]
  *   2. for axis a = 1,2,3: per line, every face i+1/2, i = -3..n+1:
- *      WENO5 of the 8 primitives (left state from cells i-2..i+2, right state
- *      the mirror from cells i+3..i-1) [A2, A3], positivity fallback [A25],
+ *      WENO5 (or MP5, rec=2, A33) of the 8 primitives (left state from cells
+ *      i-2..i+2, right state the mirror from cells i+3..i-1) [A2, A3],
+ *      positivity fallback [A25],
  *      HLL flux with the face metric [A4]; DER correction of the face fluxes
  *      [A5]; L_q -= (H_{i+1/2} - H_{i-1/2}) / Delta_a for the 5 hydro vars;
  *      field-CD EMF contributions Omega (or, divb=none, B flux differences) [A6]
@@ -99,6 +100,54 @@ double orc_weno5_left(const double u[5], int rec) {
   return w0 * q0 + w1 * q1 + w2 * q2;
 }
 
+/* MP5 (Suresh & Huynh 1997, J. Comput. Phys. 136, 83: eqs. 2.12 and 2.19-2.21 in
+ * their order), left-biased value at i+1/2 from u[0..4] = u_{i-2..i+2}; SURVEY §8(f)
+ * f3 ("other high-order reconstruction algorithms").  Reading A33: point
+ * values, so the unlimited value u_OR is the 5-point interpolant at i+1/2,
+ * (3 u_{i-2} - 20 u_{i-1} + 90 u_i + 60 u_{i+1} - 5 u_{i+2}) / 128; alpha = 4;
+ * the no-limiting test uses eps = 0. */
+static double minmod2(double a, double b) {
+  if (a > 0.0 && b > 0.0) return a < b ? a : b;
+  if (a < 0.0 && b < 0.0) return a > b ? a : b;
+  return 0.0;
+}
+static double minmod4(double a, double b, double c, double d) {
+  if (a > 0.0 && b > 0.0 && c > 0.0 && d > 0.0) return fmin(fmin(a, b), fmin(c, d));
+  if (a < 0.0 && b < 0.0 && c < 0.0 && d < 0.0) return fmax(fmax(a, b), fmax(c, d));
+  return 0.0;
+}
+static double median3(double a, double b, double c) { return a + minmod2(b - a, c - a); }
+static double min3(double a, double b, double c) { return fmin(a, fmin(b, c)); }
+static double max3(double a, double b, double c) { return fmax(a, fmax(b, c)); }
+
+double orc_mp5_left(const double u[5]) {
+  const double alpha = 4.0;
+  /* (2.12) the unlimited value and the monotonicity-preserving bound */
+  const double u_or = (3.0 * u[0] - 20.0 * u[1] + 90.0 * u[2] + 60.0 * u[3] - 5.0 * u[4]) / 128.0;
+  const double u_mp = u[2] + minmod2(u[3] - u[2], alpha * (u[2] - u[1]));
+  if ((u_or - u[2]) * (u_or - u_mp) <= 0.0) return u_or;
+  /* (2.19) second differences and their M4 limits at i+1/2 and i-1/2 */
+  const double dm = u[0] - 2.0 * u[1] + u[2];
+  const double d0 = u[1] - 2.0 * u[2] + u[3];
+  const double dp = u[2] - 2.0 * u[3] + u[4];
+  const double dm4_p = minmod4(4.0 * d0 - dp, 4.0 * dp - d0, d0, dp);
+  const double dm4_m = minmod4(4.0 * d0 - dm, 4.0 * dm - d0, d0, dm);
+  /* (2.20) upper limit, median, large curvature */
+  const double u_ul = u[2] + alpha * (u[2] - u[1]);
+  const double u_av = 0.5 * (u[2] + u[3]);
+  const double u_md = u_av - 0.5 * dm4_p;
+  const double u_lc = u[2] + 0.5 * (u[2] - u[1]) + 4.0 / 3.0 * dm4_m;
+  /* (2.21) the limit interval and the limited value */
+  const double u_min = fmax(min3(u[2], u[3], u_md), min3(u[2], u_ul, u_lc));
+  const double u_max = fmin(max3(u[2], u[3], u_md), max3(u[2], u_ul, u_lc));
+  return median3(u_or, u_min, u_max);
+}
+
+/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5 */
+static double orc_rec_left(const double u[5], int rec) {
+  return rec == 2 ? orc_mp5_left(u) : orc_weno5_left(u, rec);
+}
+
 double orc_der(const double F[5], int der) {
   if (der == 6)
     return F[2] - (F[1] - 2.0 * F[2] + F[3]) / 24.0
@@ -135,8 +184,8 @@ static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3]
     double l[5], r[5];
     for (int m = 0; m < 5; m++) l[m] = st[m][v];     /* cells i-2 .. i+2 */
     for (int m = 0; m < 5; m++) r[m] = st[5 - m][v]; /* cells i+3 .. i-1 (mirror) */
-    qL[v] = orc_weno5_left(l, c->rec);
-    qR[v] = orc_weno5_left(r, c->rec);
+    qL[v] = orc_rec_left(l, c->rec);
+    qR[v] = orc_rec_left(r, c->rec);
   }
   /* A25 positivity fallback: a non-positive reconstructed rho or p takes the
    * value of the cell the state was reconstructed in */

@@ -206,6 +206,33 @@ def weno(u, rec):
     return sum(al[k] * q[k] for k in range(3)) / sum(al)
 
 
+def mp5(u):
+    """MP5 (Suresh & Huynh 1997) on point values, A33: always the median of the unlimited
+    5-point interpolant and the MP interval (equivalent to the paper's early exit, which the
+    oracle takes, because u_i and u_MP both lie in that interval)."""
+    def minmod(*a):
+        if all(x > 0 for x in a):
+            return min(a)
+        if all(x < 0 for x in a):
+            return max(a)
+        return mp.mpf(0)
+
+    u_or = (3 * u[0] - 20 * u[1] + 90 * u[2] + 60 * u[3] - 5 * u[4]) / 128
+    dm, d0, dp = u[0] - 2 * u[1] + u[2], u[1] - 2 * u[2] + u[3], u[2] - 2 * u[3] + u[4]
+    m4p = minmod(4 * d0 - dp, 4 * dp - d0, d0, dp)
+    m4m = minmod(4 * d0 - dm, 4 * dm - d0, d0, dm)
+    ul = u[2] + 4 * (u[2] - u[1])
+    md = (u[2] + u[3]) / 2 - m4p / 2
+    lc = u[2] + (u[2] - u[1]) / 2 + mp.mpf(4) / 3 * m4m
+    lo = max(min(u[2], u[3], md), min(u[2], ul, lc))
+    hi = min(max(u[2], u[3], md), max(u[2], ul, lc))
+    return sorted([u_or, lo, hi])[1] if lo <= hi else u_or + minmod(lo - u_or, hi - u_or)
+
+
+def rec_left(u, rec):
+    return mp5(u) if rec == 2 else weno(u, rec)
+
+
 def derf(F, order):
     if order == 6:
         return F[2] - (F[1] - 2 * F[2] + F[3]) / 24 + 3 * (F[0] - 4 * F[1] + 6 * F[2] - 4 * F[3] + F[4]) / 640
@@ -247,8 +274,8 @@ class Scheme:
             cc = list(cell)
             cc[ax] = cell[ax] - 2 + mm
             st.append(self.prim(*cc))
-        qL = [weno([st[mm][v] for mm in range(5)], G.rec) for v in range(8)]
-        qR = [weno([st[5 - mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        qL = [rec_left([st[mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        qR = [rec_left([st[5 - mm][v] for mm in range(5)], G.rec) for v in range(8)]
         if not qL[0] > 0:
             qL[0] = st[2][0]
         if not qL[4] > 0:

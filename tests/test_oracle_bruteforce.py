@@ -35,7 +35,7 @@ def test_bruteforce_periodic_turbulence(orc):
     _compare(orc, c, G, P8)
 
 
-@pytest.mark.parametrize("divb,der,rec", [(1, 4, 0), (0, 6, 1)])
+@pytest.mark.parametrize("divb,der,rec", [(1, 4, 0), (0, 6, 1), (0, 6, 2), (1, 6, 2)])
 def test_bruteforce_switches(orc, divb, der, rec):
     p = I.problem(0, n=(4, 4, 4), seed=12)
     p.params.update(amp=0.2, vmax=0.5)
@@ -45,16 +45,18 @@ def test_bruteforce_switches(orc, divb, der, rec):
     _compare(orc, c, G, P8)
 
 
-def test_bruteforce_outflow_blast(orc):
+@pytest.mark.parametrize("rec", [0, 2])
+def test_bruteforce_outflow_blast(orc, rec):
     # outflow in x and y, periodic z; a pressure jump exercises the positivity fallback
+    # (and, rec=2, the MP5 limiter)
     n = (4, 4, 4)
     bc = ((1, 1), (1, 1), (0, 0))
     P8 = I.uniform_prims(n, 0.01, (0, 0, 0), 1e-3, (0.1, 0.05, 0.0))
     P8[4, :, :2, :2] = 1.0
     P8[0] *= 1 + 0.1 * I.white_noise(5, 64).reshape(4, 4, 4)
     P8[1, 1, 2, 1] = 0.3
-    c = orc.Cfg(n=n, bc=bc)
-    G = B.Grid(n, (0, 0, 0), (1, 1, 1), bc)
+    c = orc.Cfg(n=n, bc=bc, rec=rec)
+    G = B.Grid(n, (0, 0, 0), (1, 1, 1), bc, rec=rec)
     _compare(orc, c, G, P8)
 
 

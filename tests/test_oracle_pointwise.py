@@ -62,6 +62,50 @@ def test_weno5_order(orc):
         assert 1.9 < math.log2(a / b) < 2.1
 
 
+# ------------------------------------------------------------------ MP5 (rec=2, A33)
+def test_mp5_worked_values(orc):
+    # constants and linear data are reproduced exactly (the 5-point interpolant is exact for
+    # polynomials of degree <= 4 and the limiter leaves monotone linear data alone)
+    for c in (0.0, 1.0, -3.7, 1e5):
+        assert orc.mp5_left([c] * 5) == c
+    assert orc.mp5_left([1, 2, 3, 4, 5]) == pytest.approx(3.5, rel=1e-15)
+    # x^2 at x = -2..2: a smooth minimum; MP5's accuracy-preserving bounds (u_md, u_lc of
+    # Suresh & Huynh 1997 eq. 2.20) keep the exact interface value 1/4 (hand-derived in
+    # oracle_scheme.c's order: u_min = -1/2, u_max = 1)
+    assert orc.mp5_left([4, 1, 0, 1, 4]) == pytest.approx(0.25, rel=1e-15)
+    # a step: no new extremum — the face next to the jump keeps the upwind value
+    assert orc.mp5_left([0, 0, 0, 1, 1]) == 0.0
+    assert orc.mp5_left([1, 1, 1, 0, 0]) == 1.0
+    assert orc.mp5_left([0, 0, 1, 1, 1]) == 1.0
+
+
+def test_mp5_monotone_no_new_extrema(orc):
+    # monotone data of any shape: the left state lies between u_i and u_{i+1}
+    rng = np.random.default_rng(7)
+    for _ in range(2000):
+        u = np.cumsum(np.abs(rng.standard_normal(5)) ** 3) * rng.choice([-1.0, 1.0])
+        q = orc.mp5_left(u)
+        assert min(u[2], u[3]) - 1e-14 * np.max(np.abs(u)) <= q <= max(u[2], u[3]) + 1e-14 * np.max(np.abs(u))
+
+
+def test_mp5_order_and_linear_limit(orc):
+    # smooth monotone data (no extrema): the unlimited 5th-order interpolant
+    lin = np.array([3.0, -20.0, 90.0, 60.0, -5.0]) / 128.0
+    for h in (0.05, 0.1):
+        u = np.exp(np.arange(-2, 3) * h)
+        assert orc.mp5_left(u) == pytest.approx(lin @ u, rel=1e-15)
+    # order 5 on point samples of a smooth periodic function (extrema included)
+    def err(N):
+        h = 2 * math.pi / N
+        x = np.arange(N) * h
+        u = np.sin(x) + 0.3 * np.cos(2 * x)
+        return max(abs(orc.mp5_left([u[(i + m) % N] for m in range(-2, 3)]) -
+                       (math.sin(x[i] + h / 2) + 0.3 * math.cos(2 * (x[i] + h / 2)))) for i in range(N))
+    e = [err(N) for N in (64, 128, 256)]
+    for a, b in zip(e, e[1:]):
+        assert math.log2(a / b) > 4.5, e
+
+
 # ------------------------------------------------------------------ DER
 def test_der_values(orc):
     for o in (2, 4, 6):

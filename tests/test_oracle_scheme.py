@@ -194,8 +194,8 @@ def _alfven_x(N, t, eta=0.1, divb=0, rec=0, der=6):
     return P8
 
 
-def _run_alfven(orc, N, divb, tend=0.25, der=6):
-    c = orc.Cfg(n=(N, 1, 1), hi=(1.0, 1.0 / N, 1.0 / N), divb=divb, der=der)
+def _run_alfven(orc, N, divb, tend=0.25, der=6, rec=0):
+    c = orc.Cfg(n=(N, 1, 1), hi=(1.0, 1.0 / N, 1.0 / N), divb=divb, der=der, rec=rec)
     U, P = state(orc, c, _alfven_x(N, 0.0))
     nsteps = int(math.ceil(tend / (0.5 * (1.0 / N) ** (5.0 / 3.0))))
     dt = tend / nsteps
@@ -213,6 +213,13 @@ def test_alfven_convergence(orc):
     assert math.log2(e[0] / e[1]) > 4.5, e
     e = [_run_alfven(orc, N, 0) for N in (16, 32)]
     assert math.log2(e[0] / e[1]) > 1.8, e
+
+
+def test_alfven_convergence_mp5(orc):
+    # f3 / A33: the whole scheme with MP5 reconstruction is 5th order on the exact CP
+    # Alfven wave (divb=none; the limiter must stay inactive on this smooth solution)
+    e = [_run_alfven(orc, N, 1, rec=2) for N in (16, 32)]
+    assert math.log2(e[0] / e[1]) > 4.5, e
 
 
 def _sound(N, amp=1e-2):
