@@ -34,6 +34,7 @@ BYTES_PER_ZONE_STEP = 752.0      # compulsory traffic per zone-update, DESIGN.md
 FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9  # SMs x FP64 lanes x 2 flop/FMA x max clock
 # algorithmic FP64 flops per cell of one sweep launch (Minkowski, DER6, WENO5 point form), DESIGN.md §7
 FLOPS_PER_CELL_SWEEP = 901.0
+REC_NAMES = {0: "WENO5", 1: "WENO5-FV", 2: "MP5"}
 
 
 def load_peaks():
@@ -210,6 +211,7 @@ def run_ours(args, world, rank, local):
 
     K, W = args.steps, args.warmup
     p = I.problem(args.config, n=args.n)
+    p.rec = args.rec
     N = p.ncells
     stream = torch.cuda.current_stream(dev)
     g = echo.Echo(p)
@@ -312,7 +314,7 @@ def run_ours(args, world, rank, local):
             "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
-                                   f"CFL {p.cfl}, Gamma 4/3, WENO5+HLL+DER6+field-CD, SSP-RK3",
+                                   f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[p.rec]}+HLL+DER6+field-CD, SSP-RK3",
                        "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
                        "step": "echo_max_dt + echo_step (3 stages x [3 sweeps + update])"},
@@ -336,6 +338,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--rec", type=int, default=0, choices=[0, 1, 2],
+                    help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5")
     ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")
     ap.add_argument("--ref-n", type=int, default=64)
     ap.add_argument("--cpu-n", type=int, default=64)

@@ -61,7 +61,8 @@ typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_met
  * uses Cartesian (x, y, z); Kerr-Schild uses (ln r, theta, phi) [A14] and
  * requires sin(theta) != 0 at every centre and face of the ghost-extended range.
  * bc[a][0]/[1] = lower/upper boundary of axis a.
- * rec: 0 = WENO5 point-value form (A2, default), 1 = WENO5 finite-volume form.
+ * rec: 0 = WENO5 point-value form (A2, default), 1 = WENO5 finite-volume form,
+ *      2 = MP5 (Suresh & Huynh 1997 on point values, reading A33).
  * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
  * divb: 0 = field-CD constrained transport (A6, default), 1 = none.
  * der_jump: DER shock switch (A31): the DER correction at a face is dropped

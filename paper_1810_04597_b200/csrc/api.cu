@@ -148,7 +148,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     if ((grid->bc[a][0] == ECHO_BC_PERIODIC) != (grid->bc[a][1] == ECHO_BC_PERIODIC))
       return fail(nullptr, ECHO_E_ARG, "echo_create: periodic must be set on both sides of an axis");
   }
-  if (grid->rec != 0 && grid->rec != 1) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0 or 1");
+  if (grid->rec < 0 || grid->rec > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0, 1 or 2");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
   if (grid->divb != 0 && grid->divb != 1) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0 or 1");
   if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");

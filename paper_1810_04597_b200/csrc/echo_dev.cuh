@@ -356,6 +356,46 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
   qR = fma(NR, SL * inv, u0);
 }
 
+// --------------------------------------------------------------- MP5 (A33)
+// Suresh & Huynh (1997) on point values: left state at i+1/2 = median(u_OR, u_min, u_max)
+// with u_OR the 5-point interpolant (3, -20, 90, 60, -5)/128 (the paper's early exit for
+// (u_OR - u_i)(u_OR - u_MP) <= 0 returns the same value, A33).  The right state at i-1/2
+// is the mirror; the second differences and their M4 limits are shared by both faces
+// (the mirror maps d_{i-1} <-> d_{i+1} and M4_{i+1/2} <-> M4_{i-1/2}).
+ECHO_D double mm2(double a, double b) {  // minmod
+  return (a > 0.0 && b > 0.0) ? fmin(a, b) : ((a < 0.0 && b < 0.0) ? fmax(a, b) : 0.0);
+}
+ECHO_D double mm4(double a, double b, double c, double d) {
+  return (a > 0.0 && b > 0.0 && c > 0.0 && d > 0.0) ? fmin(fmin(a, b), fmin(c, d))
+         : ((a < 0.0 && b < 0.0 && c < 0.0 && d < 0.0) ? fmax(fmax(a, b), fmax(c, d)) : 0.0);
+}
+// one face from the stencil (um2, um1, u0, up1, up2), M4 at the face (m4f) and at the
+// opposite face (m4b)
+ECHO_D double mp5_face(double um2, double um1, double u0, double up1, double up2, double m4f, double m4b) {
+  const double u_or = (3.0 * um2 - 20.0 * um1 + 90.0 * u0 + 60.0 * up1 - 5.0 * up2) * 0.0078125;  // /128
+  const double dl = u0 - um1;
+  const double u_ul = fma(4.0, dl, u0);
+  const double u_md = fma(-0.5, m4f, 0.5 * (u0 + up1));
+  const double u_lc = fma(4.0 / 3.0, m4b, fma(0.5, dl, u0));
+  const double u_min = fmax(fmin(u0, fmin(up1, u_md)), fmin(u0, fmin(u_ul, u_lc)));
+  const double u_max = fmin(fmax(u0, fmax(up1, u_md)), fmax(u0, fmax(u_ul, u_lc)));
+  return u_or + mm2(u_min - u_or, u_max - u_or);
+}
+ECHO_D void mp5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
+  const double dm = um2 - 2.0 * um1 + u0, d0 = um1 - 2.0 * u0 + up1, dp = u0 - 2.0 * up1 + up2;
+  const double m4p = mm4(4.0 * d0 - dp, 4.0 * dp - d0, d0, dp);  // at i+1/2
+  const double m4m = mm4(4.0 * d0 - dm, 4.0 * dm - d0, d0, dm);  // at i-1/2
+  qL = mp5_face(um2, um1, u0, up1, up2, m4p, m4m);
+  qR = mp5_face(up2, up1, u0, um1, um2, m4m, m4p);
+}
+
+// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5
+template <int REC>
+ECHO_D void rec_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
+  if constexpr (REC == 2) mp5_both(um2, um1, u0, up1, up2, qL, qR);
+  else weno5_both<REC>(um2, um1, u0, up1, up2, qL, qR);
+}
+
 // --------------------------------------------------------------- DER (A5)
 // H = F0 - d2F/24 + 3 d4F/640 collected by symmetric sums:
 //   H = (1067/960) F0 - (29/480)(F-1 + F+1) + (3/640)(F-2 + F+2)

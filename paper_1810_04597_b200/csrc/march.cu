@@ -268,7 +268,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           double u[5];
 #pragma unroll
           for (int m = 0; m < 5; m++) u[m] = r[pos[m]];
-          weno5_both<REC>(u[0], u[1], u[2], u[3], u[4], qL[v], qR[v]);
+          rec_both<REC>(u[0], u[1], u[2], u[3], u[4], qL[v], qR[v]);
           if (v == 0 || v == 4) {
             if (!(qL[v] > 0.0)) qL[v] = u[2];  // A25 positivity fallback
             if (!(qR[v] > 0.0)) qR[v] = u[2];
@@ -420,6 +420,7 @@ static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt,
 template <int AX, bool KS, int DER>
 static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
                               cudaStream_t st) {
+  if (g.rec == 2) return launch_dn<AX, KS, DER, 2>(g, e, mt, P, UB, R, st);
   if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, UB, R, st);
   return launch_dn<AX, KS, DER, 0>(g, e, mt, P, UB, R, st);
 }

@@ -121,6 +121,31 @@ def test_multistep_parity(E, orc, cfg, n, steps):
     assert_groups(g.get_prims(), orc.get_prims(oc, U, P), PRIM8_GROUPS, TOL_10, what="get_prims")
 
 
+@pytest.mark.parametrize("cfg,n,steps", [(0, (32, 32, 32), 10), (2, (40, 40, 40), 10), (4, (64, 32, 16), 5)])
+def test_multistep_parity_mp5(E, orc, cfg, n, steps):
+    """MP5 reconstruction (rec=2, A33): multi-step parity, incl. the blast
+    (limiter active at the shock) and the Kerr-Schild torus."""
+    p = small_problem(cfg, n)
+    p.rec = 2
+    P8 = I.initial_prims(p)
+    oc = ocfg(orc, p)
+    U, P = orc.set_prims(oc, P8)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    ocnt = [0, 0]
+    for _ in range(steps):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        U, P, cnt = orc.step(oc, dt, U, P)
+        ocnt[0] += cnt[0]
+        ocnt[1] += cnt[1]
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"mp5 {steps} steps U cfg{cfg}")
+    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"mp5 {steps} steps P cfg{cfg}")
+    st = g.stats()
+    assert (st["floor_events"], st["c2p_failures"]) == tuple(ocnt)
+
+
 def test_con2prim_parity(E, orc):
     p = small_problem(2, (20, 18, 16))
     P8 = I.initial_prims(p)
@@ -145,7 +170,7 @@ def test_con2prim_parity(E, orc):
 def test_switches_parity(E, orc):
     # rec=FV, der=4, divb=none on a multi-tile grid
     p = small_problem(0, (70, 9, 10))
-    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}):
+    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}):
         for k, v in kw.items():
             setattr(p, k, v)
         P8 = I.initial_prims(p)
