@@ -17,9 +17,9 @@ constexpr int kG = 5;  // halo: WENO5 (3) + DER6 (2), A12
 // constant bank, so every DFMA takes them as a c[][] operand (otherwise the
 // compiler rebuilds each one with a pair of UMOVs at every use).
 //   [0..2] DER6 symmetric-sum weights 1067/960, -29/480, 3/640; [3..4] DER4 13/12, -1/24
-//   [5] WENO5 eps scaled by 3 (weno5_both), [6] 1/6 (FV candidates)
+//   [5] WENO5 eps scaled by 3 (weno5_both), [6] 1/6 (FV candidates), [7] 4/3 (MP5 u_lc)
 static __constant__ double kCst[8] = {1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0, 13.0 / 12.0, -1.0 / 24.0,
-                                      3.0e-6, 1.0 / 6.0, 0.0};
+                                      3.0e-6, 1.0 / 6.0, 4.0 / 3.0};
 
 struct GridP {
   int n[3];
@@ -143,6 +143,9 @@ ECHO_D double frsqrt(double x) {
   const double r = fma(-x * y, y, 1.0);
   return fma(y * r, fma(0.375, r, 0.5), y);
 }
+// min / max by compare-select (operands are finite: no NaN handling needed, unlike fmin)
+ECHO_D double dmin(double a, double b) { return a < b ? a : b; }
+ECHO_D double dmax(double a, double b) { return a > b ? a : b; }
 ECHO_D double fsqrt(double x) { return x > 0.0 ? x * frsqrt(x) : 0.0; }
 
 // ------------------------------------------------------- device layout
@@ -246,8 +249,8 @@ ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* 
   double lmL, lpL, lmR, lpR;
   speeds(m, e, pl, sl, AX, lmL, lpL);
   speeds(m, e, pr, sr, AX, lmR, lpR);
-  const double sL = fmin(0.0, fmin(lmL, lmR));
-  const double sR = fmax(0.0, fmax(lpL, lpR));
+  const double sL = dmin(0.0, dmin(lmL, lmR));
+  const double sR = dmax(0.0, dmax(lpL, lpR));
   const double den = sR - sL;
   if (den > 0.0) {
     const double inv = m.sqrtg() * frcp(den);
@@ -362,12 +365,16 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
 // (u_OR - u_i)(u_OR - u_MP) <= 0 returns the same value, A33).  The right state at i-1/2
 // is the mirror; the second differences and their M4 limits are shared by both faces
 // (the mirror maps d_{i-1} <-> d_{i+1} and M4_{i+1/2} <-> M4_{i-1/2}).
-ECHO_D double mm2(double a, double b) {  // minmod
-  return (a > 0.0 && b > 0.0) ? fmin(a, b) : ((a < 0.0 && b < 0.0) ? fmax(a, b) : 0.0);
+// minmod through signs (copysign and fabs are sign-bit operations): the sign factor is
+// exactly -1, 0 or 1, and an argument +-0 gives 0 through the magnitude minimum, so
+// the values equal the oracle's branch form bit for bit
+ECHO_D double mm2(double a, double b) {
+  return (copysign(0.5, a) + copysign(0.5, b)) * dmin(fabs(a), fabs(b));
 }
 ECHO_D double mm4(double a, double b, double c, double d) {
-  return (a > 0.0 && b > 0.0 && c > 0.0 && d > 0.0) ? fmin(fmin(a, b), fmin(c, d))
-         : ((a < 0.0 && b < 0.0 && c < 0.0 && d < 0.0) ? fmax(fmax(a, b), fmax(c, d)) : 0.0);
+  const double sa = copysign(1.0, a);
+  const double s = (sa + copysign(1.0, b)) * fabs((sa + copysign(1.0, c)) * (sa + copysign(1.0, d)));  // -8, 0, 8
+  return (0.125 * s) * dmin(dmin(fabs(a), fabs(b)), dmin(fabs(c), fabs(d)));
 }
 // one face from the stencil (um2, um1, u0, up1, up2), M4 at the face (m4f) and at the
 // opposite face (m4b)
@@ -376,9 +383,10 @@ ECHO_D double mp5_face(double um2, double um1, double u0, double up1, double up2
   const double dl = u0 - um1;
   const double u_ul = fma(4.0, dl, u0);
   const double u_md = fma(-0.5, m4f, 0.5 * (u0 + up1));
-  const double u_lc = fma(4.0 / 3.0, m4b, fma(0.5, dl, u0));
-  const double u_min = fmax(fmin(u0, fmin(up1, u_md)), fmin(u0, fmin(u_ul, u_lc)));
-  const double u_max = fmin(fmax(u0, fmax(up1, u_md)), fmax(u0, fmax(u_ul, u_lc)));
+  const double u_lc = fma(kCst[7], m4b, fma(0.5, dl, u0));
+  // max(min(u0, up1, u_md), min(u0, u_ul, u_lc)) = min(u0, max(min(up1, u_md), min(u_ul, u_lc))), exact
+  const double u_min = dmin(u0, dmax(dmin(up1, u_md), dmin(u_ul, u_lc)));
+  const double u_max = dmax(u0, dmin(dmax(up1, u_md), dmax(u_ul, u_lc)));
   return u_or + mm2(u_min - u_or, u_max - u_or);
 }
 ECHO_D void mp5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
