@@ -53,14 +53,24 @@ typedef enum {
   ECHO_E_NONFINITE = -6    /* all CFL speeds zero / non-finite (echo_max_dt) */
 } echo_status;
 
-typedef enum { ECHO_BC_PERIODIC = 0, ECHO_BC_OUTFLOW = 1 } echo_bc;           /* A13 */
+typedef enum { ECHO_BC_PERIODIC = 0, ECHO_BC_OUTFLOW = 1, ECHO_BC_HALO = 2 } echo_bc;  /* A13; HALO: slabs */
+
+/* Ghost planes per side of a slab (z boundaries of kind ECHO_BC_HALO): kG = 5 for
+ * WENO5 + DER6, plus one because the sweeps also evaluate the EMF on the first
+ * ghost plane (the field-CD curl of the edge plane reads it). */
+#define ECHO_HALO_PLANES 6
 typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_metric_kind;
 
 /* Grid: n owned cells per axis (n >= 1; periodic n < 5 is allowed, ghosts wrap
  * modulo n [A12]); [lo, hi) coordinate extent per axis (lo < hi).  Minkowski
  * uses Cartesian (x, y, z); Kerr-Schild uses (ln r, theta, phi) [A14] and
  * requires sin(theta) != 0 at every centre and face of the ghost-extended range.
- * bc[a][0]/[1] = lower/upper boundary of axis a.
+ * bc[a][0]/[1] = lower/upper boundary of axis a.  ECHO_BC_HALO (axis 2 only) makes the
+ *   context one z-slab of a domain decomposition (the paper's MPI
+ *   Cartesian decomposition): its ghost planes are stored and must be
+ *   filled before every stage — from the neighbour slab (echo_halo_export on the
+ *   neighbour, echo_halo_import here) or, on a physical outflow side of the slab,
+ *   by echo_halo_fill; echo_step is then refused (use echo_stage).  n[2] >= 6.
  * rec: 0 = WENO5 point-value form (A2, default), 1 = WENO5 finite-volume form,
  *      2 = MP5 (Suresh & Huynh 1997 on point values, reading A33).
  * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
@@ -155,6 +165,21 @@ int echo_max_dt(echo_ctx* ctx, double cfl, double* dt_out);
 
 /* Accumulated counters (synchronises). */
 int echo_stats(echo_ctx* ctx, echo_stats_t* out);
+
+/* ---- z-slab domain decomposition (ECHO_BC_HALO) ----
+ * A halo message holds the P and U^s records of the ECHO_HALO_PLANES owned planes
+ * next to one side: echo_halo_doubles(ctx) doubles (0 without halo boundaries),
+ * an internal record layout that only echo_halo_import of a context with the same
+ * n[0], n[1] reads.  side 0 = lower z, 1 = upper z.
+ *   echo_halo_export(ctx, 0, buf, dev): planes 0..5 (for the lower neighbour's side 1)
+ *   echo_halo_import(ctx, 0, buf, dev): ghost planes -6..-1 from the lower neighbour
+ *   echo_halo_fill(ctx, side): a physical outflow side: ghost planes = the edge plane
+ * Call them between stages (after the previous stage / echo_set_prims, before
+ * echo_stage), on the context stream; device buffers stay stream-ordered. */
+long long echo_halo_doubles(const echo_ctx* ctx);
+int echo_halo_export(echo_ctx* ctx, int side, double* buf, int on_device);
+int echo_halo_import(echo_ctx* ctx, int side, const double* buf, int on_device);
+int echo_halo_fill(echo_ctx* ctx, int side);
 
 /* Text of the last error of ctx ("" if none); NULL ctx gives the last echo_create error. */
 const char* echo_last_error(const echo_ctx* ctx);

@@ -38,6 +38,8 @@ struct echo_ctx {
   MetTables mt{};
   double* tables = nullptr;
   // cell-interleaved device state (echo_kernels.h): 8 doubles per cell each
+  double* alloc_base[4] = {nullptr, nullptr, nullptr, nullptr};  // allocations (slab mode: incl. ghost planes)
+  size_t plane = 0;       // doubles per z plane of a record array (pitch n2)
   double* Un = nullptr;   // U^n
   double* Us = nullptr;   // U^s
   double* P = nullptr;    // rho, u~, p, B
@@ -143,10 +145,16 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     if (grid->n[a] < 1) return fail(nullptr, ECHO_E_ARG, "echo_create: n[a] >= 1 violated");
     if (!(grid->hi[a] > grid->lo[a])) return fail(nullptr, ECHO_E_ARG, "echo_create: lo < hi violated");
     for (int s = 0; s < 2; s++)
-      if (grid->bc[a][s] != ECHO_BC_PERIODIC && grid->bc[a][s] != ECHO_BC_OUTFLOW)
-        return fail(nullptr, ECHO_E_ARG, "echo_create: unknown boundary condition");
+      if (grid->bc[a][s] != ECHO_BC_PERIODIC && grid->bc[a][s] != ECHO_BC_OUTFLOW &&
+          !(grid->bc[a][s] == ECHO_BC_HALO && a == 2))
+        return fail(nullptr, ECHO_E_ARG, "echo_create: unknown boundary condition (ECHO_BC_HALO only on axis 2)");
     if ((grid->bc[a][0] == ECHO_BC_PERIODIC) != (grid->bc[a][1] == ECHO_BC_PERIODIC))
       return fail(nullptr, ECHO_E_ARG, "echo_create: periodic must be set on both sides of an axis");
+  }
+  {
+    const bool zh = grid->bc[2][0] == ECHO_BC_HALO || grid->bc[2][1] == ECHO_BC_HALO;
+    if (zh && grid->n[2] < ECHO_HALO_PLANES)
+      return fail(nullptr, ECHO_E_ARG, "echo_create: a slab with halo boundaries needs n[2] >= ECHO_HALO_PLANES");
   }
   if (grid->rec < 0 || grid->rec > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0, 1 or 2");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
@@ -204,10 +212,19 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   // are not powers of two (DRAM channel spread of the y/z pencils)
   g.vs = g.n[0] + (g.n[0] & 1);
   g.pitch = 8LL * g.vs + 8;
-  const size_t rec = (size_t)g.pitch * g.n[1] * g.n[2];  // doubles per record array
-  auto alloc = [&](double** p, size_t nd) { return cudaMalloc(p, sizeof(double) * nd); };
-  if (alloc(&c->Un, rec) != cudaSuccess || alloc(&c->Us, rec) != cudaSuccess || alloc(&c->P, rec) != cudaSuccess ||
-      alloc(&c->R, rec) != cudaSuccess ||
+  // slab mode (z boundaries of kind ECHO_BC_HALO): kZH stored ghost planes below and above
+  // the owned ones in every record array; the array pointers point at plane 0
+  g.zhalo = (g.bc[2][0] == ECHO_BC_HALO || g.bc[2][1] == ECHO_BC_HALO) ? 1 : 0;
+  c->plane = (size_t)g.pitch * g.n[1];
+  const size_t ghost = g.zhalo ? (size_t)kZH * c->plane : 0;
+  const size_t rec = c->plane * g.n[2] + 2 * ghost;  // doubles per record array
+  auto alloc = [&](int slot, double** p) {
+    cudaError_t e = cudaMalloc(&c->alloc_base[slot], sizeof(double) * rec);
+    *p = c->alloc_base[slot] ? c->alloc_base[slot] + ghost : nullptr;
+    return e;
+  };
+  if (alloc(0, &c->Un) != cudaSuccess || alloc(1, &c->Us) != cudaSuccess || alloc(2, &c->P) != cudaSuccess ||
+      alloc(3, &c->R) != cudaSuccess ||
       cudaMalloc(&c->dcnt, 4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&c->dbad, sizeof(long long)) != cudaSuccess ||
       cudaMallocHost(&c->hpin, 4 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -216,12 +233,12 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     return fail(nullptr, ECHO_E_OOM, "echo_create: device allocation failed");
   }
   cudaMemset(c->dcnt, 0, 4 * sizeof(unsigned long long));
-  cudaMemset(c->R, 0, sizeof(double) * rec);
+  for (double* b : c->alloc_base) cudaMemset(b, 0, sizeof(double) * rec);
   if (ks) {
     KsTables t;
     build_ks_tables(metric->M, metric->a, g.n, g.lo, g.dx, &t);
     size_t total = t.cen.size() + t.der.size() + t.f0.size() + t.f1.size();
-    if (alloc(&c->tables, total) != cudaSuccess) {
+    if (cudaMalloc(&c->tables, sizeof(double) * total) != cudaSuccess) {
       echo_destroy(c);
       return fail(nullptr, ECHO_E_OOM, "echo_create: metric table allocation failed");
     }
@@ -250,10 +267,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
 
 void echo_destroy(echo_ctx* c) {
   if (!c) return;
-  cudaFree(c->Un);
-  cudaFree(c->Us);
-  cudaFree(c->P);
-  cudaFree(c->R);
+  for (double* b : c->alloc_base) cudaFree(b);
   cudaFree(c->scratch);
   cudaFree(c->dcnt);
   cudaFree(c->dbad);
@@ -446,6 +460,9 @@ int echo_step(echo_ctx* c, double dt) {
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_step: no state (call echo_set_prims first)");
   if (c->next_stage != 1) return fail(c, ECHO_E_ORDER, "echo_step: a step is in progress (finish its stages)");
+  if (c->g.zhalo)
+    return fail(c, ECHO_E_ORDER,
+                "echo_step: halo (slab) boundaries need a halo exchange before every stage: use echo_stage");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_step: dt > 0 violated");
   for (int s = 1; s <= 3; s++) {
     int rc = run_stage(c, s, dt);
@@ -485,6 +502,56 @@ int echo_stats(echo_ctx* c, echo_stats_t* out) {
   out->c2p_failures = c->hpin[1];
   out->steps = c->steps;
   out->stages = c->stages;
+  return ECHO_OK;
+}
+
+// ------------------------------------------------------------ slab halos
+long long echo_halo_doubles(const echo_ctx* c) {
+  if (!c || !c->g.zhalo) return 0;
+  return 2LL * ECHO_HALO_PLANES * (long long)c->plane;
+}
+
+// message = [P planes][U^s planes] of the ECHO_HALO_PLANES owned planes next to `side`
+int echo_halo_export(echo_ctx* c, int side, double* buf, int on_device) {
+  if (!c || !buf || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_export: bad argument") : ECHO_E_ARG;
+  if (!c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_halo_export: the context has no halo boundary");
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_halo_export: no state");
+  const size_t blk = (size_t)ECHO_HALO_PLANES * c->plane;
+  const size_t k0 = side == 0 ? 0 : (size_t)(c->g.n[2] - ECHO_HALO_PLANES);
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  CK(cudaMemcpyAsync(buf, c->P + k0 * c->plane, sizeof(double) * blk, kind, c->st), "echo_halo_export");
+  CK(cudaMemcpyAsync(buf + blk, ucur(c) + k0 * c->plane, sizeof(double) * blk, kind, c->st), "echo_halo_export");
+  if (!on_device) CK(cudaStreamSynchronize(c->st), "echo_halo_export");
+  return ECHO_OK;
+}
+
+int echo_halo_import(echo_ctx* c, int side, const double* buf, int on_device) {
+  if (!c || !buf || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_import: bad argument") : ECHO_E_ARG;
+  if (!c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_halo_import: the context has no halo boundary");
+  const size_t blk = (size_t)ECHO_HALO_PLANES * c->plane;
+  const long long k0 = side == 0 ? -ECHO_HALO_PLANES : c->g.n[2];
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CK(cudaMemcpyAsync(c->P + k0 * (long long)c->plane, buf, sizeof(double) * blk, kind, c->st), "echo_halo_import");
+  CK(cudaMemcpyAsync(ucur_mut(c) + k0 * (long long)c->plane, buf + blk, sizeof(double) * blk, kind, c->st),
+     "echo_halo_import");
+  if (!on_device) CK(cudaStreamSynchronize(c->st), "echo_halo_import");
+  return ECHO_OK;
+}
+
+// a physical outflow side of a slab: every ghost plane = the owned edge plane (A13)
+int echo_halo_fill(echo_ctx* c, int side) {
+  if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_fill: bad argument") : ECHO_E_ARG;
+  if (!c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_halo_fill: the context has no halo boundary");
+  if (c->g.bc[2][side] != ECHO_BC_OUTFLOW)
+    return fail(c, ECHO_E_ARG, "echo_halo_fill: only an outflow side is filled locally (halo sides are imported)");
+  const long long edge = side == 0 ? 0 : c->g.n[2] - 1;
+  for (int h = 1; h <= ECHO_HALO_PLANES; h++) {
+    const long long k = side == 0 ? -h : c->g.n[2] - 1 + h;
+    for (double* a : {c->P, ucur_mut(c)})
+      CK(cudaMemcpyAsync(a + k * (long long)c->plane, a + edge * (long long)c->plane, sizeof(double) * c->plane,
+                         cudaMemcpyDeviceToDevice, c->st),
+         "echo_halo_fill");
+  }
   return ECHO_OK;
 }
 

@@ -239,8 +239,9 @@ ECHO_D void cell_L(const GridP& g, const EosP& e, const MetTables& mt, const M& 
 #pragma unroll
     for (int a = 0; a < 3; a++) {
       const long long wrap = (long long)(g.n[a] - 1) * stride[a];
-      om_off[a][0] = (ci[a] > 0) ? -stride[a] : (g.bc[a][0] == 0 ? wrap : 0);
-      om_off[a][1] = (ci[a] < g.n[a] - 1) ? stride[a] : (g.bc[a][1] == 0 ? -wrap : 0);
+      // (slab mode, z: an inter-slab side reads the stored ghost plane, whose EMF the sweeps computed)
+      om_off[a][0] = (ci[a] > 0) ? -stride[a] : (g.bc[a][0] == 0 ? wrap : (g.bc[a][0] == 2 ? -stride[a] : 0));
+      om_off[a][1] = (ci[a] < g.n[a] - 1) ? stride[a] : (g.bc[a][1] == 0 ? -wrap : (g.bc[a][1] == 2 ? stride[a] : 0));
     }
     double onb[3][2][2];  // [axis][-/+][which of the two Omega components used along it]
 #pragma unroll

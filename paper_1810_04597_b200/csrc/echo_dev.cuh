@@ -12,6 +12,8 @@
 namespace echo {
 
 constexpr int kG = 5;  // halo: WENO5 (3) + DER6 (2), A12
+constexpr int kZH = 6; // stored z ghost planes per side in slab mode (kG + 1: the sweeps also
+                       // produce the EMF on the first ghost plane, which the field-CD curl reads)
 
 // FP64 constants that are not exact in a 32-bit-high-word immediate live in the
 // constant bank, so every DFMA takes them as a c[][] operand (otherwise the
@@ -27,7 +29,8 @@ struct GridP {
   double lo[3];
   double dx[3];     // (hi - lo) / n
   double idx[3];    // 1 / dx
-  int bc[3][2];     // 0 periodic, 1 outflow
+  int bc[3][2];     // 0 periodic, 1 outflow, 2 halo (z only: planes filled by the caller, echo_halo_*)
+  int zhalo;        // z ghost planes are stored (kZH per side) and filled by the caller before each stage
   int rec, der, divb;
   double der_jump;  // A31 DER shock switch (+inf: off; the host maps <= 0 to +inf)
   long long vs;     // variable stride inside a row: n1 rounded up to even (16-byte aligned variables, TMA)

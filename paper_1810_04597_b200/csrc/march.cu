@@ -132,13 +132,16 @@ ECHO_D void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 struct LineGeom {
   int na, nt, tt_groups, nz, nchunks;
   int vec16;
+  // slab mode (stored z ghost planes): the x/y sweeps also run on the planes zoff = -1 and nz;
+  // the z sweep's lines cover cells coff = -1 .. n3 and read every ghost as a stored plane
+  int zoff, coff, stored;
   long long nunits;
 };
 
 template <int AX>
 ECHO_D void unit_origin(const LineGeom& lg, long long unit, int& t0, int& zz) {
   t0 = (int)(unit % lg.tt_groups) * Geo<AX>::NL;
-  zz = (int)(unit / lg.tt_groups);
+  zz = (int)(unit / lg.tt_groups) + lg.zoff;
 }
 
 template <int AX>
@@ -159,7 +162,10 @@ template <int AX>
 ECHO_D void load_cells(const GridP& g, const LineGeom& lg, long long lb, int t, int x, bool vec,
                        const double* __restrict__ P, const double* __restrict__ UB, unsigned sbase) {
   using GE = Geo<AX>;
-  const int ag = map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
+  // slab z sweep: ghosts are stored planes (-kZH .. n + kZH - 1); the clamp only touches the
+  // cells past the line end that the last chunk's window over-fetches (never used)
+  const int ag = lg.stored ? min(max(x + lg.coff, -kZH), g.n[AX] + kZH - 1)
+                           : map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
   const long long off = lb + ag * axis_stride<AX>(g);
   const long long vs = g.vs;
   const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, GE::RING>(t, GE::ring(x)));
@@ -238,7 +244,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       else __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
       if (AX != 0 && d2) {  // old rhs/EMF values of the output cells (accumulated in D)
         if (!(vec && (t & 1))) {
-          const int a = min(X0 + i, lg.na - 1);
+          const int a = min(X0 + i, lg.na - 1) + lg.coff;
           const double* src = R + lb + a * as;
           const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
 #pragma unroll
@@ -335,7 +341,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           for (int q = 0; q < 7; q++) Hm[q] = smem[GE::OFF_HE + par * 7 * GE::VE + q * GE::VE + eslot_in * GE::NL + t];
         }
         if (X0 + i < lg.na && line_ok) {
-          double* dst = R + lb + (X0 + i) * as;
+          double* dst = R + lb + (X0 + i + lg.coff) * as;
 #pragma unroll
           for (int q = 0; q < 7; q++) {
             double d;
@@ -403,7 +409,20 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
   lg.nt = g.n[AX == 0 ? 1 : 0];
   lg.tt_groups = (lg.nt + GE::NL - 1) / GE::NL;
   lg.nz = (AX == 2) ? g.n[1] : g.n[2];
-  lg.nchunks = (lg.na + GE::CH - 1) / GE::CH;
+  lg.zoff = 0;
+  lg.coff = 0;
+  lg.stored = 0;
+  if (g.zhalo) {
+    if (AX == 2) {  // lines over the owned planes and the first ghost plane on each side
+      lg.na += 2;
+      lg.coff = -1;
+      lg.stored = 1;
+    } else {        // x/y sweeps also on the first ghost planes (their EMF feeds the curl)
+      lg.nz += 2;
+      lg.zoff = -1;
+    }
+  }
+  lg.nchunks = (lg.na + GE::CH - 1) / GE::CH;  // (after the slab extension of na)
   lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
   lg.nunits = (long long)lg.tt_groups * lg.nz;
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);

@@ -26,7 +26,8 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 OK, E_ARG, E_CUDA, E_OOM, E_ORDER, E_UNPHYSICAL, E_NONFINITE = 0, -1, -2, -3, -4, -5, -6
-BC_PERIODIC, BC_OUTFLOW = 0, 1
+BC_PERIODIC, BC_OUTFLOW, BC_HALO = 0, 1, 2
+HALO_PLANES = 6
 METRIC_MINKOWSKI, METRIC_KERR_SCHILD = 0, 1
 
 
@@ -72,6 +73,10 @@ _sig = {
     "echo_kernel_classes": (C.c_int, []),
     "echo_kernel_name": (C.c_char_p, [C.c_int]),
     "echo_launch_count": (C.c_longlong, [_P]),
+    "echo_halo_doubles": (C.c_longlong, [_P]),
+    "echo_halo_export": (C.c_int, [_P, C.c_int, _P, C.c_int]),
+    "echo_halo_import": (C.c_int, [_P, C.c_int, _P, C.c_int]),
+    "echo_halo_fill": (C.c_int, [_P, C.c_int]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -230,6 +235,24 @@ def kernel_name(i: int) -> str:
 
 def launch_count(ctx) -> int:
     return int(_lib.echo_launch_count(ctx))
+
+
+def halo_doubles(ctx) -> int:
+    return int(_lib.echo_halo_doubles(ctx))
+
+
+def halo_export(ctx, side: int, buf):
+    p, d = _buf(buf, True)
+    return _check(ctx, _lib.echo_halo_export(ctx, int(side), p, d))
+
+
+def halo_import(ctx, side: int, buf):
+    p, d = _buf(buf)
+    return _check(ctx, _lib.echo_halo_import(ctx, int(side), p, d))
+
+
+def halo_fill(ctx, side: int):
+    return _check(ctx, _lib.echo_halo_fill(ctx, int(side)))
 
 
 # ------------------------------------------------------- convenience

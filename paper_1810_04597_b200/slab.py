@@ -1,0 +1,192 @@
+"""z-slab domain decomposition of the time step.
+
+The paper's code scales by a Cartesian MPI domain decomposition with a ghost
+exchange per stage.  Here every rank (one process per GPU)
+owns a contiguous block of z planes of the global grid; its context has z
+boundaries of kind BC_HALO (stored ghost planes, echo.h) and, before every RK
+stage, the 6 boundary planes of P and U^s travel to the neighbours:
+
+    for s in 1, 2, 3:  exchange()  ->  echo_stage(s, dt)
+
+with dt = the minimum over ranks of each slab's CFL dt (the max signal speed is
+a max over cells, so the decomposed dt equals the single-domain one bit for bit).
+The library does the arithmetic (export/import are stream-ordered device copies);
+this module only pairs the messages: torch.distributed point-to-point (NCCL over
+NVLink on GPUs, gloo on CPU) between ranks, or direct copies between slabs held by
+one process (`LocalSlabs`, which makes the decomposed step testable on one GPU).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import replace
+
+LOWER, UPPER = 0, 1
+
+
+def decompose_z(n3: int, nranks: int) -> list[tuple[int, int]]:
+    """(z0, nz) of each rank: contiguous, balanced (sizes differ by at most one plane),
+    every slab at least HALO_PLANES = 6 planes thick."""
+    if nranks < 1:
+        raise ValueError("nranks >= 1")
+    base, extra = divmod(n3, nranks)
+    if base < 6:
+        raise ValueError(f"{n3} planes cannot give {nranks} slabs of >= 6 planes")
+    out, z0 = [], 0
+    for r in range(nranks):
+        nz = base + (1 if r < extra else 0)
+        out.append((z0, nz))
+        z0 += nz
+    return out
+
+
+def neighbours(rank: int, nranks: int, periodic: bool) -> tuple[int | None, int | None]:
+    """(lower, upper) neighbour ranks along z; None at a physical (outflow) end."""
+    lo = rank - 1 if rank > 0 else (nranks - 1 if periodic else None)
+    hi = rank + 1 if rank < nranks - 1 else (0 if periodic else None)
+    return lo, hi
+
+
+def slab_problem(problem, rank: int, nranks: int):
+    """The rank's slab of an echo_inputs.Problem: its z planes and coordinate range, z
+    boundaries BC_HALO towards neighbours and the global rule at physical ends."""
+    from .echo import BC_HALO
+
+    z0, nz = decompose_z(problem.n[2], nranks)[rank]
+    dz = (problem.hi[2] - problem.lo[2]) / problem.n[2]
+    periodic = problem.bc[2][0] == 0
+    lo_nb, hi_nb = neighbours(rank, nranks, periodic)
+    bcz = (BC_HALO if lo_nb is not None else problem.bc[2][0], BC_HALO if hi_nb is not None else problem.bc[2][1])
+    bc = (tuple(problem.bc[0]), tuple(problem.bc[1]), bcz)
+    return replace(problem, n=(problem.n[0], problem.n[1], nz), lo=(problem.lo[0], problem.lo[1], problem.lo[2] + z0 * dz),
+                   hi=(problem.hi[0], problem.hi[1], problem.lo[2] + (z0 + nz) * dz), bc=bc), (z0, nz)
+
+
+class LocalSlabs:
+    """All slabs of one grid in one process (one GPU): the decomposed step with the
+    ghost exchange done by device-to-device copies between the contexts."""
+
+    def __init__(self, problem, nslabs: int, device="cuda"):
+        import torch
+
+        from . import echo as E
+
+        self.E = E
+        self.problem = problem
+        self.periodic = problem.bc[2][0] == 0
+        self.parts = []
+        for r in range(nslabs):
+            sp, (z0, nz) = slab_problem(problem, r, nslabs)
+            self.parts.append((E.Echo(sp), z0, nz))
+        nd = E.halo_doubles(self.parts[0][0].ctx)
+        self.buf = torch.empty(nd, dtype=torch.float64, device=device)
+
+    def set_prims(self, p8):
+        for g, z0, nz in self.parts:
+            g.set_prims(p8[:, z0:z0 + nz].copy())
+
+    def exchange(self):
+        E, n = self.E, len(self.parts)
+        for r, (g, _, _) in enumerate(self.parts):
+            lo, hi = neighbours(r, n, self.periodic)
+            for side, nb in ((LOWER, lo), (UPPER, hi)):
+                if nb is None:
+                    E.halo_fill(g.ctx, side)
+                else:  # my side-`side` ghosts = the neighbour's planes next to its opposite side
+                    E.halo_export(self.parts[nb][0].ctx, 1 - side, self.buf)
+                    E.halo_import(g.ctx, side, self.buf)
+
+    def max_dt(self, cfl: float) -> float:
+        return min(g.max_dt(cfl) for g, _, _ in self.parts)
+
+    def step(self, dt: float):
+        for s in (1, 2, 3):
+            self.exchange()
+            for g, _, _ in self.parts:
+                g.stage(s, dt)
+
+    def gather(self, getter):
+        import numpy as np
+
+        return np.concatenate([getter(g) for g, _, _ in self.parts], axis=-3)
+
+    def close(self):
+        for g, _, _ in self.parts:
+            g.close()
+
+
+class DistSlab:
+    """This rank's slab under torch.distributed: point-to-point ghost exchange with the
+    z neighbours (send my boundary planes, receive theirs), min-reduced CFL dt.
+    `io` supplies export(side, buf) / import_(side, buf) / fill(side) / halo_doubles
+    (the library context by default; a host stand-in in the CPU tests)."""
+
+    def __init__(self, io, rank: int, nranks: int, periodic: bool, device):
+        import torch
+
+        self.io, self.rank, self.n = io, rank, nranks
+        self.lo, self.hi = neighbours(rank, nranks, periodic)
+        nd = io.halo_doubles()
+        self.send = [torch.empty(nd, dtype=torch.float64, device=device) for _ in range(2)]
+        self.recv = [torch.empty(nd, dtype=torch.float64, device=device) for _ in range(2)]
+
+    def exchange(self):
+        import torch.distributed as dist
+
+        # sends in the order (upper planes, lower planes), receives (lower ghosts, upper ghosts),
+        # tagged with the side of the sender's planes: with two ranks both neighbours are the
+        # same peer, and NCCL ignores tags and matches point-to-point messages in issue order
+        for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
+            if nb is not None:
+                self.io.export(side, self.send[side])
+        ops = []
+        for side, nb in ((UPPER, self.hi), (LOWER, self.lo)):
+            if nb is not None and nb != self.rank:
+                ops.append(dist.P2POp(dist.isend, self.send[side], nb, tag=side))
+        for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
+            if nb is not None and nb != self.rank:
+                ops.append(dist.P2POp(dist.irecv, self.recv[side], nb, tag=1 - side))
+        if ops:
+            self.io.sync()
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
+            if nb is None:
+                self.io.fill(side)
+            elif nb == self.rank:
+                self.io.import_(side, self.send[1 - side])
+            else:
+                self.io.import_(side, self.recv[side])
+
+    def min_dt(self, dt_local: float) -> float:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([dt_local], dtype=torch.float64, device=self.send[0].device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t.item())
+
+
+class CtxIO:
+    """DistSlab's io over a library context (device buffers on the context stream)."""
+
+    def __init__(self, echo_obj):
+        from . import echo as E
+
+        self.E, self.g = E, echo_obj
+
+    def halo_doubles(self):
+        return self.E.halo_doubles(self.g.ctx)
+
+    def export(self, side, buf):
+        self.E.halo_export(self.g.ctx, side, buf)
+
+    def import_(self, side, buf):
+        self.E.halo_import(self.g.ctx, side, buf)
+
+    def fill(self, side):
+        self.E.halo_fill(self.g.ctx, side)
+
+    def sync(self):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
