@@ -193,6 +193,90 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------- ours, z-slab decomposition
+def run_decomp(args, world, rank, local):
+    """--decomp: the config's grid split into z slabs, strong
+    scaling: N ranks x 1 slab (ghost exchange by NCCL point-to-point over NVLink), or
+    on one GPU --slabs S slabs in one process (device copies; the decomposition's own
+    cost: the extra ghost-plane sweeps and the exchange)."""
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1810_04597_b200 import build
+
+    build.build()
+    from paper_1810_04597_b200 import echo, slab
+
+    K, W = args.steps, args.warmup
+    p = I.problem(args.config, n=args.n)
+    p.rec = args.rec
+    N = p.ncells
+    stream = torch.cuda.current_stream(dev)
+    P8 = I.initial_prims(p, device=dev)
+    if world == 1:
+        S = slab.LocalSlabs(p, args.slabs, device=dev)
+        S.set_prims(P8)
+        launches0 = sum(echo.launch_count(g.ctx) for g, _, _ in S.parts)
+
+        def one_step():
+            S.step(S.max_dt(p.cfl))
+        nslab = args.slabs
+    else:
+        sp, (z0, nz) = slab.slab_problem(p, rank, world)
+        g = echo.Echo(sp)
+        echo.set_stream(g.ctx, stream.cuda_stream)
+        g.set_prims(P8[:, z0:z0 + nz].contiguous())
+        D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev)
+        launches0 = echo.launch_count(g.ctx)
+
+        def one_step():
+            dt = D.min_dt(g.max_dt(p.cfl))
+            for s in (1, 2, 3):
+                D.exchange()
+                g.stage(s, dt)
+        nslab = world
+    del P8
+    for _ in range(W):
+        one_step()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
+    clk.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = clk.stop()
+    t = reduce_max(e0.elapsed_time(e1) / 1e3, world, dev)
+    launches = (sum(echo.launch_count(g.ctx) for g, _, _ in S.parts) if world == 1 else echo.launch_count(g.ctx)) - launches0
+    if rank == 0:
+        out = {"metric": METRIC, "value": N * K / t, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+               "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic",
+               "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
+                                      f"{REC_NAMES[p.rec]}+HLL+DER6+field-CD, SSP-RK3",
+                          "grid": list(p.n), "parallelism": f"{nslab} z-slabs" + (f" on {world} GPUs (NCCL P2P ghost exchange)"
+                                                                                 if world > 1 else " on 1 GPU (device-copy exchange)"),
+                          "step": "min-reduced CFL dt + 3 x (ghost exchange + echo_stage)"},
+               "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- ours
 def run_ours(args, world, rank, local):
     import numpy as np
@@ -338,6 +422,9 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--decomp", action="store_true",
+                    help="z-slab domain decomposition (strong scaling; default N>1 mode is independent replicas)")
+    ap.add_argument("--slabs", type=int, default=2, help="--decomp on one GPU: slabs held by this process")
     ap.add_argument("--rec", type=int, default=0, choices=[0, 1, 2],
                     help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5")
     ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")
@@ -349,6 +436,8 @@ def main(argv=None):
     world, rank, local = dist_setup()
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    if args.decomp:
+        return run_decomp(args, world, rank, local)
     return run_ours(args, world, rank, local)
 
 

@@ -81,8 +81,10 @@ class LocalSlabs:
         self.buf = torch.empty(nd, dtype=torch.float64, device=device)
 
     def set_prims(self, p8):
+        """p8: the global user prims [8][n3][n2][n1] (numpy, or a torch CUDA tensor)."""
         for g, z0, nz in self.parts:
-            g.set_prims(p8[:, z0:z0 + nz].copy())
+            x = p8[:, z0:z0 + nz]
+            g.set_prims(x.contiguous() if hasattr(x, "contiguous") else x.copy())
 
     def exchange(self):
         E, n = self.E, len(self.parts)
