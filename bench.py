@@ -363,7 +363,7 @@ def run_ours(args, world, rank, local):
 
     # ---------------- end to end through the C-ABI with HOST buffers
     host_in = torch.empty(P8.shape, dtype=torch.float64, pin_memory=True)
-    host_in.copy_(P8)
+    host_in.copy_(P8 if torch.is_tensor(P8) else torch.from_numpy(P8))
     host_out = torch.empty(P8.shape, dtype=torch.float64, pin_memory=True)
     del P8
     torch.cuda.empty_cache()
