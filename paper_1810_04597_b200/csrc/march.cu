@@ -1,11 +1,11 @@
 // march.cu — the axis-sweep kernels K2x/K2y/K2z as a marching pipeline
 // (DESIGN.md §2 step 2, rows a1-a5; §7).
 //
-// A persistent CTA owns a group of NL lines (x sweep: 4 lines x 32 cells,
-// 128 threads (one warp per line), 6 CTAs/SM; y/z sweeps: 8 consecutive x-lines = 64-byte rows x
-// 16 cells, 128 threads, 4 CTAs/SM — several CTAs per SM so that their phases
-// desynchronise and the FP64 pipe stays fed across the barriers) and marches
-// along the sweep axis in chunks of CH cells.  Thread i
+// A persistent CTA owns a group of NL lines and marches along them in chunks of
+// CH cells: x sweep 4 lines x 32 cells, 128 threads (one warp per line), 6 CTAs/SM;
+// y/z sweeps 8 consecutive x-lines (64-byte rows) x 4 cells = one warp per CTA,
+// 12 CTAs/SM.  In both every exchange of the march stays inside a warp, so the
+// chunk barriers are warp barriers and the warps run decoupled.  Thread i
 // of a line handles, in chunk c (base B = CH c):
 //   A  WENO5 of reconstructed cell B+3+i (8 variables, both faces; a2) and the
 //      A31 jump flag of face B+3+i
@@ -40,8 +40,8 @@ namespace march {
 #endif
 #ifndef ECHO_YZ_NL
 #define ECHO_YZ_NL 8
-#define ECHO_YZ_CH 16
-#define ECHO_YZ_BPS 4
+#define ECHO_YZ_CH 4
+#define ECHO_YZ_BPS 12
 #endif
 struct GeomSpec {
   int nl, ch, bps;
@@ -60,17 +60,22 @@ struct Geo {
   static constexpr int LOG_NL = ilog2(NL);
   static constexpr int LOG_CH = ilog2(CH);
   // ring length for primitives and face fluxes: >= CH + 10 live entries (a power of two when cheap)
-  static constexpr int RING = (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
+  static constexpr int RING = (CH + 10 <= 16) ? 16 : (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
+  // face-flux ring: B(c) writes faces B+2..B+CH+1 while faces B-2..B+1 are still needed by D(c+1)
+  static constexpr int RINGF = (CH + 4 <= 8) ? 8 : (CH + 4 <= 32) ? 32 : (CH + 4 <= 64) ? 64 : CH + 16;
+  // first chunk: its A phase reaches down to the ghost cell -3 (WENO of cells -3.. for faces -3..)
+  static constexpr int C_FIRST = -((6 + CH - 1) / CH);
+  static constexpr int B_FIRST = C_FIRST * CH;
   // ring length (bytes per line) of the A31 face flags: written in A for faces B+3..B+CH+2 while D
   // reads faces B-CH-2..B+1 in the same barrier interval -> >= 2 CH + 5
-  static constexpr int RR = (2 * CH + 5 <= 64) ? 64 : (2 * CH + 5 <= 128) ? 128 : 256;
+  static constexpr int RR = (2 * CH + 5 <= 16) ? 16 : (2 * CH + 5 <= 64) ? 64 : (2 * CH + 5 <= 128) ? 128 : 256;
   static constexpr int THREADS = NL * CH;
   static constexpr int BPS = S.bps;
   static constexpr int DELTA = (AX == 0) ? 1 : NL;           // lane distance between slots i and i+1
   static constexpr int SLOTS_PER_WARP = 32 / DELTA;           // consecutive slots inside one warp
   static constexpr int NEDGE = CH / SLOTS_PER_WARP;           // warp-edge slots per line
   static constexpr int VP = NL * RING;                        // variable stride, primitive ring
-  static constexpr int VF = NL * RING;                        // component stride, F ring
+  static constexpr int VF = NL * RINGF;                       // component stride, F ring
   static constexpr int VA = NL * CH;                          // component stride, accumulation buffer
   static constexpr int VE = NL * NEDGE;                       // variable stride, edge buffers
   static constexpr int OFF_P = 0;
@@ -82,9 +87,11 @@ struct Geo {
   static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RR;  // + A31 flag ring (bytes)
   // x sweep with one warp per line: every exchange of the march (ring, edges, flags, loads) stays
   // inside the warp, so the chunk barriers are warp barriers and the warps run decoupled
-  static constexpr bool WARP_LOCAL = (AX == 0 && CH == 32);
+  // (likewise any one-warp CTA, e.g. y/z: 8 lines x 4 cells)
+  static constexpr bool WARP_LOCAL = (AX == 0 && CH == 32) || THREADS == 32;
   static_assert(is_pow2(NL) && is_pow2(CH), "NL and CH must be powers of two");
-  static_assert(CH >= 16 && THREADS <= 1024 && (AX == 0 ? CH >= 32 : NL <= 32), "unsupported line geometry");
+  static_assert(CH >= 4 && THREADS <= 1024 && THREADS >= 32 && (AX == 0 ? CH >= 32 : NL <= 32),
+                "unsupported line geometry");
   static_assert(AX != 0 || NL * CH <= 1024, "x geometry");
   // a ring position of cell/face x (x may be negative)
   static ECHO_HD int ring(int x) {
@@ -97,6 +104,19 @@ struct Geo {
     else return p >= RING ? p - RING : (p < 0 ? p + RING : p);
   }
 };
+
+template <int AX>
+ECHO_HD int ringf(int x) {
+  constexpr int RF = Geo<AX>::RINGF;
+  if constexpr (is_pow2(RF)) return x & (RF - 1);
+  else return ((x % RF) + RF) % RF;
+}
+template <int AX>
+ECHO_HD int wrapf(int p) {
+  constexpr int RF = Geo<AX>::RINGF;
+  if constexpr (is_pow2(RF)) return p & (RF - 1);
+  else return p >= RF ? p - RF : (p < 0 ? p + RF : p);
+}
 
 template <int AX, int LEN>
 ECHO_HD int loff(int t, int pos) {  // conflict-free: slot/position fastest for x, line fastest for y/z
@@ -193,8 +213,8 @@ ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int 
   const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
   if (vec && (t & 1)) return;
   const long long lb = line_base<AX>(g, lg, t0, zz, t);
-  load_cells<AX>(g, lg, lb, t, -kG + i, vec, P, UB, sbase);
-  if (i < 2 * kG) load_cells<AX>(g, lg, lb, t, -kG + GE::CH + i, vec, P, UB, sbase);
+#pragma unroll
+  for (int x = -kG + i; x <= GE::B_FIRST + 2 * GE::CH + 4; x += GE::CH) load_cells<AX>(g, lg, lb, t, x, vec, P, UB, sbase);
 }
 
 template <int AX, bool KS, int DER, int REC, bool DN>
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         const double* __restrict__ UB, double* R) {
   using GE = Geo<AX>;
-  constexpr int CH = GE::CH, RING = GE::RING, RR = GE::RR;
+  constexpr int CH = GE::CH, RING = GE::RING, RINGF = GE::RINGF, RR = GE::RR;
   extern __shared__ double smem[];
   unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RR] face flags
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
@@ -228,12 +248,13 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
     const long long as = axis_stride<AX>(g);
     const int tt = min(t0 + t, lg.nt - 1);
     const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
-    int rb = GE::ring(-CH);  // ring position of the chunk base B
+    int rb = GE::ring(GE::B_FIRST);  // primitive-ring position of the chunk base B
+    int rbf = ringf<AX>(GE::B_FIRST);  // face-flux-ring position of B
     // Chunk c (base B = c CH): A = WENO of cells B+3+i, B = HLL at faces B+2+i, D = DER + flux
     // difference of the cells of chunk c-1 (their faces up to B+1 were written by B(c-1)), so one
     // chunk needs two barriers.  c = -1 is the prologue (A/B of the line start), c = nchunks the
     // epilogue (D of the last chunk).
-    for (int c = -1; c <= lg.nchunks; c++, rb = GE::wrap(rb + CH)) {
+    for (int c = GE::C_FIRST; c <= lg.nchunks; c++, rb = GE::wrap(rb + CH), rbf = wrapf<AX>(rbf + CH)) {
       const int B = c * CH;
       const int par = c & 1;
       const bool ab = c < lg.nchunks;       // A and B phases
@@ -260,7 +281,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) and the A31 flag of face xr ----
       const int rr = GE::wrap(rb + 3 + i);  // ring position of xr
       double qL[8], qR[8];
-      if (!(ab && (c >= 0 || i >= CH - 6))) {  // the prologue needs cells -3..2 only
+      if (!(ab && B + 3 + i >= -3)) {  // the prologue needs cells -3..2 only
 #pragma unroll
         for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
       } else {
@@ -299,7 +320,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         for (int m = 0; m < 5; m++) plain |= rough[t * RR + ((X0 + i - 2 + m) & (RR - 1))] != 0;  // A31
         int fpos[5];
 #pragma unroll
-        for (int m = 0; m < 5; m++) fpos[m] = loff<AX, RING>(t, GE::wrap(rb - CH + i - 2 + m));
+        for (int m = 0; m < 5; m++) fpos[m] = loff<AX, RINGF>(t, wrapf<AX>(rbf - CH + i - 2 + m));
 #pragma unroll
         for (int q = 0; q < 7; q++) {
           const double* Fq = smem + GE::OFF_F + q * GE::VF;
@@ -322,7 +343,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 
       {  // prefetch: the next chunk's CH new cells, or the next line group's first window
          // (the prologue's window already holds chunk 0's cells)
-        if (c < 0 || c >= lg.nchunks) {
+        if (c <= GE::C_FIRST || c >= lg.nchunks) {  // (the window holds the first two chunks)
         } else if (c + 1 < lg.nchunks) {
           if (!(vec && (t & 1))) load_cells<AX>(g, lg, lb, t, B + CH + kG + i, vec, P, UB, sbase);
         } else if (unit + gridDim.x < lg.nunits) {
@@ -367,7 +388,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           for (int v = 0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + eslot_in * GE::NL + t];
         }
         const int xf = B + 2 + i;
-        if (c >= 0 || i >= CH - 5) {
+        if (xf >= -3) {
           double F[7];
           if (KS) {
             const int af = max(-kG, min(xf + 1, lg.na + kG));  // face af - 1/2
@@ -379,7 +400,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           } else {
             hll_face(FlatMet(), e, pl, qR, AX, F);
           }
-          const int fp = loff<AX, RING>(t, GE::wrap(rr - 1));
+          const int fp = loff<AX, RINGF>(t, wrapf<AX>(rbf + 2 + i));
 #pragma unroll
           for (int q = 0; q < 7; q++) smem[GE::OFF_F + q * GE::VF + fp] = F[q];
         }
