@@ -187,10 +187,19 @@ def run_reference(args, world, rank):
     out = {"impl": "reference", "metric": METRIC, "value": zu, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
            "warmup": W, "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"cfg{args.config} recipe, {n}^3 sample", "grid": [n, n, n]},
+           "config": workload_config(args, I.problem(args.config), world=1),
            "cpu_baseline": {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": zu, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def workload_config(args, p, world):
+    """The `config` object of both arms (the reference arm times a bounded sample of it)."""
+    return {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
+                        f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[args.rec]}+HLL+DER6+field-CD, SSP-RK3",
+            "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
+            "step": "echo_max_dt + echo_step (3 stages x [3 sweeps + update])"}
 
 
 # ------------------------------------------------- ours, z-slab decomposition
@@ -397,11 +406,7 @@ def run_ours(args, world, rank, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
-                                   f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[p.rec]}+HLL+DER6+field-CD, SSP-RK3",
-                       "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
-                       "step": "echo_max_dt + echo_step (3 stages x [3 sweeps + update])"},
+            "config": workload_config(args, p, world),
             "hbm_roofline": hbm, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,
             "counters": {"floor_events": st["floor_events"], "c2p_failures": st["c2p_failures"]},
