@@ -228,7 +228,7 @@ def run_decomp(args, world, rank, local):
     stream = torch.cuda.current_stream(dev)
     P8 = I.initial_prims(p, device=dev)
     if world == 1:
-        S = slab.LocalSlabs(p, args.slabs, device=dev)
+        S = slab.LocalSlabs(p, args.slabs, device=dev, fused=args.fused)
         S.set_prims(P8)
         launches0 = sum(echo.launch_count(g.ctx) for g, _, _ in S.parts)
 
@@ -276,7 +276,7 @@ def run_decomp(args, world, rank, local):
                "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
                                       f"{REC_NAMES[p.rec]}+HLL+DER6+field-CD, SSP-RK3",
                           "grid": list(p.n), "parallelism": f"{nslab} z-slabs" + (f" on {world} GPUs (NCCL P2P ghost exchange)"
-                                                                                 if world > 1 else " on 1 GPU (device-copy exchange)"),
+                                                                                 if world > 1 else (" on 1 GPU (ghost planes stored by the update kernels)" if args.fused else " on 1 GPU (device-copy exchange)")),
                           "step": "min-reduced CFL dt + 3 x (ghost exchange + echo_stage)"},
                "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(out), flush=True)
@@ -430,6 +430,8 @@ def main(argv=None):
     ap.add_argument("--decomp", action="store_true",
                     help="z-slab domain decomposition (strong scaling; default N>1 mode is independent replicas)")
     ap.add_argument("--slabs", type=int, default=2, help="--decomp on one GPU: slabs held by this process")
+    ap.add_argument("--fused", action="store_true",
+                    help="--decomp on one GPU: the update kernels store the neighbours' ghost planes (echo_halo_link)")
     ap.add_argument("--rec", type=int, default=0, choices=[0, 1, 2],
                     help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5")
     ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")

@@ -156,6 +156,12 @@ int echo_con2prim(echo_ctx* ctx, echo_stats_t* delta);
  * Stages must be issued in order 1, 2, 3 (ECHO_E_ORDER otherwise).  Asynchronous. */
 int echo_stage(echo_ctx* ctx, int s, double dt);
 
+/* The two halves of echo_stage(s, dt): the axis sweeps of stage s (L of the stage
+ * input), then the K3 update (sources, curl, RK combine, con2prim; slab mode: the
+ * fused ghost stores of echo_halo_link).  In order, without other stage calls between. */
+int echo_stage_sweeps(echo_ctx* ctx, int s);
+int echo_stage_update(echo_ctx* ctx, int s, double dt);
+
 /* One full SSP-RK3 step (stages 1, 2, 3) with dt > 0.  Asynchronous. */
 int echo_step(echo_ctx* ctx, double dt);
 
@@ -177,6 +183,14 @@ int echo_stats(echo_ctx* ctx, echo_stats_t* out);
  * Call them between stages (after the previous stage / echo_set_prims, before
  * echo_stage), on the context stream; device buffers stay stream-ordered. */
 long long echo_halo_doubles(const echo_ctx* ctx);
+/* Fused exchange: link `side` of ctx to the slab `peer` (in this process; another
+ * device needs peer access enabled).  From then on the update of each stage also
+ * stores the new P and U of ctx's 6 planes next to `side` straight into peer's ghost
+ * planes (and, on a physical outflow side, replicates the edge plane into ctx's own
+ * ghost planes): no export/import is needed.  The caller orders, per stage,
+ * echo_stage_sweeps on every slab before echo_stage_update on any (the update
+ * overwrites ghost planes the neighbour's sweeps read).  peer = NULL unlinks. */
+int echo_halo_link(echo_ctx* ctx, int side, echo_ctx* peer);
 int echo_halo_export(echo_ctx* ctx, int side, double* buf, int on_device);
 int echo_halo_import(echo_ctx* ctx, int side, const double* buf, int on_device);
 int echo_halo_fill(echo_ctx* ctx, int side);

@@ -39,6 +39,8 @@ struct echo_ctx {
   double* tables = nullptr;
   // cell-interleaved device state (echo_kernels.h): 8 doubles per cell each
   double* alloc_base[4] = {nullptr, nullptr, nullptr, nullptr};  // allocations (slab mode: incl. ghost planes)
+  echo_ctx* link[2] = {nullptr, nullptr};  // slab mode: neighbours whose ghost planes K3 writes (echo_halo_link)
+  int swept = 0;                           // stage whose sweeps ran (echo_stage_sweeps), 0 = none
   size_t plane = 0;       // doubles per z plane of a record array (pitch n2)
   double* Un = nullptr;   // U^n
   double* Us = nullptr;   // U^s
@@ -116,23 +118,53 @@ static int run_sweeps(echo_ctx* c) {
   return ECHO_OK;
 }
 
-static int run_stage(echo_ctx* c, int s, double dt) {
+// the fused ghost exchange of slab mode for stage s (targets: the linked neighbours' P and
+// same-role U arrays, shifted so that my record offset lands in their ghost planes)
+static GhostLinks ghost_links(echo_ctx* c, int s) {
+  GhostLinks gl{};
+  if (!c->g.zhalo) return gl;
+  const long long plane = (long long)c->g.n[1] * c->g.pitch;
+  for (int side = 0; side < 2; side++) {
+    echo_ctx* nb = c->link[side];
+    if (nb) {
+      // side 0: my plane k (< 6) -> the lower neighbour's plane nz_nb + k;
+      // side 1: my plane k (>= nz - 6) -> the upper neighbour's plane k - nz
+      const long long shift = side == 0 ? (long long)nb->g.n[2] * plane : -(long long)c->g.n[2] * plane;
+      gl.dstP[side] = nb->P + shift;
+      gl.dstU[side] = (s == 3 ? nb->Un : nb->Us) + shift;
+      gl.on = 1;
+    }
+    if (c->g.bc[2][side] == ECHO_BC_OUTFLOW) {
+      gl.replicate[side] = 1;
+      gl.on = 1;
+    }
+  }
+  return gl;
+}
+
+static int run_update(echo_ctx* c, int s, double dt) {
   const double* Uin = (s == 1) ? c->Un : c->Us;
-  int rc = run_sweeps(c);
-  if (rc) return rc;
   double* Uout = (s == 3) ? c->Un : c->Us;
   // the last stage also reduces the CFL rate of the new state (a9 fused into K3)
   unsigned long long* cfl = (s == 3) ? c->dcnt + 2 : nullptr;
   if (cfl) CK(cudaMemsetAsync(cfl, 0, sizeof(unsigned long long), c->st), "stage");
+  const GhostLinks gl = ghost_links(c, s);
   cudaError_t e = launch(c, kUpdateStage, [&] {
     return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Un, Uin, Uout, c->P, nullptr,
-                         c->dcnt, cfl, c->st);
+                         c->dcnt, cfl, c->st, &gl);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
   c->cfl_valid = (s == 3);
   c->stages++;
   c->next_stage = (s == 3) ? 1 : s + 1;
+  c->swept = 0;
   return ECHO_OK;
+}
+
+static int run_stage(echo_ctx* c, int s, double dt) {
+  int rc = run_sweeps(c);
+  if (rc) return rc;
+  return run_update(c, s, dt);
 }
 
 extern "C" {
@@ -324,6 +356,7 @@ int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
   c->have_state = true;
   c->cfl_valid = false;
   c->next_stage = 1;
+  c->swept = 0;
   return ECHO_OK;
 }
 
@@ -451,7 +484,7 @@ int echo_stage(echo_ctx* c, int s, double dt) {
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage: no state (call echo_set_prims first)");
   if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage: s must be 1, 2 or 3");
-  if (s != c->next_stage) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
+  if (s != c->next_stage || c->swept) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage: dt > 0 violated");
   return run_stage(c, s, dt);
 }
@@ -505,7 +538,41 @@ int echo_stats(echo_ctx* c, echo_stats_t* out) {
   return ECHO_OK;
 }
 
+// ------------------------------------------------------------ stage halves
+int echo_stage_sweeps(echo_ctx* c, int s) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: no state");
+  if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage_sweeps: s must be 1, 2 or 3");
+  if (s != c->next_stage || c->swept) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: stages must run in order");
+  int rc = run_sweeps(c);
+  if (rc) return rc;
+  c->swept = s;
+  return ECHO_OK;
+}
+
+int echo_stage_update(echo_ctx* c, int s, double dt) {
+  if (!c) return ECHO_E_ARG;
+  if (c->swept != s) return fail(c, ECHO_E_ORDER, "echo_stage_update: echo_stage_sweeps(s) must come first");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage_update: dt > 0 violated");
+  return run_update(c, s, dt);
+}
+
 // ------------------------------------------------------------ slab halos
+int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
+  if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_link: bad argument") : ECHO_E_ARG;
+  if (!peer) {
+    c->link[side] = nullptr;
+    return ECHO_OK;
+  }
+  if (!c->g.zhalo || c->g.bc[2][side] != ECHO_BC_HALO || !peer->g.zhalo || peer->g.bc[2][1 - side] != ECHO_BC_HALO)
+    return fail(c, ECHO_E_ARG, "echo_halo_link: both facing sides must be halo boundaries");
+  if (peer->g.n[0] != c->g.n[0] || peer->g.n[1] != c->g.n[1] || peer->g.pitch != c->g.pitch || peer->ks != c->ks)
+    return fail(c, ECHO_E_ARG, "echo_halo_link: the slabs must share n[0], n[1] and the metric");
+  c->link[side] = peer;
+  return ECHO_OK;
+}
+
+
 long long echo_halo_doubles(const echo_ctx* c) {
   if (!c || !c->g.zhalo) return 0;
   return 2LL * ECHO_HALO_PLANES * (long long)c->plane;

@@ -2,6 +2,7 @@
 // con2prim Newton (A8, A27, A28), floors (A9) and the metric sources (a6).
 #pragma once
 #include "echo_dev.cuh"
+#include "echo_kernels.h"
 
 namespace echo {
 constexpr int kCellThreads = 256;
@@ -286,7 +287,7 @@ ECHO_D double cfl_rate(const M& m, const GridP& g, const EosP& e, const double* 
 template <bool KS, bool DIVB_NONE>
 ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* __restrict__ R,
                       const double* Un, const double* Us, double* Uout, double* P, int i, int j, int k,
-                      bool want_rate, double& rate) {
+                      bool want_rate, double& rate, const GhostLinks* gl = nullptr) {
   const auto m = MetAt<KS>::get(mt, i, j);
   const long long rb = rec_base(g, i, j, k), vs = g.vs;
   double Pp[8];
@@ -322,6 +323,27 @@ ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s,
   st8(Uout + rb, vs, Uo);
   st_prims<KS>(P + rb, vs, Po);
   if (want_rate) rate = fmax(rate, cfl_rate(m, g, e, Po));  // a9 fused: CFL rate of the new state
+  if (gl && gl->on) {  // slab mode: the fused ghost exchange (echo_halo_link) and outflow replication
+    const long long plane = (long long)g.n[1] * g.pitch;
+    if (k < kZH && gl->dstP[0]) {
+      st_prims<KS>(gl->dstP[0] + rb, vs, Po);
+      st8(gl->dstU[0] + rb, vs, Uo);
+    }
+    if (k >= g.n[2] - kZH && gl->dstP[1]) {
+      st_prims<KS>(gl->dstP[1] + rb, vs, Po);
+      st8(gl->dstU[1] + rb, vs, Uo);
+    }
+    if (k == 0 && gl->replicate[0])
+      for (int h = 1; h <= kZH; h++) {
+        st_prims<KS>(P + rb - h * plane, vs, Po);
+        st8(Uout + rb - h * plane, vs, Uo);
+      }
+    if (k == g.n[2] - 1 && gl->replicate[1])
+      for (int h = 1; h <= kZH; h++) {
+        st_prims<KS>(P + rb + h * plane, vs, Po);
+        st8(Uout + rb + h * plane, vs, Uo);
+      }
+  }
   return ev;
 }
 

@@ -19,6 +19,19 @@ namespace echo {
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
                          const double* UB, double* R, cudaStream_t st);
 
+// slab mode, fused ghost exchange: K3 also stores the new P and U of the owned planes
+// next to a linked side straight into the neighbour slab's ghost planes (peer memory:
+// the same device, or another GPU over NVLink), and replicates the edge plane into its
+// own ghost planes on a physical outflow side.  dstP/dstU[side]: the neighbour's P /
+// (same-role) U array shifted so that adding a cell's record offset gives the target
+// ghost cell; NULL = not linked.
+struct GhostLinks {
+  double* dstP[2];
+  double* dstU[2];
+  int replicate[2];
+  int on;
+};
+
 // K3 modes
 enum UpdateMode { kModeStage = 0, kModeRhs = 1, kModeC2P = 2 };
 
@@ -28,7 +41,8 @@ enum UpdateMode { kModeStage = 0, kModeRhs = 1, kModeC2P = 2 };
 // max-speed reduction (a9) of the new state, fused into the same pass.
 cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                           const double* R, const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                          unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st);
+                          unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st,
+                          const GhostLinks* links = nullptr);
 
 // a9: per-cell sum_a max|lambda_a|/Delta_a, max-reduced into *out (u64 bit pattern, zeroed by caller)
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,

@@ -37,7 +37,7 @@ template <bool KS, int MODE, bool DIVB_NONE>
 __global__ void __launch_bounds__(kCellThreads, 3)
 k_update(const GridP g, const EosP e, const MetTables mt, const int s, const double dt, const double* __restrict__ R,
          const double* Un, const double* Us, double* Uout, double* P, double* __restrict__ Lout,
-         unsigned long long* counters, unsigned long long* cfl_out) {
+         unsigned long long* counters, unsigned long long* cfl_out, const GhostLinks gl) {
   const long long N = g.N;
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = id < N;
@@ -47,7 +47,7 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
     int i, j, k;
     cell_ijk(g, id, i, j, k);
     if (MODE == kModeStage) {
-      ev = stage_cell<KS, DIVB_NONE>(g, e, mt, s, dt, R, Un, Us, Uout, P, i, j, k, cfl_out != nullptr, rate);
+      ev = stage_cell<KS, DIVB_NONE>(g, e, mt, s, dt, R, Un, Us, Uout, P, i, j, k, cfl_out != nullptr, rate, &gl);
     } else {
       const auto m = MetAt<KS>::get(mt, i, j);
       const long long rb = rec_base(g, i, j, k), vs = g.vs;
@@ -90,29 +90,32 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
 template <bool KS, int MODE>
 static cudaError_t upd2(const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* R,
                         const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st) {
+                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st, const GhostLinks& gl) {
   unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
   if (g.divb == 1)
-    k_update<KS, MODE, true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl);
+    k_update<KS, MODE, true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, gl);
   else
-    k_update<KS, MODE, false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl);
+    k_update<KS, MODE, false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, gl);
   return cudaGetLastError();
 }
 
 template <bool KS>
 static cudaError_t upd1(int mode, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* R,
                         const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st) {
-  if (mode == kModeRhs) return upd2<KS, kModeRhs>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, nullptr, st);
-  if (mode == kModeC2P) return upd2<KS, kModeC2P>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st);
-  return upd2<KS, kModeStage>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st);
+                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st, const GhostLinks& gl) {
+  if (mode == kModeRhs) return upd2<KS, kModeRhs>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, nullptr, st, gl);
+  if (mode == kModeC2P) return upd2<KS, kModeC2P>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st, gl);
+  return upd2<KS, kModeStage>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st, gl);
 }
 
 cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                           const double* R, const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                          unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st) {
-  if (ks) return upd1<true>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st);
-  return upd1<false>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st);
+                          unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st,
+                          const GhostLinks* links) {
+  GhostLinks none{};
+  const GhostLinks& gl = links ? *links : none;
+  if (ks) return upd1<true>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st, gl);
+  return upd1<false>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st, gl);
 }
 
 // ------------------------------------------------------ CFL reduction (a9)

@@ -74,6 +74,9 @@ _sig = {
     "echo_kernel_name": (C.c_char_p, [C.c_int]),
     "echo_launch_count": (C.c_longlong, [_P]),
     "echo_halo_doubles": (C.c_longlong, [_P]),
+    "echo_halo_link": (C.c_int, [_P, C.c_int, _P]),
+    "echo_stage_sweeps": (C.c_int, [_P, C.c_int]),
+    "echo_stage_update": (C.c_int, [_P, C.c_int, C.c_double]),
     "echo_halo_export": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_import": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_fill": (C.c_int, [_P, C.c_int]),
@@ -235,6 +238,18 @@ def kernel_name(i: int) -> str:
 
 def launch_count(ctx) -> int:
     return int(_lib.echo_launch_count(ctx))
+
+
+def halo_link(ctx, side: int, peer):
+    return _check(ctx, _lib.echo_halo_link(ctx, int(side), peer))
+
+
+def stage_sweeps(ctx, s: int):
+    return _check(ctx, _lib.echo_stage_sweeps(ctx, int(s)))
+
+
+def stage_update(ctx, s: int, dt: float):
+    return _check(ctx, _lib.echo_stage_update(ctx, int(s), float(dt)))
 
 
 def halo_doubles(ctx) -> int:

@@ -63,9 +63,11 @@ def slab_problem(problem, rank: int, nranks: int):
 
 class LocalSlabs:
     """All slabs of one grid in one process (one GPU): the decomposed step with the
-    ghost exchange done by device-to-device copies between the contexts."""
+    ghost exchange done by device-to-device copies between the contexts, or, fused=True,
+    by the update kernels storing their edge planes straight into the neighbours' ghost
+    planes (echo_halo_link; per stage all sweeps, then all updates)."""
 
-    def __init__(self, problem, nslabs: int, device="cuda"):
+    def __init__(self, problem, nslabs: int, device="cuda", fused: bool = False):
         import torch
 
         from . import echo as E
@@ -79,12 +81,21 @@ class LocalSlabs:
             self.parts.append((E.Echo(sp), z0, nz))
         nd = E.halo_doubles(self.parts[0][0].ctx)
         self.buf = torch.empty(nd, dtype=torch.float64, device=device)
+        self.fused = fused
+        if fused:
+            for r, (g, _, _) in enumerate(self.parts):
+                lo, hi = neighbours(r, nslabs, self.periodic)
+                for side, nb in ((LOWER, lo), (UPPER, hi)):
+                    if nb is not None:
+                        E.halo_link(g.ctx, side, self.parts[nb][0].ctx)
 
     def set_prims(self, p8):
         """p8: the global user prims [8][n3][n2][n1] (numpy, or a torch CUDA tensor)."""
         for g, z0, nz in self.parts:
             x = p8[:, z0:z0 + nz]
             g.set_prims(x.contiguous() if hasattr(x, "contiguous") else x.copy())
+        if self.fused:  # the first stage's ghosts; later ones are written by the updates
+            self.exchange()
 
     def exchange(self):
         E, n = self.E, len(self.parts)
@@ -101,10 +112,17 @@ class LocalSlabs:
         return min(g.max_dt(cfl) for g, _, _ in self.parts)
 
     def step(self, dt: float):
+        E = self.E
         for s in (1, 2, 3):
-            self.exchange()
-            for g, _, _ in self.parts:
-                g.stage(s, dt)
+            if self.fused:
+                for g, _, _ in self.parts:
+                    E.stage_sweeps(g.ctx, s)
+                for g, _, _ in self.parts:
+                    E.stage_update(g.ctx, s, dt)
+            else:
+                self.exchange()
+                for g, _, _ in self.parts:
+                    g.stage(s, dt)
 
     def gather(self, getter):
         import numpy as np
@@ -112,6 +130,12 @@ class LocalSlabs:
         return np.concatenate([getter(g) for g, _, _ in self.parts], axis=-3)
 
     def close(self):
+        for g, _, _ in self.parts:
+            for side in (LOWER, UPPER):
+                try:
+                    self.E.halo_link(g.ctx, side, None)
+                except Exception:
+                    pass
         for g, _, _ in self.parts:
             g.close()
 

@@ -27,20 +27,24 @@ def E():
     return echo
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("cfg,n,nslabs,steps", [
     (0, (32, 24, 32), 2, 3),     # periodic turbulence: a ring of 2 (both neighbours the same slab)
     (0, (20, 16, 40), 3, 3),     # periodic, 3 unequal slabs (14/13/13 planes)
+    (0, (16, 16, 16), 1, 2),     # one periodic slab: its own neighbour on both sides
     (2, (24, 20, 36), 3, 3),     # outflow blast: physical ends filled locally, shocks crossing slab edges
     (4, (48, 24, 24), 2, 2),     # Kerr-Schild torus, slabs in phi
 ])
-def test_slabs_match_single_domain_bitwise(E, orc, cfg, n, nslabs, steps):
+def test_slabs_match_single_domain_bitwise(E, orc, cfg, n, nslabs, steps, fused):
+    """fused=False: export/copy/import before every stage; fused=True: the updates store
+    their edge planes into the neighbours' ghost planes (echo_halo_link)."""
     from paper_1810_04597_b200.slab import LocalSlabs
 
     p = I.problem(cfg, n=n)
     P8 = I.initial_prims(p)
     one = E.Echo(p)
     one.set_prims(P8)
-    sl = LocalSlabs(p, nslabs)
+    sl = LocalSlabs(p, nslabs, fused=fused)
     sl.set_prims(P8)
     for _ in range(steps):
         dt1 = one.max_dt(p.cfl)
