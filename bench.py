@@ -241,10 +241,15 @@ def run_decomp(args, world, rank, local):
         echo.set_stream(g.ctx, stream.cuda_stream)
         g.set_prims(P8[:, z0:z0 + nz].contiguous())
         D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev)
+        if args.fused:  # neighbours' arrays mapped by CUDA IPC; the updates store the ghost planes
+            D.link_fused()
         launches0 = echo.launch_count(g.ctx)
 
         def one_step():
             dt = D.min_dt(g.max_dt(p.cfl))
+            if args.fused:
+                D.step_fused(dt)
+                return
             for s in (1, 2, 3):
                 D.exchange()
                 g.stage(s, dt)
@@ -275,7 +280,7 @@ def run_decomp(args, world, rank, local):
                "dtype": "f64", "data": "synthetic",
                "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
                                       f"{REC_NAMES[p.rec]}+HLL+DER6+field-CD, SSP-RK3",
-                          "grid": list(p.n), "parallelism": f"{nslab} z-slabs" + (f" on {world} GPUs (NCCL P2P ghost exchange)"
+                          "grid": list(p.n), "parallelism": f"{nslab} z-slabs" + (f" on {world} GPUs (" + ("ghost planes stored by the update kernels over CUDA IPC / NVLink" if args.fused else "NCCL P2P ghost exchange") + ")"
                                                                                  if world > 1 else (" on 1 GPU (ghost planes stored by the update kernels)" if args.fused else " on 1 GPU (device-copy exchange)")),
                           "step": "min-reduced CFL dt + 3 x (ghost exchange + echo_stage)"},
                "gpu_launches": int(launches), "clocks": clocks}

@@ -191,6 +191,19 @@ long long echo_halo_doubles(const echo_ctx* ctx);
  * echo_stage_sweeps on every slab before echo_stage_update on any (the update
  * overwrites ghost planes the neighbour's sweeps read).  peer = NULL unlinks. */
 int echo_halo_link(echo_ctx* ctx, int side, echo_ctx* peer);
+/* The same link to a slab owned by another process (one process per GPU): the
+ * peer exports its arrays' CUDA IPC handles (echo_ipc_export: 3 x 64 bytes into
+ * `handles`, its n[2] into *nz), this process maps them (echo_halo_link_ipc; the
+ * peer's n[0], n[1] must equal ctx's; handles = NULL unlinks and unmaps).  Across
+ * processes the stage ordering is the caller's: every rank's sweeps of stage s
+ * complete before any neighbour's update of stage s, and every update before the
+ * neighbours' next sweeps (slab.DistSlab: stream sync + barrier). */
+int echo_ipc_export(echo_ctx* ctx, void* handles, int* nz);
+/* Fill the ghost planes of `side` by reading the linked neighbour's 6 edge planes
+ * (P and the stage-input U) through the link — the first stage's ghosts after
+ * echo_set_prims; later stages get theirs from the neighbour's update. */
+int echo_halo_pull(echo_ctx* ctx, int side);
+int echo_halo_link_ipc(echo_ctx* ctx, int side, const void* handles, int peer_nz);
 int echo_halo_export(echo_ctx* ctx, int side, double* buf, int on_device);
 int echo_halo_import(echo_ctx* ctx, int side, const double* buf, int on_device);
 int echo_halo_fill(echo_ctx* ctx, int side);

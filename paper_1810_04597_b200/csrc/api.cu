@@ -40,6 +40,14 @@ struct echo_ctx {
   // cell-interleaved device state (echo_kernels.h): 8 doubles per cell each
   double* alloc_base[4] = {nullptr, nullptr, nullptr, nullptr};  // allocations (slab mode: incl. ghost planes)
   echo_ctx* link[2] = {nullptr, nullptr};  // slab mode: neighbours whose ghost planes K3 writes (echo_halo_link)
+  // ... or a neighbour in another process: its P, Un, Us (plane 0) mapped by CUDA IPC
+  struct Remote {
+    double* base[3] = {nullptr, nullptr, nullptr};  // opened allocation bases (P, Un, Us)
+    double* P = nullptr;
+    double* Un = nullptr;
+    double* Us = nullptr;
+    int nz = 0;
+  } rlink[2];
   int swept = 0;                           // stage whose sweeps ran (echo_stage_sweeps), 0 = none
   size_t plane = 0;       // doubles per z plane of a record array (pitch n2)
   double* Un = nullptr;   // U^n
@@ -118,6 +126,15 @@ static int run_sweeps(echo_ctx* c) {
   return ECHO_OK;
 }
 
+static void ipc_close(echo_ctx::Remote& rm) {
+  for (double*& b : rm.base)
+    if (b) {
+      cudaIpcCloseMemHandle(b);
+      b = nullptr;
+    }
+  rm.P = rm.Un = rm.Us = nullptr;
+}
+
 // the fused ghost exchange of slab mode for stage s (targets: the linked neighbours' P and
 // same-role U arrays, shifted so that my record offset lands in their ghost planes)
 static GhostLinks ghost_links(echo_ctx* c, int s) {
@@ -126,12 +143,20 @@ static GhostLinks ghost_links(echo_ctx* c, int s) {
   const long long plane = (long long)c->g.n[1] * c->g.pitch;
   for (int side = 0; side < 2; side++) {
     echo_ctx* nb = c->link[side];
+    const echo_ctx::Remote& rm = c->rlink[side];
+    double *nP = nullptr, *nUn = nullptr, *nUs = nullptr;
+    int nnz = 0;
     if (nb) {
+      nP = nb->P, nUn = nb->Un, nUs = nb->Us, nnz = nb->g.n[2];
+    } else if (rm.P) {
+      nP = rm.P, nUn = rm.Un, nUs = rm.Us, nnz = rm.nz;
+    }
+    if (nP) {
       // side 0: my plane k (< 6) -> the lower neighbour's plane nz_nb + k;
       // side 1: my plane k (>= nz - 6) -> the upper neighbour's plane k - nz
-      const long long shift = side == 0 ? (long long)nb->g.n[2] * plane : -(long long)c->g.n[2] * plane;
-      gl.dstP[side] = nb->P + shift;
-      gl.dstU[side] = (s == 3 ? nb->Un : nb->Us) + shift;
+      const long long shift = side == 0 ? (long long)nnz * plane : -(long long)c->g.n[2] * plane;
+      gl.dstP[side] = nP + shift;
+      gl.dstU[side] = (s == 3 ? nUn : nUs) + shift;
       gl.on = 1;
     }
     if (c->g.bc[2][side] == ECHO_BC_OUTFLOW) {
@@ -299,6 +324,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
 
 void echo_destroy(echo_ctx* c) {
   if (!c) return;
+  for (auto& rm : c->rlink) ipc_close(rm);
   for (double* b : c->alloc_base) cudaFree(b);
   cudaFree(c->scratch);
   cudaFree(c->dcnt);
@@ -558,6 +584,67 @@ int echo_stage_update(echo_ctx* c, int s, double dt) {
 }
 
 // ------------------------------------------------------------ slab halos
+// CUDA IPC: the allocation handles of P, Un, Us (3 x cudaIpcMemHandle_t) and n[2]
+int echo_ipc_export(echo_ctx* c, void* handles, int* nz) {
+  if (!c || !handles) return c ? fail(c, ECHO_E_ARG, "echo_ipc_export: NULL buffer") : ECHO_E_ARG;
+  if (!c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_ipc_export: the context has no halo boundary");
+  cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(handles);
+  const int slot[3] = {2, 0, 1};  // P, Un, Us
+  for (int q = 0; q < 3; q++) CK(cudaIpcGetMemHandle(&h[q], c->alloc_base[slot[q]]), "echo_ipc_export");
+  if (nz) *nz = c->g.n[2];
+  return ECHO_OK;
+}
+
+int echo_halo_link_ipc(echo_ctx* c, int side, const void* handles, int peer_nz) {
+  if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_link_ipc: bad argument") : ECHO_E_ARG;
+  ipc_close(c->rlink[side]);
+  if (!handles) return ECHO_OK;
+  if (!c->g.zhalo || c->g.bc[2][side] != ECHO_BC_HALO || peer_nz < ECHO_HALO_PLANES)
+    return fail(c, ECHO_E_ARG, "echo_halo_link_ipc: the side must be a halo boundary facing a slab of >= 6 planes");
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+  echo_ctx::Remote& rm = c->rlink[side];
+  for (int q = 0; q < 3; q++) {
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      ipc_close(rm);
+      return cuda_fail(c, e, "echo_halo_link_ipc");
+    }
+    rm.base[q] = static_cast<double*>(p);
+  }
+  // the peer's arrays start kZH ghost planes into their allocations (same n[0], n[1], pitch)
+  const long long ghost = (long long)kZH * (long long)c->g.n[1] * c->g.pitch;
+  rm.P = rm.base[0] + ghost;
+  rm.Un = rm.base[1] + ghost;
+  rm.Us = rm.base[2] + ghost;
+  rm.nz = peer_nz;
+  return ECHO_OK;
+}
+
+// fill the ghost planes of `side` from the linked neighbour's edge planes (peer / IPC reads)
+int echo_halo_pull(echo_ctx* c, int side) {
+  if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_pull: bad argument") : ECHO_E_ARG;
+  echo_ctx* nb = c->link[side];
+  const echo_ctx::Remote& rm = c->rlink[side];
+  double *nP = nullptr, *nU = nullptr;
+  int nnz = 0;
+  const bool first = c->next_stage == 1;  // the stage-input role of U: U^n before stage 1, U^s after
+  if (nb) {
+    nP = nb->P, nU = first ? nb->Un : nb->Us, nnz = nb->g.n[2];
+  } else if (rm.P) {
+    nP = rm.P, nU = first ? rm.Un : rm.Us, nnz = rm.nz;
+  } else {
+    return fail(c, ECHO_E_ORDER, "echo_halo_pull: the side is not linked");
+  }
+  const long long plane = (long long)c->g.n[1] * c->g.pitch;
+  const long long src_k = side == 0 ? nnz - ECHO_HALO_PLANES : 0;
+  const long long dst_k = side == 0 ? -ECHO_HALO_PLANES : c->g.n[2];
+  const size_t bytes = sizeof(double) * ECHO_HALO_PLANES * plane;
+  CK(cudaMemcpyAsync(c->P + dst_k * plane, nP + src_k * plane, bytes, cudaMemcpyDefault, c->st), "echo_halo_pull");
+  CK(cudaMemcpyAsync(ucur_mut(c) + dst_k * plane, nU + src_k * plane, bytes, cudaMemcpyDefault, c->st), "echo_halo_pull");
+  return ECHO_OK;
+}
+
 int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
   if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_link: bad argument") : ECHO_E_ARG;
   if (!peer) {

@@ -75,6 +75,9 @@ _sig = {
     "echo_launch_count": (C.c_longlong, [_P]),
     "echo_halo_doubles": (C.c_longlong, [_P]),
     "echo_halo_link": (C.c_int, [_P, C.c_int, _P]),
+    "echo_ipc_export": (C.c_int, [_P, _P, C.POINTER(C.c_int)]),
+    "echo_halo_link_ipc": (C.c_int, [_P, C.c_int, _P, C.c_int]),
+    "echo_halo_pull": (C.c_int, [_P, C.c_int]),
     "echo_stage_sweeps": (C.c_int, [_P, C.c_int]),
     "echo_stage_update": (C.c_int, [_P, C.c_int, C.c_double]),
     "echo_halo_export": (C.c_int, [_P, C.c_int, _P, C.c_int]),
@@ -242,6 +245,25 @@ def launch_count(ctx) -> int:
 
 def halo_link(ctx, side: int, peer):
     return _check(ctx, _lib.echo_halo_link(ctx, int(side), peer))
+
+
+def ipc_export(ctx):
+    """(bytes of the 3 CUDA IPC handles of P, Un, Us, n[2]) of a slab context."""
+    buf = C.create_string_buffer(3 * 64)
+    nz = C.c_int(0)
+    _check(ctx, _lib.echo_ipc_export(ctx, buf, C.byref(nz)))
+    return buf.raw, nz.value
+
+
+def halo_link_ipc(ctx, side: int, handles, peer_nz: int):
+    if handles is None:
+        return _check(ctx, _lib.echo_halo_link_ipc(ctx, int(side), None, 0))
+    buf = C.create_string_buffer(bytes(handles), len(handles))
+    return _check(ctx, _lib.echo_halo_link_ipc(ctx, int(side), buf, int(peer_nz)))
+
+
+def halo_pull(ctx, side: int):
+    return _check(ctx, _lib.echo_halo_pull(ctx, int(side)))
 
 
 def stage_sweeps(ctx, s: int):

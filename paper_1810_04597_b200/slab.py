@@ -144,7 +144,12 @@ class DistSlab:
     """This rank's slab under torch.distributed: point-to-point ghost exchange with the
     z neighbours (send my boundary planes, receive theirs), min-reduced CFL dt.
     `io` supplies export(side, buf) / import_(side, buf) / fill(side) / halo_doubles
-    (the library context by default; a host stand-in in the CPU tests)."""
+    (the library context by default; a host stand-in in the CPU tests).
+
+    Fused mode (`link_fused`, GPUs): the neighbours' arrays are mapped by CUDA IPC and
+    every update stores its edge planes straight into them (NVLink peer stores); a
+    step is then, per stage, sweeps -> stream sync + barrier -> update -> sync +
+    barrier, with no data messages at all."""
 
     def __init__(self, io, rank: int, nranks: int, periodic: bool, device):
         import torch
@@ -183,6 +188,43 @@ class DistSlab:
             else:
                 self.io.import_(side, self.recv[side])
 
+    def link_fused(self):
+        """Exchange the slabs' IPC handles and link both z sides (a self-neighbour, i.e. a
+        single periodic rank, links in-process); then pull the first stage's ghosts."""
+        import torch.distributed as dist
+
+        mine = self.io.ipc_export()
+        allh = [None] * self.n
+        dist.all_gather_object(allh, mine)
+        for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
+            if nb is None:
+                continue
+            if nb == self.rank:
+                self.io.link_self(side)
+            else:
+                self.io.link_ipc(side, *allh[nb])
+        self.fused = True
+        self.barrier()
+        for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
+            if nb is None:
+                self.io.fill(side)
+            else:
+                self.io.pull(side)
+        self.barrier()
+
+    def barrier(self):
+        import torch.distributed as dist
+
+        self.io.sync()
+        dist.barrier()
+
+    def step_fused(self, dt: float):
+        for s in (1, 2, 3):
+            self.io.sweeps(s)
+            self.barrier()   # every neighbour finished reading the ghost planes my update overwrites
+            self.io.update(s, dt)
+            self.barrier()   # my ghost planes hold the neighbours' new edge planes
+
     def min_dt(self, dt_local: float) -> float:
         import torch
         import torch.distributed as dist
@@ -216,3 +258,21 @@ class CtxIO:
         import torch
 
         torch.cuda.current_stream().synchronize()
+
+    def ipc_export(self):
+        return self.E.ipc_export(self.g.ctx)
+
+    def link_ipc(self, side, handles, nz):
+        self.E.halo_link_ipc(self.g.ctx, side, handles, nz)
+
+    def link_self(self, side):
+        self.E.halo_link(self.g.ctx, side, self.g.ctx)
+
+    def pull(self, side):
+        self.E.halo_pull(self.g.ctx, side)
+
+    def sweeps(self, s):
+        self.E.stage_sweeps(self.g.ctx, s)
+
+    def update(self, s, dt):
+        self.E.stage_update(self.g.ctx, s, dt)
