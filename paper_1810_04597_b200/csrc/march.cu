@@ -7,21 +7,25 @@
 // 12 CTAs/SM.  In both every exchange of the march stays inside a warp, so the
 // chunk barriers are warp barriers and the warps run decoupled.  Thread i
 // of a line handles, in chunk c (base B = CH c):
-//   A  WENO5 of reconstructed cell B+3+i (8 variables, both faces; a2) and the
-//      A31 jump flag of face B+3+i
-//   B  HLL flux at face B+2+i (a3): the left state comes from thread i-1
-//      (warp shuffle; across warps and chunks through a small edge buffer)
-//   C1 DER6 at face B+i from the F ring (a4)
-//   C2 flux difference + field-CD EMF of cell B+i (a5)
+//   A  WENO5 (or MP5) of reconstructed cell B+3+i (8 variables, both faces; a2)
+//      and the A31 jump flag of face B+3+i
+//   D1 DER6 (a4) at the right face of cell B-CH+i of the previous chunk (its
+//      5-face stencil ends at face B+1, written by B(c-1)); edge lanes publish it
+//   -- barrier (1): primitives of chunk c dead, edges visible; prefetch chunk c+1 --
+//   D2 the left face from lane i-1 (shuffle / edge buffer), the flux difference
+//      into the rhs and the field-CD EMF (a5) of cell B-CH+i
+//   B  HLL flux at face B+2+i (a3): the left state comes from lane i-1 (warp
+//      shuffle; the first slot from the previous chunk through an edge buffer)
+//   -- barrier (0) of chunk c+1 --
 // so every reconstruction, every face flux and every DER value is computed
-// exactly once per line: no tile halo is recomputed (the 6 cells / 5 faces /
-// 1 DER value of overlap are carried from the previous chunk), and every lane
-// is busy in every phase.  A prologue chunk c = -1 computes the carried values
-// of the line start.  Primitives stream through a ring of >= CH + 10 cells in
-// shared memory: the next chunk's CH cells (or the next line group's first window) are
-// prefetched with cp.async as soon as phase A has consumed the current ones; the
-// ghost fill (a1) is the index map of those loads.  Results are bitwise
-// deterministic (fixed per-thread operation order).
+// exactly once per line (no tile halo), and a chunk needs two barriers.  The
+// first chunk starts at C_FIRST = -ceil(6/CH) so that A reaches the ghost cell
+// -3; one epilogue chunk (D only) finishes the line.  Primitives stream through a
+// ring of >= CH + 10 cells in shared memory: the next chunk's CH cells (or the
+// next line group's first window) are prefetched with cp.async as soon as phase A
+// has consumed the current ones; the ghost fill (a1) is the index map of those
+// loads (slab mode: stored ghost planes).  Results are bitwise deterministic
+// (fixed per-lane operation order).
 #include <cuda_runtime.h>
 
 #include "echo_dev.cuh"
