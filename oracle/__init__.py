@@ -140,6 +140,7 @@ def lib():
             "orc_sources_pt": (C.c_int, [P, _D, _D, _D]),
             "orc_weno5_left": (C.c_double, [_D, C.c_int]),
             "orc_mp5_left": (C.c_double, [_D]),
+            "orc_wenoz_left": (C.c_double, [_D]),
             "orc_der": (C.c_double, [_D, C.c_int]),
             "orc_c2p_pt": (C.c_int, [P, _D, _D, _D, _D, C.POINTER(C.c_int)]),
             "orc_set_prims": (C.c_int, [P, _D, _D, _D, _LL]),
@@ -225,6 +226,10 @@ def weno5_left(u, rec: int = 0) -> float:
 
 def mp5_left(u) -> float:
     return float(lib().orc_mp5_left(_p(_v(u, 5))))
+
+
+def wenoz_left(u) -> float:
+    return float(lib().orc_wenoz_left(_p(_v(u, 5))))
 
 
 def der(F, order: int = 6) -> float:

@@ -143,8 +143,31 @@ double orc_mp5_left(const double u[5]) {
   return median3(u_or, u_min, u_max);
 }
 
-/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5 */
+/* WENO-Z (Borges, Carmona, Costa & Don 2008, J. Comput. Phys. 227, 3191: eqs. 24-28),
+ * point-value candidates and ideal weights as WENO5 (A2), the same Jiang-Shu beta_k;
+ * alpha_k = d_k (1 + tau5 / (beta_k + eps)) with tau5 = |beta_0 - beta_2|, eps = 1e-40
+ * (their value; reading A34).  Left-biased value at i+1/2 from u[0..4] = u_{i-2..i+2}. */
+double orc_wenoz_left(const double u[5]) {
+  const double eps = 1e-40;
+  double b0 = 13.0 / 12.0 * (u[0] - 2.0 * u[1] + u[2]) * (u[0] - 2.0 * u[1] + u[2])
+            + 0.25 * (u[0] - 4.0 * u[1] + 3.0 * u[2]) * (u[0] - 4.0 * u[1] + 3.0 * u[2]);
+  double b1 = 13.0 / 12.0 * (u[1] - 2.0 * u[2] + u[3]) * (u[1] - 2.0 * u[2] + u[3])
+            + 0.25 * (u[1] - u[3]) * (u[1] - u[3]);
+  double b2 = 13.0 / 12.0 * (u[2] - 2.0 * u[3] + u[4]) * (u[2] - 2.0 * u[3] + u[4])
+            + 0.25 * (3.0 * u[2] - 4.0 * u[3] + u[4]) * (3.0 * u[2] - 4.0 * u[3] + u[4]);
+  double q0 = (3.0 * u[0] - 10.0 * u[1] + 15.0 * u[2]) / 8.0;
+  double q1 = (-u[1] + 6.0 * u[2] + 3.0 * u[3]) / 8.0;
+  double q2 = (3.0 * u[2] + 6.0 * u[3] - u[4]) / 8.0;
+  double tau5 = fabs(b0 - b2);
+  double a0 = 1.0 / 16.0 * (1.0 + tau5 / (b0 + eps));
+  double a1 = 10.0 / 16.0 * (1.0 + tau5 / (b1 + eps));
+  double a2 = 5.0 / 16.0 * (1.0 + tau5 / (b2 + eps));
+  return (a0 * q0 + a1 * q1 + a2 * q2) / (a0 + a1 + a2);
+}
+
+/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z */
 static double orc_rec_left(const double u[5], int rec) {
+  if (rec == 3) return orc_wenoz_left(u);
   return rec == 2 ? orc_mp5_left(u) : orc_weno5_left(u, rec);
 }
 

@@ -19,9 +19,10 @@ constexpr int kZH = 6; // stored z ghost planes per side in slab mode (kG + 1: t
 // constant bank, so every DFMA takes them as a c[][] operand (otherwise the
 // compiler rebuilds each one with a pair of UMOVs at every use).
 //   [0..2] DER6 symmetric-sum weights 1067/960, -29/480, 3/640; [3..4] DER4 13/12, -1/24
-//   [5] WENO5 eps scaled by 3 (weno5_both), [6] 1/6 (FV candidates), [7] 4/3 (MP5 u_lc)
-static __constant__ double kCst[8] = {1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0, 13.0 / 12.0, -1.0 / 24.0,
-                                      3.0e-6, 1.0 / 6.0, 4.0 / 3.0};
+//   [5] WENO5 eps scaled by 3 (weno5_both), [6] 1/6 (FV candidates), [7] 4/3 (MP5 u_lc),
+//   [8] WENO-Z eps scaled by 3
+static __constant__ double kCst[9] = {1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0, 13.0 / 12.0, -1.0 / 24.0,
+                                      3.0e-6, 1.0 / 6.0, 4.0 / 3.0, 3.0e-40};
 
 struct GridP {
   int n[3];
@@ -311,9 +312,10 @@ ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
 //    (3u_0 - 4u_1 + u_2) = d2p - 2dp; since sum(omega) = 1 each face value is
 //    u_0 + sum_k omega_k (q_k - u_0) with the candidate increments q_k - u_0
 //    linear in the differences (2 flops each instead of 5).
+// REC 0: point form (A2), 1: finite-volume form, 3: WENO-Z weights on the point form (A34)
 template <int REC>
 ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
-  const double eps3 = kCst[5];
+  const double eps3 = REC == 3 ? kCst[8] : kCst[5];
   const double dmm = um1 - um2, dm = u0 - um1, dp = up1 - u0, dpp = up2 - up1;
   // 3 beta_k as quadratic forms of the first differences (12 beta_k = 13 t^2 + 3 tb^2):
   //   3 beta_0 = 10 dm^2 - 11 dm dmm + 4 dmm^2
@@ -324,6 +326,22 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
   double s0 = fma(10.0, m2, fma(dmm, fma(4.0, dmm, -11.0 * dm), eps3));
   double s1 = fma(4.0, m2, fma(4.0, p2, fma(-5.0 * dm, dp, eps3)));
   double s2 = fma(10.0, p2, fma(dpp, fma(4.0, dpp, -11.0 * dp), eps3));
+  if constexpr (REC == 3) {
+    // WENO-Z: alpha_k = d_k (1 + tau5 / s_k), tau5 = |s_0 - s_2| (the common factor 3 of s_k and
+    // tau5 cancels); times s_0 s_1 s_2: A_k = (s_k + tau5) prod_{l != k} s_l.  The mirror face
+    // swaps s_0 and s_2, i.e. A_0 <-> A_2, with the same candidate increments as the point form.
+    const double tau = fabs(s0 - s2);
+    const double A0 = (s0 + tau) * (s1 * s2), A1 = (s1 + tau) * (s0 * s2), A2 = (s2 + tau) * (s0 * s1);
+    const double C0 = fma(0.875, dm, -0.375 * dmm), C1 = fma(1.25, dm, 3.75 * dp), C2 = fma(3.125, dp, -0.625 * dpp);
+    const double E0 = fma(0.375, dpp, -0.875 * dp), E1 = fma(-1.25, dp, -3.75 * dm), E2 = fma(0.625, dmm, -3.125 * dm);
+    const double SL = fma(10.0, A1, fma(5.0, A2, A0)), SR = fma(10.0, A1, fma(5.0, A0, A2));
+    const double NL = fma(A2, C2, fma(A1, C1, A0 * C0));
+    const double NR = fma(A0, E2, fma(A1, E1, A2 * E0));
+    const double inv = frcp(SL * SR);
+    qL = fma(NL, SR * inv, u0);
+    qR = fma(NR, SL * inv, u0);
+    return;
+  }
   s0 *= s0;
   s1 *= s1;
   s2 *= s2;
@@ -400,7 +418,7 @@ ECHO_D void mp5_both(double um2, double um1, double u0, double up1, double up2, 
   qR = mp5_face(up2, up1, u0, um1, um2, m4m, m4p);
 }
 
-// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5
+// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z
 template <int REC>
 ECHO_D void rec_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
   if constexpr (REC == 2) mp5_both(um2, um1, u0, up1, up2, qL, qR);

@@ -229,7 +229,22 @@ def mp5(u):
     return sorted([u_or, lo, hi])[1] if lo <= hi else u_or + minmod(lo - u_or, hi - u_or)
 
 
+def wenoz(u):
+    """WENO-Z (Borges et al. 2008) on the point form, eps = 1e-40 (A34)."""
+    eps = mp.mpf("1e-40")
+    b = [mp.mpf(13) / 12 * (u[0] - 2 * u[1] + u[2]) ** 2 + (u[0] - 4 * u[1] + 3 * u[2]) ** 2 / 4,
+         mp.mpf(13) / 12 * (u[1] - 2 * u[2] + u[3]) ** 2 + (u[1] - u[3]) ** 2 / 4,
+         mp.mpf(13) / 12 * (u[2] - 2 * u[3] + u[4]) ** 2 + (3 * u[2] - 4 * u[3] + u[4]) ** 2 / 4]
+    q = [(3 * u[0] - 10 * u[1] + 15 * u[2]) / 8, (-u[1] + 6 * u[2] + 3 * u[3]) / 8, (3 * u[2] + 6 * u[3] - u[4]) / 8]
+    d = [mp.mpf(1) / 16, mp.mpf(10) / 16, mp.mpf(5) / 16]
+    tau = abs(b[0] - b[2])
+    al = [d[k] * (1 + tau / (b[k] + eps)) for k in range(3)]
+    return sum(al[k] * q[k] for k in range(3)) / sum(al)
+
+
 def rec_left(u, rec):
+    if rec == 3:
+        return wenoz(u)
     return mp5(u) if rec == 2 else weno(u, rec)
 
 

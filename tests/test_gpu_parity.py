@@ -121,12 +121,14 @@ def test_multistep_parity(E, orc, cfg, n, steps):
     assert_groups(g.get_prims(), orc.get_prims(oc, U, P), PRIM8_GROUPS, TOL_10, what="get_prims")
 
 
-@pytest.mark.parametrize("cfg,n,steps", [(0, (32, 32, 32), 10), (2, (40, 40, 40), 10), (4, (64, 32, 16), 5)])
-def test_multistep_parity_mp5(E, orc, cfg, n, steps):
-    """MP5 reconstruction (rec=2, A33): multi-step parity, incl. the blast
-    (limiter active at the shock) and the Kerr-Schild torus."""
+@pytest.mark.parametrize("cfg,n,steps,rec", [(0, (32, 32, 32), 10, 2), (2, (40, 40, 40), 10, 2),
+                                              (4, (64, 32, 16), 5, 2), (0, (32, 32, 32), 10, 3),
+                                              (2, (40, 40, 40), 10, 3)])
+def test_multistep_parity_mp5(E, orc, cfg, n, steps, rec):
+    """MP5 (rec=2, A33) and WENO-Z (rec=3, A34) reconstruction: multi-step
+    parity, incl. the blast (limiter active at the shock) and the Kerr-Schild torus."""
     p = small_problem(cfg, n)
-    p.rec = 2
+    p.rec = rec
     P8 = I.initial_prims(p)
     oc = ocfg(orc, p)
     U, P = orc.set_prims(oc, P8)
@@ -140,8 +142,8 @@ def test_multistep_parity_mp5(E, orc, cfg, n, steps):
         ocnt[1] += cnt[1]
         g.step(dt)
     gn, _, gp = g.get_state()
-    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"mp5 {steps} steps U cfg{cfg}")
-    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"mp5 {steps} steps P cfg{cfg}")
+    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"rec{rec} {steps} steps U cfg{cfg}")
+    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"rec{rec} {steps} steps P cfg{cfg}")
     st = g.stats()
     assert (st["floor_events"], st["c2p_failures"]) == tuple(ocnt)
 
@@ -170,7 +172,7 @@ def test_con2prim_parity(E, orc):
 def test_switches_parity(E, orc):
     # rec=FV, der=4, divb=none on a multi-tile grid
     p = small_problem(0, (70, 9, 10))
-    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}):
+    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}, {"rec": 3}):
         for k, v in kw.items():
             setattr(p, k, v)
         P8 = I.initial_prims(p)

@@ -106,6 +106,38 @@ def test_mp5_order_and_linear_limit(orc):
         assert math.log2(a / b) > 4.5, e
 
 
+# ------------------------------------------------------------------ WENO-Z (rec=3, A34)
+def test_wenoz_worked_values(orc):
+    for c in (0.0, 1.0, -3.7, 1e5):
+        assert orc.wenoz_left([c] * 5) == pytest.approx(c, rel=1e-15, abs=1e-300)
+    assert orc.wenoz_left([1, 2, 3, 4, 5]) == pytest.approx(3.5, rel=1e-15)
+    # x^2: the three beta_k are equal (13/3), tau5 = 0 -> ideal weights -> exact 1/4
+    assert orc.wenoz_left([4, 1, 0, 1, 4]) == pytest.approx(0.25, rel=1e-15)
+
+
+def _henrick(orc, f, N, A):
+    # Henrick et al. (2005) critical-point test: u = sin(pi x - sin(pi x)/pi) has u' = 0 with a non-zero
+    # third derivative; amplitude A >> 1 puts beta_k >> eps
+    g = lambda x: np.sin(np.pi * x - np.sin(np.pi * x) / np.pi)
+    h = 2.0 / N
+    x = -1 + np.arange(N) * h
+    u = A * g(x)
+    return max(abs(f([u[(i + m) % N] for m in range(-2, 3)]) - A * g(x[i] + h / 2)) for i in range(N)) / A
+
+
+def test_wenoz_critical_points(orc):
+    # the property WENO-Z was designed for (Borges et al. 2008): 5th order at critical points,
+    # where WENO5-JS with eps small against beta drops towards 4th (measured here: 4.1)
+    ez = [_henrick(orc, orc.wenoz_left, N, 1e3) for N in (80, 160, 320, 640)]
+    ej = [_henrick(orc, lambda u: orc.weno5_left(u, 0), N, 1e3) for N in (80, 160, 320, 640)]
+    assert all(math.log2(a / b) > 4.9 for a, b in zip(ez, ez[1:])), ez
+    assert math.log2(ej[-2] / ej[-1]) < 4.3, ej
+    # and close to the ideal (linear) 5-point interpolant there
+    lin = np.array([3.0, -20.0, 90.0, 60.0, -5.0]) / 128.0
+    el = _henrick(orc, lambda u: float(lin @ np.asarray(u)), 640, 1e3)
+    assert ez[-1] == pytest.approx(el, rel=0.05)
+
+
 # ------------------------------------------------------------------ DER
 def test_der_values(orc):
     for o in (2, 4, 6):
