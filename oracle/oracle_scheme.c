@@ -165,8 +165,22 @@ double orc_wenoz_left(const double u[5]) {
   return (a0 * q0 + a1 * q1 + a2 * q2) / (a0 + a1 + a2);
 }
 
-/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z */
+/* MC2: the monotonized-central limited linear reconstruction (van Leer 1977), the
+ * "limited" second-order entry of SURVEY f3 (reading A35): left value at i+1/2 =
+ * u_i + slope/2 with slope = minmod(2 (u_i - u_{i-1}), (u_{i+1} - u_{i-1}) / 2,
+ * 2 (u_{i+1} - u_i)); uses u[1..3] of the 5-point stencil. */
+double orc_mc2_left(const double u[5]) {
+  const double dl = u[2] - u[1], dr = u[3] - u[2], dc = 0.5 * (u[3] - u[1]);
+  double slope;
+  if (dl > 0.0 && dr > 0.0) slope = fmin(fmin(2.0 * dl, dc), 2.0 * dr);
+  else if (dl < 0.0 && dr < 0.0) slope = fmax(fmax(2.0 * dl, dc), 2.0 * dr);
+  else slope = 0.0;
+  return u[2] + 0.5 * slope;
+}
+
+/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2 */
 static double orc_rec_left(const double u[5], int rec) {
+  if (rec == 4) return orc_mc2_left(u);
   if (rec == 3) return orc_wenoz_left(u);
   return rec == 2 ? orc_mp5_left(u) : orc_weno5_left(u, rec);
 }

@@ -418,10 +418,22 @@ ECHO_D void mp5_both(double um2, double um1, double u0, double up1, double up2, 
   qR = mp5_face(up2, up1, u0, um1, um2, m4m, m4p);
 }
 
-// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z
+// MC2 (A35): u_i +- slope/2 with the monotonized-central slope; the mirror face has the
+// negated slope exactly (minmod is odd)
+ECHO_D void mc2_both(double um1, double u0, double up1, double& qL, double& qR) {
+  const double dl = u0 - um1, dr = up1 - u0, dc = 0.5 * (up1 - um1);
+  double slope = 0.0;
+  if (dl > 0.0 && dr > 0.0) slope = dmin(dmin(2.0 * dl, dc), 2.0 * dr);
+  else if (dl < 0.0 && dr < 0.0) slope = dmax(dmax(2.0 * dl, dc), 2.0 * dr);
+  qL = u0 + 0.5 * slope;
+  qR = u0 + 0.5 * -slope;
+}
+
+// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2
 template <int REC>
 ECHO_D void rec_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
-  if constexpr (REC == 2) mp5_both(um2, um1, u0, up1, up2, qL, qR);
+  if constexpr (REC == 4) mc2_both(um1, u0, up1, qL, qR);
+  else if constexpr (REC == 2) mp5_both(um2, um1, u0, up1, up2, qL, qR);
   else weno5_both<REC>(um2, um1, u0, up1, up2, qL, qR);
 }
 

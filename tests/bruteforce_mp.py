@@ -242,7 +242,19 @@ def wenoz(u):
     return sum(al[k] * q[k] for k in range(3)) / sum(al)
 
 
+def mc2(u):
+    """MC2 limited linear reconstruction (A35)."""
+    dl, dr, dc = u[2] - u[1], u[3] - u[2], (u[3] - u[1]) / 2
+    if dl > 0 and dr > 0:
+        return u[2] + min(2 * dl, dc, 2 * dr) / 2
+    if dl < 0 and dr < 0:
+        return u[2] + max(2 * dl, dc, 2 * dr) / 2
+    return u[2]
+
+
 def rec_left(u, rec):
+    if rec == 4:
+        return mc2(u)
     if rec == 3:
         return wenoz(u)
     return mp5(u) if rec == 2 else weno(u, rec)

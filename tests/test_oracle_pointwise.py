@@ -138,6 +138,34 @@ def test_wenoz_critical_points(orc):
     assert ez[-1] == pytest.approx(el, rel=0.05)
 
 
+# ------------------------------------------------------------------ MC2 (rec=4, A35)
+def test_mc2_values_and_tvd(orc):
+    for c in (0.0, 1.0, -3.7):
+        assert orc.mc2_left([c] * 5) == c
+    assert orc.mc2_left([1, 2, 3, 4, 5]) == 3.5          # linear data: exact
+    assert orc.mc2_left([4, 1, 0, 1, 4]) == 0.0          # an extremum: first order (slope 0)
+    assert orc.mc2_left([0, 0, 0, 1, 1]) == 0.0          # a step: no overshoot
+    assert orc.mc2_left([0, 0, 1, 1, 1]) == 1.0
+    rng = np.random.default_rng(9)
+    for _ in range(2000):  # TVD: the face value stays between u_i and u_{i+1}
+        u = rng.standard_normal(5)
+        q = orc.mc2_left(u)
+        assert min(u[2], u[3]) - 1e-15 <= q <= max(u[2], u[3]) + 1e-15 or \
+            (u[2] - u[1]) * (u[3] - u[2]) <= 0 and q == u[2]
+
+
+def test_mc2_order(orc):
+    # second order on smooth monotone data (no extrema in the stencils)
+    def err(N):
+        h = 1.0 / N
+        x = np.arange(N) * h
+        u = np.exp(x)
+        return max(abs(orc.mc2_left(u[i - 2:i + 3]) - math.exp(x[i] + h / 2)) for i in range(2, N - 2))
+    e = [err(N) for N in (32, 64, 128)]
+    for a, b in zip(e, e[1:]):
+        assert 1.9 < math.log2(a / b) < 2.1, e
+
+
 # ------------------------------------------------------------------ DER
 def test_der_values(orc):
     for o in (2, 4, 6):
