@@ -274,3 +274,34 @@ def test_errors_are_loud(E):
     assert ei.value.code == E.E_ORDER
     with pytest.raises(E.EchoError):
         E.create(n=(0, 4, 4), lo=(0, 0, 0), hi=(1, 1, 1), bc=((0, 0),) * 3)
+
+
+# ------------------------------------------------------------ degenerate grids
+@pytest.mark.parametrize("n,bc", [
+    ((16, 1, 1), ((0, 0), (0, 0), (0, 0))),   # 1-D along x (the y/z sweeps see single-cell lines)
+    ((1, 16, 1), ((0, 0), (0, 0), (0, 0))),   # 1-D along y
+    ((1, 1, 16), ((0, 0), (0, 0), (0, 0))),   # 1-D along z
+    ((4, 4, 4), ((0, 0), (0, 0), (0, 0))),    # every axis shorter than the 5-cell halo (wrap mod n, A12)
+    ((5, 3, 7), ((1, 1), (1, 1), (1, 1))),    # outflow everywhere, odd sizes below one chunk
+    ((33, 2, 9), ((0, 0), (1, 1), (0, 0))),   # one cell past a 32-cell chunk, 2-cell outflow axis
+])
+def test_degenerate_grids_parity(E, orc, n, bc):
+    """Edge cases of the march: lines shorter than a chunk or the halo, single-cell axes,
+    ragged chunk tails; stage-chained parity and 3 steps."""
+    p = I.problem(0, n=n)
+    p.bc = bc
+    P8 = I.initial_prims(p)
+    oc = ocfg(orc, p)
+    U, P = orc.set_prims(oc, P8)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    dt = orc.max_dt(oc, U, P, p.cfl)
+    assert g.max_dt(p.cfl) == pytest.approx(dt, rel=1e-14)
+    assert_rhs_groups(g.rhs(), orc.rhs(oc, U, P), U, dt, CONS_GROUPS, TOL_STAGE, what=f"rhs {n}")
+    for _ in range(3):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        U, P, _ = orc.step(oc, dt, U, P)
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"3 steps U {n}")
+    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"3 steps P {n}")
