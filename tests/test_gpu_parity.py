@@ -305,3 +305,46 @@ def test_degenerate_grids_parity(E, orc, n, bc):
     gn, _, gp = g.get_state()
     assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"3 steps U {n}")
     assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"3 steps P {n}")
+
+
+def test_full_size_conservation_and_divb(E):
+    """Properties that hold at any size, checked at BASELINE.json's 512^3 (config 3, the
+    bench workload and launch configuration): periodic Minkowski -> the sums of
+    sqrt(g) U are conserved to roundoff over 2 steps (P2), and the field-CD scheme keeps
+    the D2 divergence of B at roundoff (P3).  The reductions are test-side torch ops."""
+    import math
+
+    import torch
+
+    p = I.problem(3)
+    g = E.Echo(p)
+    P8 = I.initial_prims(p, device="cuda")
+    g.set_prims(P8)
+    del P8
+    N = p.ncells
+    U = torch.empty((8, N), dtype=torch.float64, device="cuda")
+
+    def sums_and_div():
+        E.get_cons(g.ctx, U)
+        torch.cuda.synchronize()
+        s = [float(U[q].sum()) for q in range(8)]
+        a = [float(U[q].abs().sum()) for q in range(8)]
+        B = U[5:8].view(3, p.n[2], p.n[1], p.n[0])
+        dx = 1.0 / p.n[0]
+        div = ((torch.roll(B[0], -1, 2) - torch.roll(B[0], 1, 2)) + (torch.roll(B[1], -1, 1) - torch.roll(B[1], 1, 1)) +
+               (torch.roll(B[2], -1, 0) - torch.roll(B[2], 1, 0))) / (2 * dx)
+        return s, a, float(div.abs().max()), float(B.abs().max())
+
+    s0, a0, d0, bmax = sums_and_div()
+    dx = 1.0 / p.n[0]
+    assert d0 < 100 * 2.2e-16 * bmax / dx
+    for _ in range(2):
+        g.step(g.max_dt(p.cfl))
+    s1, _, d1, _ = sums_and_div()
+    assert d1 < 100 * 2.2e-16 * bmax / dx, (d0, d1)
+    for q in range(8):
+        # summation error of the test's own float64 reductions (~sqrt(N) eps) dominates the bound
+        assert abs(s1[q] - s0[q]) <= 1e-12 * a0[q], (q, s0[q], s1[q], a0[q])
+    st = g.stats()
+    assert st["floor_events"] == 0 and st["c2p_failures"] == 0
+    g.close()
