@@ -37,6 +37,9 @@ namespace march {
 // Line-group geometry per sweep axis: NL lines x CH cells per chunk
 // (THREADS = NL CH), BPS CTAs per SM.  Overridable at build time for tuning
 // runs (-DECHO_YZ_NL=8 -DECHO_YZ_CH=32 -DECHO_YZ_BPS=2, likewise ECHO_X_*).
+#ifndef ECHO_BALLOT_FLAGS
+#define ECHO_BALLOT_FLAGS 1  // A31 flags as warp ballots + a per-line bit history (warp-local kernels)
+#endif
 #ifndef ECHO_X_NL
 #define ECHO_X_NL 4
 #define ECHO_X_CH 32
@@ -227,6 +230,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         const double* __restrict__ UB, double* R) {
   using GE = Geo<AX>;
   constexpr int CH = GE::CH, RING = GE::RING, RINGF = GE::RINGF, RR = GE::RR;
+  // A31 flags as ballots: warp-local kernels whose chunk of a line lies in one warp
+  constexpr bool kBallot = ECHO_BALLOT_FLAGS && GE::WARP_LOCAL && (AX == 0 ? CH == 32 : CH * GE::NL == 32);
   extern __shared__ double smem[];
   unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RR] face flags
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
@@ -252,6 +257,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
     const long long as = axis_stride<AX>(g);
     const int tt = min(t0 + t, lg.nt - 1);
     const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
+    unsigned long long fhist = 0ull;  // A31 flags of this line's faces, newest chunk in the top CH bits
     int rb = GE::ring(GE::B_FIRST);  // primitive-ring position of the chunk base B
     int rbf = ringf<AX>(GE::B_FIRST);  // face-flux-ring position of B
     // Chunk c (base B = c CH): A = WENO of cells B+3+i, B = HLL at faces B+2+i, D = DER + flux
@@ -285,11 +291,11 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       // ---- A: WENO5 of reconstructed cell xr = B+3+i (a2) and the A31 flag of face xr ----
       const int rr = GE::wrap(rb + 3 + i);  // ring position of xr
       double qL[8], qR[8];
+      bool rgh = false;
       if (!(ab && B + 3 + i >= -3)) {  // the prologue needs cells -3..2 only
 #pragma unroll
         for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
       } else {
-        bool rgh = false;
         int pos[5];
 #pragma unroll
         for (int m = 0; m < 5; m++) pos[m] = loff<AX, RING>(t, GE::wrap(rr - 2 + m));
@@ -308,7 +314,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
             rgh |= fabs(u[3] - u[2]) > g.der_jump * lo;
           }
         }
-        rough[t * RR + ((B + 3 + i) & (RR - 1))] = rgh;
+        if constexpr (!kBallot) rough[t * RR + ((B + 3 + i) & (RR - 1))] = rgh;
         if (edge_out) {  // publish the left state of cell xr for the slot to the right
           const int dpar = (i == CH - 1) ? ((c + 1) & 1) : par;
 #pragma unroll
@@ -316,12 +322,22 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         }
       }
 
+      unsigned fm = 0u;  // this chunk's CH flags of line t
+      if constexpr (kBallot) {
+        const unsigned b = __ballot_sync(0xffffffffu, rgh);
+        if constexpr (AX == 0) fm = b;  // lane = slot
+        else fm = (((b >> t) & 0x01010101u) * 0x10204080u) >> 28;  // lanes i*8 + t, i = 0..3
+      }
       // ---- D1: DER flux (a4) at the right face X0+i+1/2 of cell X0+i (faces X0+i-2..X0+i+2) ----
       double H[7];
       if (d2 || (c == 0 && i == CH - 1)) {  // c = 0: the left face -1/2 of cell 0, carried to D(1)
         bool plain = false;
 #pragma unroll
-        for (int m = 0; m < 5; m++) plain |= rough[t * RR + ((X0 + i - 2 + m) & (RR - 1))] != 0;  // A31
+        for (int m = 0; m < 5; m++)
+          if constexpr (!kBallot) plain |= rough[t * RR + ((X0 + i - 2 + m) & (RR - 1))] != 0;  // A31
+        if constexpr (kBallot) {  // faces X0+i-2+m: bits 59-CH+i+m of the line's history (chunk c-1 on top)
+          plain = ((fhist >> (59 - CH + i)) & 0x1Full) != 0;
+        }
         int fpos[5];
 #pragma unroll
         for (int m = 0; m < 5; m++) fpos[m] = loff<AX, RINGF>(t, wrapf<AX>(rbf - CH + i - 2 + m));
@@ -342,6 +358,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         for (int q = 0; q < 7; q++) H[q] = 0.0;
       }
       cp_async_wait0();  // the old rhs/EMF values of this thread's copies
+      if constexpr (kBallot) fhist = (fhist >> CH) | ((unsigned long long)fm << (64 - CH));
       if constexpr (GE::WARP_LOCAL) __syncwarp();
       else __syncthreads();  // (1) A and D1 done: primitives of chunk c dead, edges published, A buffer landed
 
