@@ -292,9 +292,13 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       const int rr = GE::wrap(rb + 3 + i);  // ring position of xr
       double qL[8], qR[8];
       bool rgh = false;
+      // inactive lanes' values are shuffled but never used; the x sweep zero-fills them all the
+      // same (without it ptxas spills at 80 registers), the y/z sweeps skip the fill
       if (!(ab && B + 3 + i >= -3)) {  // the prologue needs cells -3..2 only
+        if constexpr (AX == 0) {
 #pragma unroll
-        for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
+          for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
+        }
       } else {
         int pos[5];
 #pragma unroll
@@ -353,7 +357,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 #pragma unroll
           for (int q = 0; q < 7; q++) smem[GE::OFF_HE + dpar * 7 * GE::VE + q * GE::VE + eslot_out * GE::NL + t] = H[q];
         }
-      } else {
+      } else if constexpr (AX == 0) {
 #pragma unroll
         for (int q = 0; q < 7; q++) H[q] = 0.0;
       }
