@@ -74,7 +74,8 @@ typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_met
  * rec: 0 = WENO5 point-value form (A2, default), 1 = WENO5 finite-volume form,
  *      2 = MP5 (Suresh & Huynh 1997 on point values, reading A33),
  *      3 = WENO-Z (Borges et al. 2008 weights on the point form, reading A34),
- *      4 = MC2, the monotonized-central limited linear reconstruction (reading A35).
+ *      4 = MC2, the monotonized-central limited linear reconstruction (reading A35),
+ *      5 = PPM (Colella & Woodward 1984 constraints on point values, reading A36).
  * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
  * divb: 0 = field-CD constrained transport (A6, default), 1 = none.
  * der_jump: DER shock switch (A31): the DER correction at a face is dropped

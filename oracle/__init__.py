@@ -142,6 +142,7 @@ def lib():
             "orc_mp5_left": (C.c_double, [_D]),
             "orc_wenoz_left": (C.c_double, [_D]),
             "orc_mc2_left": (C.c_double, [_D]),
+            "orc_ppm_left": (C.c_double, [_D]),
             "orc_der": (C.c_double, [_D, C.c_int]),
             "orc_c2p_pt": (C.c_int, [P, _D, _D, _D, _D, C.POINTER(C.c_int)]),
             "orc_set_prims": (C.c_int, [P, _D, _D, _D, _LL]),
@@ -235,6 +236,10 @@ def wenoz_left(u) -> float:
 
 def mc2_left(u) -> float:
     return float(lib().orc_mc2_left(_p(_v(u, 5))))
+
+
+def ppm_left(u) -> float:
+    return float(lib().orc_ppm_left(_p(_v(u, 5))))
 
 
 def der(F, order: int = 6) -> float:

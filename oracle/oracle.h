@@ -55,7 +55,8 @@ typedef struct {
   int rec;           /* 0 WENO5 point-value form (A2), 1 WENO5 finite-volume form,
                         2 MP5 (Suresh & Huynh 1997, point values, A33),
                         3 WENO-Z (Borges et al. 2008, point values, A34),
-                        4 MC2 (monotonized-central limited linear, A35) */
+                        4 MC2 (monotonized-central limited linear, A35),
+                        5 PPM (Colella & Woodward 1984 on point values, A36) */
   int der;           /* 6 DER6, 4 DER4, 2 plain difference (A5) */
   int divb;          /* 0 field-CD (A6), 1 none: plain flux difference for B */
   double der_jump;   /* A31 DER switch: the DER correction at a face is dropped (H = F) when a face
@@ -91,6 +92,8 @@ double orc_mp5_left(const double u[5]);
 double orc_wenoz_left(const double u[5]);
 /* MC2 left value at i+1/2 from u[0..4] (only u[1..3] enter; A35) */
 double orc_mc2_left(const double u[5]);
+/* PPM left state at i+1/2 (u_R of cell i) from u[0..4] (A36) */
+double orc_ppm_left(const double u[5]);
 /* DER correction at the centre face from F[0..4] = F_{i-3/2..i+5/2}; der = 6/4/2 */
 double orc_der(const double F[5], int der);
 /* con2prim at one cell: non-densitised cons u, guess prims (for Z0), result prims.

@@ -178,8 +178,35 @@ double orc_mc2_left(const double u[5]) {
   return u[2] + 0.5 * slope;
 }
 
-/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2 */
+/* PPM (Colella & Woodward 1984, J. Comput. Phys. 54, 174: eqs. 1.6-1.10) on point values
+ * (reading A36): the interface values of cell i are the 4th-order point interpolants
+ * (-u_{i-1} + 9 u_i + 9 u_{i+1} - u_{i+2}) / 16 at i+1/2 (and the mirror at i-1/2),
+ * kept between the neighbouring cells (eq. 1.8's role: min/max of u_i, u_{i+1}); then the
+ * monotonicity constraints of eq. 1.10: a local extremum flattens both to u_i; an
+ * interface value that would put an extremum of the parabola inside the cell is reset
+ * (u_R = 3 u_i - 2 u_L, or u_L = 3 u_i - 2 u_R).  Contact steepening and flattening
+ * (CW84 §1 eqs. 1.14-1.17) are not used.  Returns the left state at i+1/2 (u_R of cell i). */
+static double ppm_face(double a, double b, double c, double d) {  /* interface between b and c */
+  double v = (-a + 9.0 * b + 9.0 * c - d) / 16.0;
+  const double lo = fmin(b, c), hi = fmax(b, c);
+  if (v < lo) v = lo;
+  if (v > hi) v = hi;
+  return v;
+}
+double orc_ppm_left(const double u[5]) {
+  double uR = ppm_face(u[1], u[2], u[3], u[4]); /* i+1/2 */
+  double uL = ppm_face(u[0], u[1], u[2], u[3]); /* i-1/2 */
+  const double ui = u[2];
+  if ((uR - ui) * (ui - uL) <= 0.0) return ui;
+  const double du = uR - uL, m6 = 6.0 * (ui - 0.5 * (uL + uR));
+  if (du * m6 > du * du) uL = 3.0 * ui - 2.0 * uR;
+  if (-du * du > du * m6) uR = 3.0 * ui - 2.0 * uL;
+  return uR;
+}
+
+/* reconstruction switch: rec 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2, 5 PPM */
 static double orc_rec_left(const double u[5], int rec) {
+  if (rec == 5) return orc_ppm_left(u);
   if (rec == 4) return orc_mc2_left(u);
   if (rec == 3) return orc_wenoz_left(u);
   return rec == 2 ? orc_mp5_left(u) : orc_weno5_left(u, rec);

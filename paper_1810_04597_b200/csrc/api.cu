@@ -213,7 +213,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     if (zh && grid->n[2] < ECHO_HALO_PLANES)
       return fail(nullptr, ECHO_E_ARG, "echo_create: a slab with halo boundaries needs n[2] >= ECHO_HALO_PLANES");
   }
-  if (grid->rec < 0 || grid->rec > 4) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..4");
+  if (grid->rec < 0 || grid->rec > 5) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..5");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
   if (grid->divb != 0 && grid->divb != 1) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0 or 1");
   if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");

@@ -429,10 +429,34 @@ ECHO_D void mc2_both(double um1, double u0, double up1, double& qL, double& qR) 
   qR = u0 + 0.5 * -slope;
 }
 
-// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2
+// PPM (A36): the limiter's decisions are discontinuous, so every quantity that enters one is
+// evaluated with explicitly rounded operations in the oracle's order (no FMA contraction):
+// the decisions, and hence the states, match the oracle's bit for bit.
+ECHO_D double ppm_face(double a, double b, double c, double d) {  // interface between b and c
+  double v = __dmul_rn(__dsub_rn(__dadd_rn(__dadd_rn(-a, __dmul_rn(9.0, b)), __dmul_rn(9.0, c)), d), 0.0625);
+  const double lo = dmin(b, c), hi = dmax(b, c);
+  v = dmax(v, lo);
+  return dmin(v, hi);
+}
+ECHO_D double ppm_right_of(double uL, double ui, double uR) {  // the constrained u_R of a cell
+  if (!(__dmul_rn(__dsub_rn(uR, ui), __dsub_rn(ui, uL)) > 0.0)) return ui;
+  const double du = __dsub_rn(uR, uL);
+  const double m6 = __dmul_rn(6.0, __dsub_rn(ui, __dmul_rn(0.5, __dadd_rn(uL, uR))));
+  if (-__dmul_rn(du, du) > __dmul_rn(du, m6)) return __dsub_rn(__dmul_rn(3.0, ui), __dmul_rn(2.0, uL));
+  return uR;
+}
+ECHO_D void ppm_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
+  // left state at i+1/2: u_R of cell i from the stencil (um2..up2); right state at i-1/2:
+  // u_R of the mirrored stencil (up2..um2), i.e. its interfaces evaluated in the mirror order
+  qL = ppm_right_of(ppm_face(um2, um1, u0, up1), u0, ppm_face(um1, u0, up1, up2));
+  qR = ppm_right_of(ppm_face(up2, up1, u0, um1), u0, ppm_face(up1, u0, um1, um2));
+}
+
+// reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2, 5 PPM
 template <int REC>
 ECHO_D void rec_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {
-  if constexpr (REC == 4) mc2_both(um1, u0, up1, qL, qR);
+  if constexpr (REC == 5) ppm_both(um2, um1, u0, up1, up2, qL, qR);
+  else if constexpr (REC == 4) mc2_both(um1, u0, up1, qL, qR);
   else if constexpr (REC == 2) mp5_both(um2, um1, u0, up1, up2, qL, qR);
   else weno5_both<REC>(um2, um1, u0, up1, up2, qL, qR);
 }

@@ -485,6 +485,7 @@ static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt,
 template <int AX, bool KS, int DER>
 static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
                               cudaStream_t st) {
+  if (g.rec == 5) return launch_dn<AX, KS, DER, 5>(g, e, mt, P, UB, R, st);
   if (g.rec == 4) return launch_dn<AX, KS, DER, 4>(g, e, mt, P, UB, R, st);
   if (g.rec == 3) return launch_dn<AX, KS, DER, 3>(g, e, mt, P, UB, R, st);
   if (g.rec == 2) return launch_dn<AX, KS, DER, 2>(g, e, mt, P, UB, R, st);

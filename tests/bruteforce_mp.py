@@ -252,7 +252,24 @@ def mc2(u):
     return u[2]
 
 
+def ppm(u):
+    """PPM on point values (A36): 4th-order interface interpolants kept between the
+    neighbours, then the Colella-Woodward monotonicity constraints; u_R of cell i."""
+    def face(a, b, c, d):
+        v = (-a + 9 * b + 9 * c - d) / 16
+        return min(max(v, min(b, c)), max(b, c))
+    uR, uL, ui = face(u[1], u[2], u[3], u[4]), face(u[0], u[1], u[2], u[3]), u[2]
+    if (uR - ui) * (ui - uL) <= 0:
+        return ui
+    du, m6 = uR - uL, 6 * (ui - (uL + uR) / 2)
+    if -du * du > du * m6:
+        uR = 3 * ui - 2 * uL
+    return uR
+
+
 def rec_left(u, rec):
+    if rec == 5:
+        return ppm(u)
     if rec == 4:
         return mc2(u)
     if rec == 3:

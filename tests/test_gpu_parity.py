@@ -123,7 +123,8 @@ def test_multistep_parity(E, orc, cfg, n, steps):
 
 @pytest.mark.parametrize("cfg,n,steps,rec", [(0, (32, 32, 32), 10, 2), (2, (40, 40, 40), 10, 2),
                                               (4, (64, 32, 16), 5, 2), (0, (32, 32, 32), 10, 3),
-                                              (2, (40, 40, 40), 10, 3), (2, (40, 40, 40), 10, 4)])
+                                              (2, (40, 40, 40), 10, 3), (2, (40, 40, 40), 10, 4),
+                                              (0, (32, 32, 32), 10, 5), (2, (40, 40, 40), 10, 5)])
 def test_multistep_parity_mp5(E, orc, cfg, n, steps, rec):
     """MP5 (rec=2, A33) and WENO-Z (rec=3, A34) reconstruction: multi-step
     parity, incl. the blast (limiter active at the shock) and the Kerr-Schild torus."""
@@ -172,7 +173,7 @@ def test_con2prim_parity(E, orc):
 def test_switches_parity(E, orc):
     # rec=FV, der=4, divb=none on a multi-tile grid
     p = small_problem(0, (70, 9, 10))
-    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}, {"rec": 3}, {"rec": 4, "der": 2}):
+    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}, {"rec": 3}, {"rec": 4, "der": 2}, {"rec": 5, "der": 4}):
         for k, v in kw.items():
             setattr(p, k, v)
         P8 = I.initial_prims(p)

@@ -166,6 +166,33 @@ def test_mc2_order(orc):
         assert 1.9 < math.log2(a / b) < 2.1, e
 
 
+# ------------------------------------------------------------------ PPM (rec=5, A36)
+def test_ppm_values_and_monotonicity(orc):
+    for c in (0.0, 1.0, -3.7):
+        assert orc.ppm_left([c] * 5) == c
+    assert orc.ppm_left([1, 2, 3, 4, 5]) == 3.5       # linear data: exact
+    assert orc.ppm_left([4, 1, 0, 1, 4]) == 0.0       # an extremum: the parabola is flattened
+    assert orc.ppm_left([0, 0, 0, 1, 1]) == 0.0       # steps: no overshoot
+    assert orc.ppm_left([0, 0, 1, 1, 1]) == 1.0
+    rng = np.random.default_rng(13)
+    for _ in range(2000):  # the face value stays between u_i and u_{i+1} (or is u_i)
+        u = rng.standard_normal(5)
+        q = orc.ppm_left(u)
+        assert min(u[2], u[3]) - 1e-15 <= q <= max(u[2], u[3]) + 1e-15
+
+
+def test_ppm_order(orc):
+    # smooth monotone data: the 4th-order point interpolant survives the limiter
+    def err(N):
+        h = 1.0 / N
+        x = np.arange(N) * h
+        u = np.exp(x)
+        return max(abs(orc.ppm_left(u[i - 2:i + 3]) - math.exp(x[i] + h / 2)) for i in range(2, N - 2))
+    e = [err(N) for N in (32, 64, 128, 256)]
+    for a, b in zip(e, e[1:]):
+        assert 3.9 < math.log2(a / b) < 4.1, e
+
+
 # ------------------------------------------------------------------ DER
 def test_der_values(orc):
     for o in (2, 4, 6):
