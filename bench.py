@@ -199,7 +199,7 @@ def workload_config(args, p, world):
                         f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[args.rec]}+HLL+DER6+field-CD, SSP-RK3",
             "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
             "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
-            "step": "echo_max_dt + echo_step (3 stages x [3 sweeps + update])"}
+            "step": "CFL reduction -> dt, then one SSP-RK3 step (3 stages x [3 sweeps + update])"}
 
 
 # ------------------------------------------------- ours, z-slab decomposition
@@ -330,11 +330,14 @@ def run_ours(args, world, rank, local):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    dts = []
-    for _ in range(K):
-        dt = g.max_dt(p.cfl)
-        dts.append(dt)
-        g.step(dt)
+    if args.loop == "device":
+        dts = g.advance(K, p.cfl).tolist()  # dt on the device, one graph replay per step
+    else:
+        dts = []
+        for _ in range(K):
+            dt = g.max_dt(p.cfl)
+            dts.append(dt)
+            g.step(dt)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -389,15 +392,19 @@ def run_ours(args, world, rank, local):
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     echo.set_prims(g.ctx, hin)          # H2D of the inputs (pinned) + prim2cons
-    for _ in range(K):
-        g.step(g.max_dt(p.cfl))         # each step reads its dt back (8 B D2H)
+    if args.loop == "device":
+        g.advance(K, p.cfl)             # the K dt values come back at the end (8 B each)
+    else:
+        for _ in range(K):
+            g.step(g.max_dt(p.cfl))     # each step reads its dt back (8 B D2H)
     echo.get_prims(g.ctx, hout)         # D2H of the result
     f1.record(stream)
     torch.cuda.synchronize()
     te2e = reduce_max(f0.elapsed_time(f1) / 1e3, world, dev)
     e2e = {"value": world * N * K / te2e, "unit": UNIT,
            "h2d_bytes_per_step": int(8 * N * 8 / K) + 0, "d2h_bytes_per_step": int(8 * N * 8 / K) + 8,
-           "what": "echo_set_prims(pinned host) + K x (echo_max_dt + echo_step) + echo_get_prims(pinned host)"}
+           "what": "echo_set_prims(pinned host) + " + ("echo_advance(K)" if args.loop == "device" else
+                                                        "K x (echo_max_dt + echo_step)") + " + echo_get_prims(pinned host)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -414,6 +421,8 @@ def run_ours(args, world, rank, local):
             "config": workload_config(args, p, world),
             "hbm_roofline": hbm, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,
+            "loop": ("echo_advance: dt computed on the device, each step one CUDA-graph replay, one sync per K steps"
+                     if args.loop == "device" else "host loop: K x (echo_max_dt readback + echo_step)"),
             "counters": {"floor_events": st["floor_events"], "c2p_failures": st["c2p_failures"]},
             "dt_first_last": [dts[0], dts[-1]],
         }
@@ -439,6 +448,8 @@ def main(argv=None):
                     help="--decomp on one GPU: the update kernels store the neighbours' ghost planes (echo_halo_link)")
     ap.add_argument("--rec", type=int, default=0, choices=[0, 1, 2, 3, 4, 5],
                     help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5, 3 WENO-Z, 4 MC2, 5 PPM")
+    ap.add_argument("--loop", choices=["device", "host"], default="device",
+                    help="device: echo_advance (dt on the device, CUDA-graph step); host: echo_max_dt + echo_step per step")
     ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")
     ap.add_argument("--ref-n", type=int, default=64)
     ap.add_argument("--cpu-n", type=int, default=64)

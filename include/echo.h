@@ -172,6 +172,18 @@ int echo_step(echo_ctx* ctx, double dt);
  * Synchronises (one 8-byte device-to-host copy).  ECHO_E_NONFINITE if the max is 0 or not finite. */
 int echo_max_dt(echo_ctx* ctx, double cfl, double* dt_out);
 
+/* nsteps x (echo_max_dt(cfl) + echo_step(dt)) with the time step computed on the device:
+ * the same dt values bit for bit (dt = cfl / m in IEEE division, m the reduction fused
+ * into the previous step's last update) and the same state, without a host round trip
+ * per step.  The step (its dt kernel, 9 sweeps and 3 updates) is captured once into a
+ * CUDA graph (re-captured when cfl changes) and replayed nsteps times; one
+ * synchronisation at the end.  dt_log: host array of nsteps doubles receiving each
+ * step's dt (may be NULL); *steps_done (may be NULL): steps completed.
+ * ECHO_E_NONFINITE if the max speed became 0 or not finite before step *steps_done + 1:
+ * the device skips every later update, so the state is that after *steps_done steps.
+ * Not in slab mode (ECHO_E_ORDER), nor with a step in progress.  Synchronises. */
+int echo_advance(echo_ctx* ctx, int nsteps, double cfl, double* dt_log, int* steps_done);
+
 /* Accumulated counters (synchronises). */
 int echo_stats(echo_ctx* ctx, echo_stats_t* out);
 

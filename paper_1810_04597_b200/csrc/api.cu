@@ -22,10 +22,10 @@ namespace {
 
 enum KernelClass {
   kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kLayout,
-  kNumClasses
+  kCflDt, kNumClasses
 };
-const char* kNames[kNumClasses] = {"sweep_x", "sweep_y",   "sweep_z",   "update_stage", "update_rhs",
-                                   "con2prim", "max_speed", "prim2cons", "get_prims",    "layout"};
+const char* kNames[kNumClasses] = {"sweep_x",   "sweep_y",   "sweep_z",   "update_stage", "update_rhs", "con2prim",
+                                   "max_speed", "prim2cons", "get_prims", "layout",       "cfl_dt"};
 
 std::string g_create_error;
 
@@ -64,6 +64,13 @@ struct echo_ctx {
   int next_stage = 1;
   unsigned long long steps = 0, stages = 0;
   long long launches = 0;
+  // device-driven time loop (echo_advance): adv = [dt, halt, steps done], then the dt log
+  double* dadv = nullptr;
+  long long dlog_cap = 0;
+  cudaStream_t cap_st = nullptr;       // private stream the step graph is captured on
+  cudaGraphExec_t step_exec = nullptr;  // one step: k_cfl_dt + 3 x (3 sweeps + update)
+  double step_cfl = 0.0;               // the cfl baked into step_exec
+  long long step_kernels = 0;          // kernels per replay
   std::string err;
   // profiling
   bool prof = false;
@@ -167,7 +174,7 @@ static GhostLinks ghost_links(echo_ctx* c, int s) {
   return gl;
 }
 
-static int run_update(echo_ctx* c, int s, double dt) {
+static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr) {
   const double* Uin = (s == 1) ? c->Un : c->Us;
   double* Uout = (s == 3) ? c->Un : c->Us;
   // the last stage also reduces the CFL rate of the new state (a9 fused into K3)
@@ -176,7 +183,7 @@ static int run_update(echo_ctx* c, int s, double dt) {
   const GhostLinks gl = ghost_links(c, s);
   cudaError_t e = launch(c, kUpdateStage, [&] {
     return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Un, Uin, Uout, c->P, nullptr,
-                         c->dcnt, cfl, c->st, &gl);
+                         c->dcnt, cfl, c->st, &gl, dtp);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
   c->cfl_valid = (s == 3);
@@ -330,6 +337,9 @@ void echo_destroy(echo_ctx* c) {
   cudaFree(c->dcnt);
   cudaFree(c->dbad);
   cudaFree(c->tables);
+  cudaFree(c->dadv);
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->hpin) cudaFreeHost(c->hpin);
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
@@ -550,6 +560,117 @@ int echo_max_dt(echo_ctx* c, double cfl, double* dt_out) {
   if (!(m > 0.0) || !std::isfinite(m))
     return fail(c, ECHO_E_NONFINITE, "echo_max_dt: max signal speed is zero or not finite (static field, dt unbounded)");
   *dt_out = cfl / m;
+  return ECHO_OK;
+}
+
+// ------------------------------------------------- device-driven time loop
+// one step with dt computed on the device (k_cfl_dt) from the previous reduction
+static int issue_step_dev(echo_ctx* c, double cfl) {
+  CK(launch(c, kCflDt, [&] { return launch_cfl_dt(cfl, c->dcnt + 2, c->dadv, c->dadv + 4, c->dlog_cap, c->st); }),
+     "echo_advance");
+  for (int s = 1; s <= 3; s++) {
+    int rc = run_sweeps(c);
+    if (!rc) rc = run_update(c, s, 0.0, c->dadv);
+    if (rc) return rc;
+  }
+  return ECHO_OK;
+}
+
+// capture issue_step_dev into c->step_exec (on a private stream: the caller's may be the
+// legacy default stream, which cannot be captured); host bookkeeping is restored after
+static int capture_step(echo_ctx* c, double cfl) {
+  if (c->step_exec) {
+    cudaGraphExecDestroy(c->step_exec);
+    c->step_exec = nullptr;
+  }
+  if (!c->cap_st) CK(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking), "echo_advance");
+  const cudaStream_t user = c->st;
+  const long long launches0 = c->launches;
+  const unsigned long long stages0 = c->stages;
+  c->st = c->cap_st;
+  CK(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal), "echo_advance capture");
+  int rc = issue_step_dev(c, cfl);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_st, &graph);
+  c->st = user;
+  c->step_kernels = c->launches - launches0;
+  c->launches = launches0;
+  c->stages = stages0;
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "echo_advance capture");
+  e = cudaGraphInstantiate(&c->step_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(c, e, "echo_advance instantiate");
+  c->step_cfl = cfl;
+  return ECHO_OK;
+}
+
+int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps_done) {
+  if (steps_done) *steps_done = 0;
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_advance: no state (call echo_set_prims first)");
+  if (c->next_stage != 1 || c->swept) return fail(c, ECHO_E_ORDER, "echo_advance: a step is in progress (finish its stages)");
+  if (c->g.zhalo)
+    return fail(c, ECHO_E_ORDER, "echo_advance: halo (slab) boundaries need a halo exchange before every stage");
+  if (nsteps < 0) return fail(c, ECHO_E_ARG, "echo_advance: nsteps >= 0 violated");
+  if (!(cfl > 0.0) || !std::isfinite(cfl)) return fail(c, ECHO_E_ARG, "echo_advance: cfl > 0 violated");
+  if (nsteps == 0) return ECHO_OK;
+  const unsigned long long stages0 = c->stages;
+  const long long cap = dt_log ? nsteps : 0;
+  if (!c->dadv || cap > c->dlog_cap) {  // adv block + log; a new buffer invalidates the captured step
+    cudaFree(c->dadv);
+    c->dadv = nullptr;
+    const long long ncap = cap > c->dlog_cap ? cap : c->dlog_cap;
+    if (cudaMalloc(&c->dadv, sizeof(double) * (4 + ncap)) != cudaSuccess)
+      return fail(c, ECHO_E_OOM, "echo_advance: dt log allocation failed");
+    c->dlog_cap = ncap;
+    if (c->step_exec) {
+      cudaGraphExecDestroy(c->step_exec);
+      c->step_exec = nullptr;
+    }
+  }
+  if (!c->cfl_valid) {  // the first dt needs the reduction of the current state
+    CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_advance");
+    cudaError_t e = launch(c, kMaxSpeed, [&] {
+      return launch_max_speed(c->ks, c->g, c->e, c->mt, c->P, ucur(c), c->dcnt + 2, c->st);
+    });
+    if (e != cudaSuccess) return cuda_fail(c, e, "max_speed launch");
+  }
+  CK(cudaMemsetAsync(c->dadv, 0, 4 * sizeof(double), c->st), "echo_advance");
+  if (c->prof) {  // per-kernel events cannot live inside a graph: issue the launches directly
+    for (int n = 0; n < nsteps; n++) {
+      int rc = issue_step_dev(c, cfl);
+      if (rc) return rc;
+    }
+  } else {
+    if (!c->step_exec || c->step_cfl != cfl) {
+      int rc = capture_step(c, cfl);
+      if (rc) return rc;
+    }
+    for (int n = 0; n < nsteps; n++) {
+      CK(cudaGraphLaunch(c->step_exec, c->st), "echo_advance graph launch");
+      c->launches += c->step_kernels;
+    }
+  }
+  // one readback for the whole loop: [dt, halt, steps done] and the dt log
+  double adv[4];
+  CK(cudaMemcpyAsync(adv, c->dadv, sizeof adv, cudaMemcpyDeviceToHost, c->st), "echo_advance");
+  if (dt_log) CK(cudaMemcpyAsync(dt_log, c->dadv + 4, sizeof(double) * nsteps, cudaMemcpyDeviceToHost, c->st), "echo_advance");
+  CK(cudaStreamSynchronize(c->st), "echo_advance");
+  const int done = (int)adv[2];
+  c->steps += done;
+  c->stages = stages0 + 3ull * done;
+  if (steps_done) *steps_done = done;
+  if (adv[1] != 0.0) {
+    c->cfl_valid = false;
+    return fail(c, ECHO_E_NONFINITE,
+                "echo_advance: max signal speed is zero or not finite (static field, dt unbounded); "
+                "the state is that after the steps done");
+  }
+  c->cfl_valid = true;
   return ECHO_OK;
 }
 

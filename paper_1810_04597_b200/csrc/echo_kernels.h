@@ -42,7 +42,14 @@ enum UpdateMode { kModeStage = 0, kModeRhs = 1, kModeC2P = 2 };
 cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                           const double* R, const double* Un, const double* Us, double* Uout, double* P, double* Lout,
                           unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st,
-                          const GhostLinks* links = nullptr);
+                          const GhostLinks* links = nullptr, const double* dtp = nullptr);
+
+// device-driven time loop: dtp = adv = [dt, halt, steps done] (doubles); launch_update with
+// dtp set reads dt from adv[0] and does nothing once adv[1] != 0.  k_cfl_dt sets
+// adv[0] = cfl / m from the CFL reduction bits (halt on m <= 0 or non-finite) and appends
+// it to log[steps done] while steps done < cap.
+cudaError_t launch_cfl_dt(double cfl, const unsigned long long* maxbits, double* adv, double* log, long long cap,
+                          cudaStream_t st);
 
 // a9: per-cell sum_a max|lambda_a|/Delta_a, max-reduced into *out (u64 bit pattern, zeroed by caller)
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,

@@ -37,8 +37,13 @@ template <bool KS, int MODE, bool DIVB_NONE>
 __global__ void __launch_bounds__(kCellThreads, 3)
 k_update(const GridP g, const EosP e, const MetTables mt, const int s, const double dt, const double* __restrict__ R,
          const double* Un, const double* Us, double* Uout, double* P, double* __restrict__ Lout,
-         unsigned long long* counters, unsigned long long* cfl_out, const GhostLinks gl) {
+         unsigned long long* counters, unsigned long long* cfl_out, const GhostLinks gl, const double* dtp) {
   const long long N = g.N;
+  double dtv = dt;
+  if (dtp) {  // device-driven time loop (echo_advance): dt from k_cfl_dt; a halted loop skips the update
+    if (dtp[1] != 0.0) return;  // uniform over the grid: no thread is left at the block barrier
+    dtv = dtp[0];
+  }
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = id < N;
   int ev = 0;
@@ -47,7 +52,7 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
     int i, j, k;
     cell_ijk(g, id, i, j, k);
     if (MODE == kModeStage) {
-      ev = stage_cell<KS, DIVB_NONE>(g, e, mt, s, dt, R, Un, Us, Uout, P, i, j, k, cfl_out != nullptr, rate, &gl);
+      ev = stage_cell<KS, DIVB_NONE>(g, e, mt, s, dtv, R, Un, Us, Uout, P, i, j, k, cfl_out != nullptr, rate, &gl);
     } else {
       const auto m = MetAt<KS>::get(mt, i, j);
       const long long rb = rec_base(g, i, j, k), vs = g.vs;
@@ -90,32 +95,34 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
 template <bool KS, int MODE>
 static cudaError_t upd2(const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* R,
                         const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st, const GhostLinks& gl) {
+                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st, const GhostLinks& gl,
+                        const double* dtp) {
   unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
   if (g.divb == 1)
-    k_update<KS, MODE, true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, gl);
+    k_update<KS, MODE, true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, gl, dtp);
   else
-    k_update<KS, MODE, false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, gl);
+    k_update<KS, MODE, false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, gl, dtp);
   return cudaGetLastError();
 }
 
 template <bool KS>
 static cudaError_t upd1(int mode, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt, const double* R,
                         const double* Un, const double* Us, double* Uout, double* P, double* Lout,
-                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st, const GhostLinks& gl) {
-  if (mode == kModeRhs) return upd2<KS, kModeRhs>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, nullptr, st, gl);
-  if (mode == kModeC2P) return upd2<KS, kModeC2P>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st, gl);
-  return upd2<KS, kModeStage>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st, gl);
+                        unsigned long long* cnt, unsigned long long* cfl, cudaStream_t st, const GhostLinks& gl,
+                        const double* dtp) {
+  if (mode == kModeRhs) return upd2<KS, kModeRhs>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, nullptr, st, gl, nullptr);
+  if (mode == kModeC2P) return upd2<KS, kModeC2P>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st, gl, nullptr);
+  return upd2<KS, kModeStage>(g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, cnt, cfl, st, gl, dtp);
 }
 
 cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                           const double* R, const double* Un, const double* Us, double* Uout, double* P, double* Lout,
                           unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st,
-                          const GhostLinks* links) {
+                          const GhostLinks* links, const double* dtp) {
   GhostLinks none{};
   const GhostLinks& gl = links ? *links : none;
-  if (ks) return upd1<true>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st, gl);
-  return upd1<false>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st, gl);
+  if (ks) return upd1<true>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st, gl, dtp);
+  return upd1<false>(mode, g, e, mt, s, dt, R, Un, Us, Uout, P, Lout, counters, cfl_out, st, gl, dtp);
 }
 
 // ------------------------------------------------------ CFL reduction (a9)
@@ -145,6 +152,31 @@ cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTa
   unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
   if (ks) k_max_speed<true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, U, out);
   else k_max_speed<false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, U, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------- device-side time step (echo_advance)
+// dt = cfl / m (IEEE division: the host's echo_max_dt value bit for bit) from the
+// reduction the previous step's last update left in *maxbits; adv = [dt, halt, count].
+// A zero or non-finite m sets halt, after which every update of the loop is skipped.
+__global__ void k_cfl_dt(double cfl, const unsigned long long* __restrict__ maxbits, double* adv, double* log,
+                         long long cap) {
+  if (adv[1] != 0.0) return;
+  const double m = __longlong_as_double((long long)*maxbits);
+  if (!(m > 0.0) || !isfinite(m)) {
+    adv[1] = 1.0;
+    return;
+  }
+  const double dt = cfl / m;
+  adv[0] = dt;
+  const long long n = (long long)adv[2];
+  if (n < cap) log[n] = dt;
+  adv[2] = (double)(n + 1);
+}
+
+cudaError_t launch_cfl_dt(double cfl, const unsigned long long* maxbits, double* adv, double* log, long long cap,
+                          cudaStream_t st) {
+  k_cfl_dt<<<1, 1, 0, st>>>(cfl, maxbits, adv, log, cap);
   return cudaGetLastError();
 }
 

@@ -66,6 +66,7 @@ _sig = {
     "echo_stage": (C.c_int, [_P, C.c_int, C.c_double]),
     "echo_step": (C.c_int, [_P, C.c_double]),
     "echo_max_dt": (C.c_int, [_P, C.c_double, _D]),
+    "echo_advance": (C.c_int, [_P, C.c_int, C.c_double, _D, C.POINTER(C.c_int)]),
     "echo_stats": (C.c_int, [_P, C.POINTER(Stats)]),
     "echo_last_error": (C.c_char_p, [_P]),
     "echo_profile": (C.c_int, [_P, C.c_int]),
@@ -205,6 +206,16 @@ def max_dt(ctx, cfl: float) -> float:
     out = C.c_double(0.0)
     _check(ctx, _lib.echo_max_dt(ctx, float(cfl), C.byref(out)))
     return out.value
+
+
+def advance(ctx, nsteps: int, cfl: float, log: bool = True):
+    """nsteps x (max_dt + step) with dt computed on the device (one CUDA-graph replay per
+    step, one synchronisation): returns the dt of every step (numpy) or None."""
+    buf = np.zeros(max(int(nsteps), 1), np.float64) if log else None
+    done = C.c_int(0)
+    ptr = buf.ctypes.data_as(_D) if log else None
+    _check(ctx, _lib.echo_advance(ctx, int(nsteps), float(cfl), ptr, C.byref(done)))
+    return buf[: done.value] if log else None
 
 
 def stats(ctx) -> dict:
@@ -354,6 +365,9 @@ class Echo:
 
     def max_dt(self, cfl):
         return max_dt(self.ctx, cfl)
+
+    def advance(self, nsteps, cfl, log=True):
+        return advance(self.ctx, nsteps, cfl, log)
 
     def con2prim(self):
         return con2prim(self.ctx)
