@@ -376,6 +376,83 @@ def initial_prims(p: Problem, device=None, **kw):
     raise ValueError(cfg)
 
 
+# ----------------------------------------------- staggered field (UCT, divb = 2)
+def _coords_face(p: Problem, a: int, torch, device):
+    """centre coordinates, except the face coordinates x_{i+1/2} along axis a"""
+    xs = []
+    for b in range(3):
+        d = (p.hi[b] - p.lo[b]) / p.n[b]
+        xs.append(p.lo[b] + (np.arange(p.n[b]) + (1.0 if b == a else 0.5)) * d)
+    if torch is None:
+        return (xs[0][None, None, :], xs[1][None, :, None], xs[2][:, None, None])
+    t = [torch.tensor(x, dtype=torch.float64, device=device) for x in xs]
+    return (t[0].view(1, 1, -1), t[1].view(1, -1, 1), t[2].view(-1, 1, 1))
+
+
+def _curl_modes(modes_by_comp, a, X, Y, Z, amp, torch):
+    """component a of the analytic curl of A^c = amp sum_m w_m sin(2 pi k_m.x + phi_m) / (2 pi |k_m|):
+    d_j A^c = amp sum_m w_m (k_j / |k_m|) cos(...)"""
+    cos = np.cos if torch is None else torch.cos
+    def d(c, j):
+        out = 0.0
+        for (k, phi, w) in modes_by_comp[c]:
+            kn = math.sqrt(k[0] ** 2 + k[1] ** 2 + k[2] ** 2)
+            out = out + amp * w * (k[j] / kn) * cos(2.0 * math.pi * (k[0] * X + k[1] * Y + k[2] * Z) + phi)
+        return out
+    b1, b2 = (a + 1) % 3, (a + 2) % 3
+    return d(b2, b1) - d(b1, b2)   # (curl A)^a = d_{a+1} A^{a+2} - d_{a+2} A^{a+1}
+
+
+def face_field(p: Problem, device=None, direction=None):
+    """UCT runs (divb = 2): sqrt(gamma) B^a at the centres of the faces i_a + 1/2,
+    [3][n3][n2][n1], the ANALYTIC field of the config's initial condition sampled at the
+    faces (turbulence: B0 x-hat + the exact curl of the same seeded vector potential,
+    whose cell-centred counterpart ic_turbulence takes as a D2 curl; CP Alfven: the
+    exact wave, along `direction` = integer (k1, k2, k3) if given, else (1, 1, 1))."""
+    torch = _backend(device)
+    cfg = p.params["cfg"]
+    out = []
+    if cfg in (0, 3):
+        prm = p.params
+        rng = SplitMix64(p.seed)
+        modes = [draw_modes(rng, prm["modes"], prm["kmax"]) for _ in range(8)]
+        for a in range(3):
+            X, Y, Z = _coords_face(p, a, torch, device)
+            b = _curl_modes(modes[5:8], a, X, Y, Z, prm["amp"], torch)
+            out.append(b + (prm["B0"] if a == 0 else 0.0))
+    elif cfg == 1:
+        for a in range(3):
+            X, Y, Z = _coords_face(p, a, None, None)
+            out.append(cp_alfven_fields(p, X, Y, Z, 0.0, direction)[1][a])
+    else:
+        raise ValueError("face_field: UCT inputs exist for the periodic Minkowski configs 0, 1, 3")
+    shape = (p.n[2], p.n[1], p.n[0])
+    if torch is None:
+        return np.ascontiguousarray(np.stack([np.broadcast_to(f, shape) for f in out]).astype(np.float64))
+    return torch.stack([torch.as_tensor(f, dtype=torch.float64, device=device).expand(shape) for f in out]).contiguous()
+
+
+def cp_alfven_fields(p: Problem, X, Y, Z, t, direction=None):
+    """(v, B) of the exact CP Alfven wave of config 1 along the integer wave vector
+    `direction` (default (1,1,1)) at time t: phase 2 pi (k.x) - 2 pi |k| v_A t."""
+    prm = p.params
+    eta, B0 = prm["eta"], prm["B0"]
+    va = cp_alfven_speed(eta, B0)
+    kv = np.array(direction if direction is not None else (1, 1, 1), dtype=np.float64)
+    kn = float(np.linalg.norm(kv))
+    k = kv / kn
+    # an orthonormal pair perpendicular to k
+    t0 = np.array([0.0, 0.0, 1.0]) if abs(k[2]) < 0.9 else np.array([1.0, 0.0, 0.0])
+    e1 = np.cross(k, t0)
+    e1 /= np.linalg.norm(e1)
+    e2 = np.cross(k, e1)
+    phi = 2.0 * math.pi * (kv[0] * X + kv[1] * Y + kv[2] * Z) - 2.0 * math.pi * kn * va * t
+    c, s = np.cos(phi), np.sin(phi)
+    B = [B0 * k[i] + eta * B0 * (c * e1[i] + s * e2[i]) for i in range(3)]
+    v = [-va * eta * (c * e1[i] + s * e2[i]) for i in range(3)]
+    return v, B
+
+
 def uniform_prims(n, rho=1.0, v=(0.0, 0.0, 0.0), prs=1.0, B=(0.0, 0.0, 0.0)) -> np.ndarray:
     shape = (n[2], n[1], n[0])
     vals = [rho, v[0], v[1], v[2], prs, B[0], B[1], B[2]]

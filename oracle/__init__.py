@@ -156,6 +156,12 @@ def lib():
             "orc_max_dt": (C.c_int, [P, _D, _D, C.c_double, _D]),
             "orc_con2prim": (C.c_int, [P, _D, _D, C.POINTER(_Counts)]),
             "orc_divb": (C.c_double, [P, _D]),
+            "orc_uct_centre": (C.c_int, [P, _D, _D]),
+            "orc_uct_divh": (C.c_int, [P, _D, _D]),
+            "orc_rhs_uct": (C.c_int, [P, _D, _D, _D, _D]),
+            "orc_stage_uct": (C.c_int, [P, C.c_int, C.c_double, _D, _D, _D, _D, _D, _D, _D, _D,
+                                        C.POINTER(_Counts)]),
+            "orc_step_uct": (C.c_int, [P, C.c_double, _D, _D, _D, C.POINTER(_Counts)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -347,3 +353,61 @@ def con2prim(cfg: Cfg, U8, P5):
 
 def divb(cfg: Cfg, U8) -> float:
     return float(lib().orc_divb(C.byref(cfg.c()), _p(_v(U8))))
+
+
+# ---------------------------------------------------- UCT (divb = 2, A37-A41)
+def uct_centre(cfg: Cfg, b3) -> np.ndarray:
+    """cell-centred field I6(b3) (A37), [3][n3][n2][n1]"""
+    out = np.zeros(cfg.shape(3))
+    rc = lib().orc_uct_centre(C.byref(cfg.c()), _p(_v(b3)), _p(out))
+    if rc:
+        raise OracleError(f"orc_uct_centre rc={rc}")
+    return out
+
+
+def uct_divh(cfg: Cfg, b3) -> np.ndarray:
+    """the divergence UCT preserves, sum_a delta_a Dh_a b^a, per cell (A41)"""
+    out = np.zeros(cfg.shape(1))[0]
+    lib().orc_uct_divh(C.byref(cfg.c()), _p(_v(b3)), _p(out))
+    return out
+
+
+def set_prims_uct(cfg: Cfg, P8, b3):
+    """state of a UCT run: the hydro primitives of P8 and the staggered field b3 (the
+    cell-centred B of the state is I6(b3); P8's B slots are ignored)."""
+    P = _v(P8).copy()
+    P[5:8] = uct_centre(cfg, b3)
+    U, P5 = set_prims(cfg, P)
+    return U, P5, _v(b3).copy()
+
+
+def rhs_uct(cfg: Cfg, U8, P5, b3) -> np.ndarray:
+    out = np.zeros(cfg.shape(8))
+    rc = lib().orc_rhs_uct(C.byref(cfg.c()), _p(_v(U8)), _p(_v(P5)), _p(_v(b3)), _p(out))
+    if rc:
+        raise OracleError(f"orc_rhs_uct rc={rc}")
+    return out
+
+
+def stage_uct(cfg: Cfg, s: int, dt: float, Un, Us, Ps, bn, bs):
+    Uo = np.zeros(cfg.shape(8))
+    Po = np.zeros(cfg.shape(5))
+    bo = np.zeros(cfg.shape(3))
+    cnt = _Counts()
+    rc = lib().orc_stage_uct(C.byref(cfg.c()), s, dt, _p(_v(Un)), _p(_v(Us)), _p(_v(Ps)), _p(_v(bn)), _p(_v(bs)),
+                             _p(Uo), _p(Po), _p(bo), C.byref(cnt))
+    if rc:
+        raise OracleError(f"orc_stage_uct rc={rc}")
+    return Uo, Po, bo, (cnt.floor_events, cnt.c2p_failures)
+
+
+def step_uct(cfg: Cfg, dt: float, U8, P5, b3):
+    """one SSP-RK3 step with the staggered field; returns new copies (U8, P5, b3, counts)."""
+    U = _v(U8).copy()
+    P = _v(P5).copy()
+    b = _v(b3).copy()
+    cnt = _Counts()
+    rc = lib().orc_step_uct(C.byref(cfg.c()), dt, _p(U), _p(P), _p(b), C.byref(cnt))
+    if rc:
+        raise OracleError(f"orc_step_uct rc={rc}")
+    return U, P, b, (cnt.floor_events, cnt.c2p_failures)

@@ -58,7 +58,9 @@ typedef struct {
                         4 MC2 (monotonized-central limited linear, A35),
                         5 PPM (Colella & Woodward 1984 on point values, A36) */
   int der;           /* 6 DER6, 4 DER4, 2 plain difference (A5) */
-  int divb;          /* 0 field-CD (A6), 1 none: plain flux difference for B */
+  int divb;          /* 0 field-CD (A6), 1 none: plain flux difference for B,
+                        2 UCT: staggered field + upwind constrained transport (A37-A41;
+                        Minkowski, periodic axes; the *_uct entry points) */
   double der_jump;   /* A31 DER switch: the DER correction at a face is dropped (H = F) when a face
                         of its 5-face stencil joins cells whose rho or p differ by more than
                         der_jump x the smaller value; <= 0 disables the switch */
@@ -129,6 +131,22 @@ int orc_max_dt(const orc_cfg* c, const double* U8, const double* P5, double cfl,
 int orc_con2prim(const orc_cfg* c, double* U8, double* P5, orc_counts* cnt);
 /* max over owned cells of |sum_a D2_a(sqrt(gamma) B^a)| (SPEC.md:172 operator) */
 double orc_divb(const orc_cfg* c, const double* U8);
+
+/* ---------------- UCT (divb = 2; A37-A41) -------------------
+ * b3 [3][n3][n2][n1]: sqrt(gamma) B^a at the face i_a + 1/2 of cell (i1,i2,i3).
+ * The state's U8 slots 5..7 hold the cell-centred field I6(b3) (A37).
+ * Return -1 unless divb = 2, Minkowski and every axis periodic. */
+/* A37 centring: Bc3[a] = 6-point midpoint interpolation of b3[a] along a */
+int orc_uct_centre(const orc_cfg* c, const double* b3, double* Bc3);
+/* the preserved divergence sum_a delta_a Dh_a b^a at every cell (A41) */
+int orc_uct_divh(const orc_cfg* c, const double* b3, double* out);
+/* L on every owned cell: slots 0..4 hydro (as orc_rhs), slots 5..7 L(b^a) at the faces */
+int orc_rhs_uct(const orc_cfg* c, const double* U8, const double* P5, const double* b3, double* L8);
+/* RK stage s with the staggered field: bn, bs in, bout out (may alias bn at s = 3) */
+int orc_stage_uct(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
+                  const double* bn, const double* bs, double* Uout, double* Pout, double* bout, orc_counts* cnt);
+/* one SSP-RK3 step in place on (U8, P5, b3) */
+int orc_step_uct(const orc_cfg* c, double dt, double* U8, double* P5, double* b3, orc_counts* cnt);
 
 #ifdef __cplusplus
 }

@@ -241,8 +241,13 @@ static void der_face(const orc_cfg* c, const double F5[5][8], const int rough5[5
 
 /* Face flux at face i+1/2 from the stencil st[m][v] = prims of cells i-2+m,
  * m = 0..5, v = 0..7; xf = face coordinates; a = axis.  Shared by both paths.
+ * UCT (divb = 2, A37): bnorm -> the staggered sqrt(gamma) B^a of this face, which
+ * replaces both reconstructed normal components (Minkowski: sqrt(gamma) = 1), and
+ * fs (if not NULL) receives the face data of the EMF step (A38): v^1..3 of the left
+ * state, v^1..3 of the right state, a+ = S_R, a- = -S_L of the HLL flux (A4).
  * Returns the A31 roughness flag of the face. */
-static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8]) {
+static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8],
+                     const double* bnorm, double fs[8]) {
   double qL[8], qR[8];
   for (int v = 0; v < 8; v++) {
     double l[5], r[5];
@@ -257,9 +262,24 @@ static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3]
   if (!(qL[4] > 0.0)) qL[4] = st[2][4];
   if (!(qR[0] > 0.0)) qR[0] = st[3][0];
   if (!(qR[4] > 0.0)) qR[4] = st[3][4];
+  if (bnorm) qL[5 + a] = qR[5 + a] = *bnorm;
   orc_met m;
   orc_met_eval(c, xf, &m);
   orc_hll(&m, c->gamma, qL, qR, a, F);
+  if (fs) {
+    orc_aux al, ar;
+    orc_aux_eval(&m, c->gamma, qL, &al);
+    orc_aux_eval(&m, c->gamma, qR, &ar);
+    double lmL, lpL, lmR, lpR;
+    orc_speeds(&m, c->gamma, qL, a, &lmL, &lpL);
+    orc_speeds(&m, c->gamma, qR, a, &lmR, &lpR);
+    for (int i = 0; i < 3; i++) {
+      fs[i] = al.v[i];
+      fs[3 + i] = ar.v[i];
+    }
+    fs[6] = fmax(0.0, fmax(lpL, lpR));   /* a+ = S_R */
+    fs[7] = -fmin(0.0, fmin(lmL, lmR));  /* a- = -S_L */
+  }
   return rough_face(c, st[2], st[3]);
 }
 
@@ -334,6 +354,7 @@ static void accumulate_axis(const orc_cfg* c, int a, const double Hp[8], const d
   double d = dx_of(c, a);
   for (int q = 0; q < 5; q++) L[q] = L[q] - (Hp[q] - Hm[q]) / d;
   int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
+  if (c->divb == 2) return; /* UCT: the field is updated from edge EMFs (uct_induction) */
   if (c->divb == 1) {
     L[5 + b1] = L[5 + b1] - (Hp[5 + b1] - Hm[5 + b1]) / d;
     L[5 + b2] = L[5 + b2] - (Hp[5 + b2] - Hm[5 + b2]) / d;
@@ -366,9 +387,17 @@ static void curl_from(const orc_cfg* c, const double onb[3][3][2], double L[8]) 
   }
 }
 
-int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
+static void uct_emf_induction(const orc_cfg* c, const double* FS, const double* b3, double* L8);
+
+/* L(U) on every owned cell; UCT (b3 != NULL): slots 5..7 receive L(b^a) at the faces */
+static int rhs_full(const orc_cfg* c, const double* U8, const double* P5, const double* b3, double* L8) {
   const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
   int nt = nthreads_of(c);
+  double* FS = NULL; /* UCT face data [axis][8][N] of the faces i_a + 1/2 owned by the cells */
+  if (b3) {
+    FS = (double*)malloc(sizeof(double) * 24 * N);
+    if (!FS) return -3;
+  }
   padded P;
   P.N[0] = n0 + 2 * G;
   P.N[1] = n1 + 2 * G;
@@ -382,6 +411,7 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
   if (!P.a || !O.a) {
     free(P.a);
     free(O.a);
+    free(FS);
     return -3;
   }
   /* 1. owned primitives, then ghosts */
@@ -419,7 +449,19 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
         xf[a] = face_of(c, a, fi);
         xf[t1] = centre_of(c, t1, cell[t1]);
         xf[t2] = centre_of(c, t2, cell[t2]);
-        rf[fi + 3] = face_flux(c, st, xf, a, &F[8 * (fi + 3)]);
+        const double* bnorm = NULL;
+        double* fs = NULL;
+        if (b3) { /* the face fi+1/2 is owned by cell fi (wrapped) */
+          long long cf[3] = {cell[0], cell[1], cell[2]};
+          cf[a] = map_index(c, a, fi);
+          const long long idf = lin(c, cf[0], cf[1], cf[2]);
+          bnorm = &b3[a * N + idf];
+          if (fi >= 0 && fi < na) fs = &FS[(a * 8) * N + idf]; /* stride N between the 8 entries */
+        }
+        double fsv[8];
+        rf[fi + 3] = face_flux(c, st, xf, a, &F[8 * (fi + 3)], bnorm, fs ? fsv : NULL);
+        if (fs)
+          for (int m = 0; m < 8; m++) fs[m * N] = fsv[m];
       }
       for (long long hi = -1; hi < na; hi++) { /* DER flux at face hi+1/2 */
         double F5[5][8];
@@ -461,7 +503,9 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
         for (int q = 0; q < 8; q++) L8[q * N + id] = L[q];
       }
 
-  /* 4. field-CD curl with Omega ghosts filled by the same rule */
+  /* 4. UCT: edge EMFs and the staggered-field rhs; field-CD: curl with Omega ghosts
+   *    filled by the same rule */
+  if (b3) uct_emf_induction(c, FS, b3, L8);
   if (c->divb == 0) {
     for (long long k = -1; k <= n2; k++)
       for (long long j = -1; j <= n1; j++)
@@ -492,7 +536,13 @@ int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
   }
   free(P.a);
   free(O.a);
+  free(FS);
   return 0;
+}
+
+int orc_rhs(const orc_cfg* c, const double* U8, const double* P5, double* L8) {
+  if (c->divb == 2) return -1; /* UCT needs the staggered field: orc_rhs_uct */
+  return rhs_full(c, U8, P5, NULL, L8);
 }
 
 /* ------------------------------------------------------------------ */
@@ -521,7 +571,7 @@ static void hhat_at(const orc_cfg* c, const double* U8, const double* P5, int a,
     xf[a] = face_of(c, a, fi);
     xf[t1] = centre_of(c, t1, cell[t1]);
     xf[t2] = centre_of(c, t2, cell[t2]);
-    r5[f] = face_flux(c, st, xf, a, F[f]);
+    r5[f] = face_flux(c, st, xf, a, F[f], NULL, NULL);
   }
   der_face(c, F, r5, H);
 }
@@ -565,6 +615,7 @@ static void rhs_cell(const orc_cfg* c, const double* U8, const double* P5, const
 
 int orc_rhs_cells(const orc_cfg* c, const double* U8, const double* P5, long long ncell, const long long* idx,
                   double* out) {
+  if (c->divb == 2) return -1; /* UCT: full-grid path only */
   int nt = nthreads_of(c);
 #pragma omp parallel for num_threads(nt) schedule(dynamic)
   for (long long m = 0; m < ncell; m++) rhs_cell(c, U8, P5, &idx[3 * m], &out[8 * m]);
@@ -636,6 +687,7 @@ int orc_stage(const orc_cfg* c, int s, double dt, const double* Un, const double
 
 int orc_stage_cells(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
                     long long ncell, const long long* idx, double* Uout, double* Pout, orc_counts* cnt) {
+  if (c->divb == 2) return -1; /* UCT: full-grid path only */
   long long nfl = 0, nfa = 0;
   int nt = nthreads_of(c);
 #pragma omp parallel for num_threads(nt) schedule(dynamic) reduction(+ : nfl, nfa)
@@ -799,4 +851,253 @@ int orc_get_prims(const orc_cfg* c, const double* U8, const double* P5, double* 
         for (int a = 0; a < 3; a++) P8[(5 + a) * N + id] = pr[5 + a];
       }
   return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* UCT: staggered field + upwind constrained transport (divb = 2;      */
+/* SURVEY.md §8(f) f2; readings A37-A41).  Minkowski,        */
+/* periodic axes.  b3[a][N]: sqrt(gamma) B^a at the face i_a + 1/2     */
+/* owned by cell i (x1 fastest); E3[c][N]: EMF E^c at the edge         */
+/* (i_p + 1/2, i_q + 1/2, i_c) owned by cell i, (c, p, q) cyclic.      */
+/* ------------------------------------------------------------------ */
+/* linear index of cell x + d e_a with every index wrapped (A13) */
+static long long lin_shift(const orc_cfg* c, const long long x[3], int a, long long d) {
+  long long y[3] = {x[0], x[1], x[2]};
+  y[a] += d;
+  return lin(c, map_index(c, 0, y[0]), map_index(c, 1, y[1]), map_index(c, 2, y[2]));
+}
+
+/* A38: the two one-sided values at position +1/2 from samples f[0..5] at -2..3
+ * (lo from f[0..4], hi the mirror from f[5..1]), with the configured REC */
+static void rec_pair(const orc_cfg* c, const double f[6], double* lo, double* hi) {
+  double l[5], r[5];
+  for (int m = 0; m < 5; m++) l[m] = f[m];
+  for (int m = 0; m < 5; m++) r[m] = f[5 - m];
+  *lo = orc_rec_left(l, c->rec);
+  *hi = orc_rec_left(r, c->rec);
+}
+
+/* A39: UCT-HLL EMF E^cc at the edge owned by cell x.  p = cc+1, q = cc+2; W/E =
+ * left/right along p, S/N = left/right along q.  E^cc = v^q B^p - v^p B^q, the flux
+ * along q of B^p and minus the flux along p of B^q. */
+static double uct_emf(const orc_cfg* c, const double* FS, const double* b3, int cc, const long long x[3]) {
+  const long long N = ncells(c);
+  const int p = (cc + 1) % 3, q = (cc + 2) % 3;
+  const int comp[2] = {p, q};
+  double f[6];
+  /* p-face states (W = left, E = right) reconstructed along q: pS[side][k], pN[side][k] */
+  double pS[2][2], pN[2][2];
+  for (int side = 0; side < 2; side++)
+    for (int k = 0; k < 2; k++) {
+      for (int m = 0; m < 6; m++) f[m] = FS[(p * 8 + 3 * side + comp[k]) * N + lin_shift(c, x, q, m - 2)];
+      rec_pair(c, f, &pS[side][k], &pN[side][k]);
+    }
+  /* q-face states (S = left, N = right) reconstructed along p: qW[side][k], qE[side][k] */
+  double qW[2][2], qE[2][2];
+  for (int side = 0; side < 2; side++)
+    for (int k = 0; k < 2; k++) {
+      for (int m = 0; m < 6; m++) f[m] = FS[(q * 8 + 3 * side + comp[k]) * N + lin_shift(c, x, p, m - 2)];
+      rec_pair(c, f, &qW[side][k], &qE[side][k]);
+    }
+  /* staggered B^p along q, B^q along p */
+  double bpS, bpN, bqW, bqE;
+  for (int m = 0; m < 6; m++) f[m] = b3[p * N + lin_shift(c, x, q, m - 2)];
+  rec_pair(c, f, &bpS, &bpN);
+  for (int m = 0; m < 6; m++) f[m] = b3[q * N + lin_shift(c, x, p, m - 2)];
+  rec_pair(c, f, &bqW, &bqE);
+  /* A40: edge speeds = max over the two faces meeting at the edge */
+  const long long id = lin(c, x[0], x[1], x[2]);
+  const double app = fmax(FS[(p * 8 + 6) * N + id], FS[(p * 8 + 6) * N + lin_shift(c, x, q, 1)]);
+  const double apm = fmax(FS[(p * 8 + 7) * N + id], FS[(p * 8 + 7) * N + lin_shift(c, x, q, 1)]);
+  const double aqp = fmax(FS[(q * 8 + 6) * N + id], FS[(q * 8 + 6) * N + lin_shift(c, x, p, 1)]);
+  const double aqm = fmax(FS[(q * 8 + 7) * N + id], FS[(q * 8 + 7) * N + lin_shift(c, x, p, 1)]);
+  /* A38: quadrant velocities (v^p, v^q) = mean of the two double reconstructions */
+  double vWS[2], vWN[2], vES[2], vEN[2];
+  for (int k = 0; k < 2; k++) {
+    vWS[k] = 0.5 * (pS[0][k] + qW[0][k]);
+    vWN[k] = 0.5 * (pN[0][k] + qW[1][k]);
+    vES[k] = 0.5 * (pS[1][k] + qE[0][k]);
+    vEN[k] = 0.5 * (pN[1][k] + qE[1][k]);
+  }
+  const double EWS = vWS[1] * bpS - vWS[0] * bqW;
+  const double EWN = vWN[1] * bpN - vWN[0] * bqW;
+  const double EES = vES[1] * bpS - vES[0] * bqE;
+  const double EEN = vEN[1] * bpN - vEN[0] * bqE;
+  const double sp = app + apm, sq = aqp + aqm;
+  if (!(sp > 0.0) || !(sq > 0.0)) /* unreachable for p > 0 (A4): central average */
+    return 0.25 * (EWS + EWN + EES + EEN);
+  return (app * aqp * EWS + app * aqm * EWN + apm * aqp * EES + apm * aqm * EEN) / (sp * sq)
+       + app * apm * (bqE - bqW) / sp - aqp * aqm * (bpN - bpS) / sq;
+}
+
+/* A41: L(b^p) = -(Dh_q E^cc(+1/2) - Dh_q E^cc(-1/2)) / Delta_q
+ *              + (Dh_cc E^q(+1/2) - Dh_cc E^q(-1/2)) / Delta_cc,  cc = p-1, q = p+1,
+ * Dh_a = the DER operator along a (A5, never switched off by A31) */
+static void uct_emf_induction(const orc_cfg* c, const double* FS, const double* b3, double* L8) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  int nt = nthreads_of(c);
+  double* E3 = (double*)malloc(sizeof(double) * 3 * N);
+  if (!E3) return;
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        const long long x[3] = {i, j, k};
+        for (int cc = 0; cc < 3; cc++) E3[cc * N + lin(c, i, j, k)] = uct_emf(c, FS, b3, cc, x);
+      }
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        const long long x[3] = {i, j, k};
+        for (int p = 0; p < 3; p++) {
+          const int cc = (p + 2) % 3, q = (p + 1) % 3;
+          double Ep[5], Em[5], Gp[5], Gm[5];
+          for (int m = 0; m < 5; m++) {
+            Ep[m] = E3[cc * N + lin_shift(c, x, q, m - 2)];
+            Em[m] = E3[cc * N + lin_shift(c, x, q, m - 3)];
+            Gp[m] = E3[q * N + lin_shift(c, x, cc, m - 2)];
+            Gm[m] = E3[q * N + lin_shift(c, x, cc, m - 3)];
+          }
+          L8[(5 + p) * N + lin(c, i, j, k)] = -(orc_der(Ep, c->der) - orc_der(Em, c->der)) / dx_of(c, q)
+                                            + (orc_der(Gp, c->der) - orc_der(Gm, c->der)) / dx_of(c, cc);
+        }
+      }
+  free(E3);
+}
+
+static int uct_ok(const orc_cfg* c) {
+  if (c->divb != 2 || c->metric != ORC_MINKOWSKI) return 0;
+  for (int a = 0; a < 3; a++)
+    if (c->bc[a][0] != ORC_BC_PERIODIC) return 0;
+  return 1;
+}
+
+/* A37: cell-centred field from the staggered one, 6-point midpoint interpolation
+ * B^a(i) = (3 b_{i-5/2} - 25 b_{i-3/2} + 150 b_{i-1/2} + 150 b_{i+1/2} - 25 b_{i+3/2} + 3 b_{i+5/2}) / 256 */
+int orc_uct_centre(const orc_cfg* c, const double* b3, double* Bc3) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        const long long x[3] = {i, j, k};
+        for (int a = 0; a < 3; a++) {
+          double f[6];
+          for (int m = 0; m < 6; m++) f[m] = b3[a * N + lin_shift(c, x, a, m - 3)];
+          Bc3[a * N + lin(c, i, j, k)] =
+              (3.0 * f[0] - 25.0 * f[1] + 150.0 * f[2] + 150.0 * f[3] - 25.0 * f[4] + 3.0 * f[5]) / 256.0;
+        }
+      }
+  return 0;
+}
+
+/* the divergence UCT preserves (A41): sum_a (Dh_a b^a(+1/2) - Dh_a b^a(-1/2)) / Delta_a */
+int orc_uct_divh(const orc_cfg* c, const double* b3, double* out) {
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        const long long x[3] = {i, j, k};
+        double d = 0.0;
+        for (int a = 0; a < 3; a++) {
+          double fp[5], fm[5];
+          for (int m = 0; m < 5; m++) {
+            fp[m] = b3[a * N + lin_shift(c, x, a, m - 2)];
+            fm[m] = b3[a * N + lin_shift(c, x, a, m - 3)];
+          }
+          d += (orc_der(fp, c->der) - orc_der(fm, c->der)) / dx_of(c, a);
+        }
+        out[lin(c, i, j, k)] = d;
+      }
+  return 0;
+}
+
+int orc_rhs_uct(const orc_cfg* c, const double* U8, const double* P5, const double* b3, double* L8) {
+  if (!uct_ok(c)) return -1;
+  return rhs_full(c, U8, P5, b3, L8);
+}
+
+int orc_stage_uct(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
+                  const double* bn, const double* bs, double* Uout, double* Pout, double* bout, orc_counts* cnt) {
+  if (!uct_ok(c)) return -1;
+  const long long N = ncells(c);
+  double* L8 = (double*)malloc(sizeof(double) * 8 * N);
+  double* Bc = (double*)malloc(sizeof(double) * 3 * N);
+  if (!L8 || !Bc) {
+    free(L8);
+    free(Bc);
+    return -3;
+  }
+  int rc = rhs_full(c, Us, Ps, bs, L8);
+  if (rc) {
+    free(L8);
+    free(Bc);
+    return rc;
+  }
+  /* the staggered field: literal RK forms (A7) per face */
+  for (long long e = 0; e < 3 * N; e++) {
+    const double Lb = L8[5 * N + e];
+    if (s == 1)
+      bout[e] = bn[e] + dt * Lb;
+    else if (s == 2)
+      bout[e] = 0.75 * bn[e] + 0.25 * (bs[e] + dt * Lb);
+    else
+      bout[e] = (1.0 / 3.0) * bn[e] + (2.0 / 3.0) * (bs[e] + dt * Lb);
+  }
+  orc_uct_centre(c, bout, Bc);
+  long long nfl = 0, nfa = 0;
+  int nt = nthreads_of(c);
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2];
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(+ : nfl, nfa)
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        const long long id = lin(c, i, j, k);
+        double un[8], us[8], L[8], Uo[8], pp[5], Po[5];
+        for (int q = 0; q < 8; q++) {
+          un[q] = Un[q * N + id];
+          us[q] = Us[q * N + id];
+          L[q] = L8[q * N + id];
+        }
+        for (int q = 0; q < 5; q++) pp[q] = Ps[q * N + id];
+        combine(s, dt, un, us, L, Uo);
+        for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a * N + id]; /* A37: U_B = I6(b) */
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        orc_met m;
+        orc_met_eval(c, x, &m);
+        orc_c2p_floors(c, &m, Uo, pp, Po, &nfl, &nfa);
+        for (int q = 0; q < 8; q++) Uout[q * N + id] = Uo[q];
+        for (int q = 0; q < 5; q++) Pout[q * N + id] = Po[q];
+      }
+  free(L8);
+  free(Bc);
+  if (cnt) {
+    cnt->floor_events += nfl;
+    cnt->c2p_failures += nfa;
+  }
+  return 0;
+}
+
+int orc_step_uct(const orc_cfg* c, double dt, double* U8, double* P5, double* b3, orc_counts* cnt) {
+  if (!uct_ok(c)) return -1;
+  const long long N = ncells(c);
+  double* U1 = (double*)malloc(sizeof(double) * 8 * N);
+  double* P1 = (double*)malloc(sizeof(double) * 5 * N);
+  double* b1 = (double*)malloc(sizeof(double) * 3 * N);
+  double* U2 = (double*)malloc(sizeof(double) * 8 * N);
+  double* P2 = (double*)malloc(sizeof(double) * 5 * N);
+  double* b2 = (double*)malloc(sizeof(double) * 3 * N);
+  int rc = -3;
+  if (U1 && P1 && b1 && U2 && P2 && b2) {
+    rc = orc_stage_uct(c, 1, dt, U8, U8, P5, b3, b3, U1, P1, b1, cnt);
+    if (!rc) rc = orc_stage_uct(c, 2, dt, U8, U1, P1, b3, b1, U2, P2, b2, cnt);
+    if (!rc) rc = orc_stage_uct(c, 3, dt, U8, U2, P2, b3, b2, U8, P5, b3, cnt);
+  }
+  free(U1);
+  free(P1);
+  free(b1);
+  free(U2);
+  free(P2);
+  free(b2);
+  return rc;
 }
