@@ -77,7 +77,8 @@ typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_met
  *      4 = MC2, the monotonized-central limited linear reconstruction (reading A35),
  *      5 = PPM (Colella & Woodward 1984 constraints on point values, reading A36).
  * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
- * divb: 0 = field-CD constrained transport (A6, default), 1 = none.
+ * divb: 0 = field-CD constrained transport (A6, default), 1 = none, 2 = UCT: staggered
+ *   field + upwind constrained transport (readings A37-A41; echo_set_face_field below).
  * der_jump: DER shock switch (A31): the DER correction at a face is dropped
  *   (H = F) when one of the 5 faces of its stencil joins two cells whose rho or
  *   p differ by more than der_jump x the smaller of the two; <= 0 disables it
@@ -134,6 +135,21 @@ int echo_set_prims(echo_ctx* ctx, const double* p8, int on_device);
 
 /* Current user prims P8 (B = U_B / sqrt(gamma), v = u~ / W). */
 int echo_get_prims(echo_ctx* ctx, double* p8, int on_device);
+
+/* UCT (grid.divb = 2; readings A37-A41; Minkowski, periodic axes only,
+ * refused at echo_create otherwise): the magnetic state is the staggered field
+ * b3[a][n3][n2][n1] = sqrt(gamma) B^a at the centre of the face i_a + 1/2 of cell
+ * (i1, i2, i3) (point values).  After echo_set_prims (which supplies the hydro
+ * primitives; its B is replaced), echo_set_face_field sets b, the cell-centred field
+ * U_B = I6(b) (6-point midpoint interpolation along a) and U.  Every step then
+ * updates b by the UCT-HLL edge EMFs with the DER operator along the
+ * differentiation direction, which keeps sum_a delta_a Dh_a b^a at roundoff.
+ * Stepping a divb = 2 context before echo_set_face_field is ECHO_E_ORDER, as is
+ * echo_set_cons (U_B must stay I6(b)).  echo_rhs returns L(b^a) at the faces in
+ * slots 5..7.  echo_get_face_field returns the current b (same layout).  Host
+ * buffers synchronise; device buffers are stream-ordered. */
+int echo_set_face_field(echo_ctx* ctx, const double* b3, int on_device);
+int echo_get_face_field(echo_ctx* ctx, double* b3, int on_device);
 
 /* Replace U^n by u8 and recover P by con2prim + floors (guess: current P).
  * Requires a prior echo_set_prims (ECHO_E_ORDER). */

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libecho_b200.so")
-SOURCES = ["march.cu", "update.cu", "api.cu", "metric_tables.cpp"]
+SOURCES = ["march.cu", "update.cu", "uct.cu", "api.cu", "metric_tables.cpp"]
 HEADERS = ["echo_dev.cuh", "echo_kernels.h", "metric_tables.h", "cell_physics.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -22,10 +22,11 @@ namespace {
 
 enum KernelClass {
   kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kLayout,
-  kCflDt, kNumClasses
+  kCflDt, kUctEmf, kUctInduct, kUctCell, kNumClasses
 };
-const char* kNames[kNumClasses] = {"sweep_x",   "sweep_y",   "sweep_z",   "update_stage", "update_rhs", "con2prim",
-                                   "max_speed", "prim2cons", "get_prims", "layout",       "cfl_dt"};
+const char* kNames[kNumClasses] = {"sweep_x",   "sweep_y",   "sweep_z",   "update_stage", "update_rhs",
+                                   "con2prim",  "max_speed", "prim2cons", "get_prims",    "layout",
+                                   "cfl_dt",    "uct_emf",   "uct_induct", "uct_cell"};
 
 std::string g_create_error;
 
@@ -54,6 +55,11 @@ struct echo_ctx {
   double* Us = nullptr;   // U^s
   double* P = nullptr;    // rho, u~, p, B
   double* R = nullptr;    // rhs + EMF accumulator
+  // UCT (divb = 2, uct.cu): staggered field (slots 0..2 b^n, 3..5 b^s), face data per axis, edge EMFs
+  double* Bst = nullptr;
+  double* FS[3] = {nullptr, nullptr, nullptr};
+  double* Ed = nullptr;
+  bool have_faces = false;
   double* scratch = nullptr;  // 8N, lazily for layout conversions / host-buffer transfers
   unsigned long long* dcnt = nullptr;  // [0] floors [1] failures [2] max speed bits
   long long* dbad = nullptr;
@@ -122,13 +128,24 @@ static int ensure_scratch(echo_ctx* c) {
   return ECHO_OK;
 }
 
-// sweeps x, y, z of the current stage input P (B included) into R
+static bool is_uct(const echo_ctx* c) { return c->g.divb == 2; }
+// the stage-input staggered field (UCT)
+static double* bcur(echo_ctx* c) { return c->Bst + (c->next_stage == 1 ? 0 : 3) * c->g.vs; }
+
+// sweeps x, y, z of the current stage input P (B included) into R; UCT: then the edge EMFs
 static int run_sweeps(echo_ctx* c) {
+  const bool uct = is_uct(c);
   for (int ax = 0; ax < 3; ax++) {
     cudaError_t e = launch(c, kSweepX + ax, [&] {
-      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), c->R, c->st);
+      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), c->R, c->st,
+                          uct ? bcur(c) : nullptr, uct ? c->FS[ax] : nullptr);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
+  }
+  if (uct) {
+    const double* fs[3] = {c->FS[0], c->FS[1], c->FS[2]};
+    cudaError_t e = launch(c, kUctEmf, [&] { return launch_uct_emf(c->g, fs, bcur(c), c->Ed, c->st); });
+    if (e != cudaSuccess) return cuda_fail(c, e, "uct emf launch");
   }
   return ECHO_OK;
 }
@@ -180,6 +197,21 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
   // the last stage also reduces the CFL rate of the new state (a9 fused into K3)
   unsigned long long* cfl = (s == 3) ? c->dcnt + 2 : nullptr;
   if (cfl) CK(cudaMemsetAsync(cfl, 0, sizeof(unsigned long long), c->st), "stage");
+  if (is_uct(c)) {  // staggered field first (A41), then the cells read its centring (A37)
+    cudaError_t e = launch(c, kUctInduct, [&] {
+      return launch_uct_induct(c->g, 0, s, dt, dtp, c->Ed, c->Bst, nullptr, c->st);
+    });
+    if (e == cudaSuccess)
+      e = launch(c, kUctCell, [&] {
+        return launch_uct_cell(c->g, c->e, s, dt, dtp, c->R, c->Un, Uin, Uout, c->P, c->Bst, c->dcnt, cfl, c->st);
+      });
+    if (e != cudaSuccess) return cuda_fail(c, e, "uct update launch");
+    c->cfl_valid = (s == 3);
+    c->stages++;
+    c->next_stage = (s == 3) ? 1 : s + 1;
+    c->swept = 0;
+    return ECHO_OK;
+  }
   const GhostLinks gl = ghost_links(c, s);
   cudaError_t e = launch(c, kUpdateStage, [&] {
     return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Un, Uin, Uout, c->P, nullptr,
@@ -222,7 +254,13 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   }
   if (grid->rec < 0 || grid->rec > 5) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..5");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
-  if (grid->divb != 0 && grid->divb != 1) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0 or 1");
+  if (grid->divb < 0 || grid->divb > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0, 1 or 2");
+  if (grid->divb == 2) {  // UCT (A37): Minkowski, periodic axes
+    bool per = true;
+    for (int a = 0; a < 3; a++) per = per && grid->bc[a][0] == ECHO_BC_PERIODIC && grid->bc[a][1] == ECHO_BC_PERIODIC;
+    if (!per || metric->kind != ECHO_METRIC_MINKOWSKI)
+      return fail(nullptr, ECHO_E_ARG, "echo_create: divb = 2 (UCT) needs a Minkowski metric and periodic axes");
+  }
   if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");
   if (!(eos->rho_floor > 0.0) || !(eos->p_floor > 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: floors > 0 violated");
   if (!(eos->w_max > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: w_max > 1 violated");
@@ -296,6 +334,17 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     echo_destroy(c);
     return fail(nullptr, ECHO_E_OOM, "echo_create: device allocation failed");
   }
+  if (g.divb == 2) {
+    double** uct_arrays[5] = {&c->Bst, &c->FS[0], &c->FS[1], &c->FS[2], &c->Ed};
+    for (double** a : uct_arrays)
+      if (cudaMalloc(a, sizeof(double) * rec) != cudaSuccess) {
+        cudaGetLastError();
+        echo_destroy(c);
+        return fail(nullptr, ECHO_E_OOM, "echo_create: UCT field allocation failed");
+      } else {
+        cudaMemset(*a, 0, sizeof(double) * rec);
+      }
+  }
   cudaMemset(c->dcnt, 0, 4 * sizeof(unsigned long long));
   for (double* b : c->alloc_base) cudaMemset(b, 0, sizeof(double) * rec);
   if (ks) {
@@ -338,6 +387,9 @@ void echo_destroy(echo_ctx* c) {
   cudaFree(c->dbad);
   cudaFree(c->tables);
   cudaFree(c->dadv);
+  cudaFree(c->Bst);
+  for (double* f : c->FS) cudaFree(f);
+  cudaFree(c->Ed);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->hpin) cudaFreeHost(c->hpin);
@@ -390,6 +442,7 @@ int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
     return fail(c, ECHO_E_UNPHYSICAL, buf);
   }
   c->have_state = true;
+  c->have_faces = false;
   c->cfl_valid = false;
   c->next_stage = 1;
   c->swept = 0;
@@ -446,9 +499,40 @@ int echo_get_state(echo_ctx* c, double* un8, double* us8, double* p5, int on_dev
   return rc;
 }
 
+int echo_set_face_field(echo_ctx* c, const double* b3, int on_device) {
+  if (!c || !b3) return c ? fail(c, ECHO_E_ARG, "echo_set_face_field: NULL buffer") : ECHO_E_ARG;
+  if (!is_uct(c)) return fail(c, ECHO_E_ORDER, "echo_set_face_field: the context is not divb = 2 (UCT)");
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_set_face_field: needs a prior echo_set_prims (hydro state)");
+  const double* src = b3;
+  if (!on_device) {
+    int rc = ensure_scratch(c);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->scratch, b3, sizeof(double) * 3 * c->g.N, cudaMemcpyHostToDevice, c->st),
+       "echo_set_face_field");
+    src = c->scratch;
+  }
+  CK(launch(c, kLayout, [&] { return launch_layout(c->g, src, c->Bst, 3, false, c->st); }), "echo_set_face_field");
+  CK(launch(c, kPrim2Cons, [&] { return launch_uct_centre_p2c(c->g, c->e, c->P, c->Un, c->Bst, c->st); }),
+     "echo_set_face_field");
+  if (!on_device) CK(cudaStreamSynchronize(c->st), "echo_set_face_field");
+  c->have_faces = true;
+  c->cfl_valid = false;
+  c->next_stage = 1;
+  c->swept = 0;
+  return ECHO_OK;
+}
+
+int echo_get_face_field(echo_ctx* c, double* b3, int on_device) {
+  if (!c || !b3) return c ? fail(c, ECHO_E_ARG, "echo_get_face_field: NULL buffer") : ECHO_E_ARG;
+  if (!is_uct(c) || !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_get_face_field: no staggered field (divb = 2)");
+  return export_field(c, b3, bcur(c), 3, on_device, "echo_get_face_field");
+}
+
 int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
   if (!c || !u8) return c ? fail(c, ECHO_E_ARG, "echo_set_cons: NULL buffer") : ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_set_cons: needs a prior echo_set_prims (con2prim guess)");
+  if (is_uct(c))
+    return fail(c, ECHO_E_ORDER, "echo_set_cons: with divb = 2 the field is staggered: use echo_set_prims + echo_set_face_field");
   const double* src = u8;
   if (!on_device) {
     int rc = ensure_scratch(c);
@@ -464,6 +548,7 @@ int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
 int echo_rhs(echo_ctx* c, double* l8, int on_device) {
   if (!c || !l8) return c ? fail(c, ECHO_E_ARG, "echo_rhs: NULL buffer") : ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_rhs: no state");
+  if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_rhs: divb = 2 needs echo_set_face_field first");
   double* dst = l8;
   if (!on_device) {
     int rc = ensure_scratch(c);
@@ -478,6 +563,10 @@ int echo_rhs(echo_ctx* c, double* l8, int on_device) {
                          nullptr, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update(rhs) launch");
+  if (is_uct(c)) {
+    e = launch(c, kUctInduct, [&] { return launch_uct_induct(c->g, 1, 0, 0.0, nullptr, c->Ed, c->Bst, dst, c->st); });
+    if (e != cudaSuccess) return cuda_fail(c, e, "uct induct(rhs) launch");
+  }
   if (!on_device) {
     CK(cudaMemcpyAsync(l8, c->scratch, sizeof(double) * 8 * c->g.N, cudaMemcpyDeviceToHost, c->st), "echo_rhs");
     CK(cudaStreamSynchronize(c->st), "echo_rhs");
@@ -519,6 +608,7 @@ int echo_con2prim(echo_ctx* c, echo_stats_t* delta) {
 int echo_stage(echo_ctx* c, int s, double dt) {
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage: no state (call echo_set_prims first)");
+  if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_stage: divb = 2 needs echo_set_face_field first");
   if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage: s must be 1, 2 or 3");
   if (s != c->next_stage || c->swept) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage: dt > 0 violated");
@@ -528,6 +618,7 @@ int echo_stage(echo_ctx* c, int s, double dt) {
 int echo_step(echo_ctx* c, double dt) {
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_step: no state (call echo_set_prims first)");
+  if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_step: divb = 2 needs echo_set_face_field first");
   if (c->next_stage != 1) return fail(c, ECHO_E_ORDER, "echo_step: a step is in progress (finish its stages)");
   if (c->g.zhalo)
     return fail(c, ECHO_E_ORDER,
@@ -612,6 +703,7 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
   if (steps_done) *steps_done = 0;
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_advance: no state (call echo_set_prims first)");
+  if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_advance: divb = 2 needs echo_set_face_field first");
   if (c->next_stage != 1 || c->swept) return fail(c, ECHO_E_ORDER, "echo_advance: a step is in progress (finish its stages)");
   if (c->g.zhalo)
     return fail(c, ECHO_E_ORDER, "echo_advance: halo (slab) boundaries need a halo exchange before every stage");
@@ -689,6 +781,7 @@ int echo_stats(echo_ctx* c, echo_stats_t* out) {
 int echo_stage_sweeps(echo_ctx* c, int s) {
   if (!c) return ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: no state");
+  if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: divb = 2 needs echo_set_face_field first");
   if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage_sweeps: s must be 1, 2 or 3");
   if (s != c->next_stage || c->swept) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: stages must run in order");
   int rc = run_sweeps(c);

@@ -242,8 +242,10 @@ ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, 
 }
 
 // densitised HLL flux (7 comps) between two reconstructed states at one face (A4)
+// fs (UCT, A38): if not NULL, v^1..3 of the left and of the right state, a+ = S_R, a- = -S_L
 template <class M>
-ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* pr, int AX, double* F) {
+ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* pr, int AX, double* F,
+                     double* fs = nullptr) {
   State sl, sr;
   make_state(m, e, pl, sl);
   make_state(m, e, pr, sr);
@@ -255,6 +257,15 @@ ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* 
   speeds(m, e, pr, sr, AX, lmR, lpR);
   const double sL = dmin(0.0, dmin(lmL, lmR));
   const double sR = dmax(0.0, dmax(lpL, lpR));
+  if (fs) {
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      fs[i] = sl.v[i];
+      fs[3 + i] = sr.v[i];
+    }
+    fs[6] = sR;
+    fs[7] = -sL;
+  }
   const double den = sR - sL;
   if (den > 0.0) {
     const double inv = m.sqrtg() * frcp(den);

@@ -16,8 +16,11 @@ namespace echo {
 // a marching pipeline over whole lines (no tile-halo recomputation)
 // P: stage-input primitives; UB: the array holding B^i in slots 5..7 (P in a curved metric,
 // the stage-input U in Minkowski, where B^i = U_B)
+// UCT (divb = 2): Bface = the stage-input staggered field (slot a = b^a), FSo = this axis's
+// face-data array (uct.cu); NULL otherwise
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                         const double* UB, double* R, cudaStream_t st);
+                         const double* UB, double* R, cudaStream_t st, const double* Bface = nullptr,
+                         double* FSo = nullptr);
 
 // slab mode, fused ghost exchange: K3 also stores the new P and U of the owned planes
 // next to a linked side straight into the neighbour slab's ghost planes (peer memory:
@@ -65,5 +68,20 @@ cudaError_t launch_get_prims(bool ks, const GridP& g, const MetTables& mt, const
 
 // device records (first nq variables) <-> caller arrays [q][cell]
 cudaError_t launch_layout(const GridP& g, const double* src, double* dst, int nq, bool to_soa, cudaStream_t st);
+
+// ---- UCT (divb = 2, uct.cu; DESIGN A37-A41): Bst slots 0..2 b^n, 3..5 b^s; FS[a] face data
+// of axis a; Ed slots 0..2 the edge EMFs
+cudaError_t launch_uct_emf(const GridP& g, const double* const FS[3], const double* Bin, double* Ed, cudaStream_t st);
+// mode 0: RK stage s of the face field (dt, or from dtp as launch_update); mode 1: L(b) into
+// Lout[5 + a][cell]
+cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const double* dtp, const double* Ed,
+                              double* Bst, double* Lout, cudaStream_t st);
+// hydro RK combine (rhs from the sweeps in R), U_B = I6(b), con2prim + floors, CFL rate
+cudaError_t launch_uct_cell(const GridP& g, const EosP& e, int s, double dt, const double* dtp, const double* R,
+                            const double* Un, const double* Us, double* Uout, double* P, const double* Bst,
+                            unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st);
+// U_B = I6(b^n) and U recomputed from the state's hydro primitives (echo_set_face_field)
+cudaError_t launch_uct_centre_p2c(const GridP& g, const EosP& e, const double* P, double* U, const double* Bst,
+                                  cudaStream_t st);
 
 }  // namespace echo

@@ -224,11 +224,16 @@ ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int 
   for (int x = -kG + i; x <= GE::B_FIRST + 2 * GE::CH + 4; x += GE::CH) load_cells<AX>(g, lg, lb, t, x, vec, P, UB, sbase);
 }
 
-template <int AX, bool KS, int DER, int REC, bool DN>
+// DM: divergence treatment 0 field-CD (EMF Omega into R slots 5..7), 1 none (B flux
+// differences), 2 UCT (uct.cu: the normal field of each face from the staggered Bface,
+// the face data of the EMF step into FSo, hydro only into R)
+template <int AX, bool KS, int DER, int REC, int DM>
 __global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
-        const double* __restrict__ UB, double* R) {
+        const double* __restrict__ UB, double* R, const double* __restrict__ Bface, double* __restrict__ FSo) {
   using GE = Geo<AX>;
+  constexpr bool DN = DM == 1;
+  constexpr bool UCT = DM == 2;
   constexpr int CH = GE::CH, RING = GE::RING, RINGF = GE::RINGF, RR = GE::RR;
   // A31 flags as ballots: warp-local kernels whose chunk of a line lies in one warp
   constexpr bool kBallot = ECHO_BALLOT_FLAGS && GE::WARP_LOCAL && (AX == 0 ? CH == 32 : CH * GE::NL == 32);
@@ -280,7 +285,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
 #pragma unroll
           for (int q = 0; q < 7; q++) {
-            if (!accumulates<AX, DN>(q)) continue;
+            if (!accumulates<AX, DN>(q) || (UCT && q >= 5)) continue;
             if (vec) cp_async16(s + 8u * q * GE::VA, src + out_slot<AX, DN>(q) * vs);
             else cp_async8(s + 8u * q * GE::VA, src + out_slot<AX, DN>(q) * vs);
           }
@@ -390,6 +395,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
           double* dst = R + lb + (X0 + i + lg.coff) * as;
 #pragma unroll
           for (int q = 0; q < 7; q++) {
+            if (UCT && q >= 5) continue;
             double d;
             if (q < 5 || DN) {
               d = -(H[q] - Hm[q]) * idxa;
@@ -422,6 +428,18 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
             else if (AX == 1) rec = f1_rec(mt, tt, af);
             else rec = cen_rec(mt, tt, zz);
             hll_face(load_met(rec), e, pl, qR, AX, F);
+          } else if constexpr (UCT) {
+            // A37: both states take the staggered normal field of face xf + 1/2 (owned by cell xf)
+            const long long fo = lb + (long long)map_index(xf, lg.na, 0, 0) * as;
+            const double bnv = Bface[fo + AX * vs];
+            pl[5 + AX] = bnv;
+            qR[5 + AX] = bnv;
+            double fsv[8];
+            hll_face(FlatMet(), e, pl, qR, AX, F, fsv);
+            if (xf >= 0 && xf < lg.na && line_ok) {
+#pragma unroll
+              for (int m = 0; m < 8; m++) FSo[lb + (long long)xf * as + m * vs] = fsv[m];
+            }
           } else {
             hll_face(FlatMet(), e, pl, qR, AX, F);
           }
@@ -435,11 +453,11 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
   cp_async_wait0();
 }
 
-template <int AX, bool KS, int DER, int REC, bool DN>
+template <int AX, bool KS, int DER, int REC, int DM>
 static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB,
-                              double* R, cudaStream_t st) {
+                              double* R, const double* Bface, double* FSo, cudaStream_t st) {
   using GE = Geo<AX>;
-  auto kern = k_march<AX, KS, DER, REC, DN>;
+  auto kern = k_march<AX, KS, DER, REC, DM>;
   static int grid_cap = 0;
   if (!grid_cap) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GE::SMEM);
@@ -472,47 +490,51 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
   lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
   lg.nunits = (long long)lg.tt_groups * lg.nz;
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
-  kern<<<blocks, GE::THREADS, GE::SMEM, st>>>(g, e, mt, lg, P, UB, R);
+  kern<<<blocks, GE::THREADS, GE::SMEM, st>>>(g, e, mt, lg, P, UB, R, Bface, FSo);
   return cudaGetLastError();
 }
 
 template <int AX, bool KS, int DER, int REC>
 static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
-                             cudaStream_t st) {
-  if (g.divb == 1) return launch_one<AX, KS, DER, REC, true>(g, e, mt, P, UB, R, st);
-  return launch_one<AX, KS, DER, REC, false>(g, e, mt, P, UB, R, st);
+                             const double* Bface, double* FSo, cudaStream_t st) {
+  if (g.divb == 2) {
+    if constexpr (KS) return cudaErrorInvalidValue;  // UCT: Minkowski only (A37)
+    else return launch_one<AX, KS, DER, REC, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
+  }
+  if (g.divb == 1) return launch_one<AX, KS, DER, REC, 1>(g, e, mt, P, UB, R, nullptr, nullptr, st);
+  return launch_one<AX, KS, DER, REC, 0>(g, e, mt, P, UB, R, nullptr, nullptr, st);
 }
 template <int AX, bool KS, int DER>
 static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
-                              cudaStream_t st) {
-  if (g.rec == 5) return launch_dn<AX, KS, DER, 5>(g, e, mt, P, UB, R, st);
-  if (g.rec == 4) return launch_dn<AX, KS, DER, 4>(g, e, mt, P, UB, R, st);
-  if (g.rec == 3) return launch_dn<AX, KS, DER, 3>(g, e, mt, P, UB, R, st);
-  if (g.rec == 2) return launch_dn<AX, KS, DER, 2>(g, e, mt, P, UB, R, st);
-  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, UB, R, st);
-  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, UB, R, st);
+                              const double* Bface, double* FSo, cudaStream_t st) {
+  if (g.rec == 5) return launch_dn<AX, KS, DER, 5>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (g.rec == 4) return launch_dn<AX, KS, DER, 4>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (g.rec == 3) return launch_dn<AX, KS, DER, 3>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (g.rec == 2) return launch_dn<AX, KS, DER, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, UB, R, Bface, FSo, st);
+  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, UB, R, Bface, FSo, st);
 }
 template <int AX, bool KS>
 static cudaError_t launch_der(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
-                              cudaStream_t st) {
-  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, UB, R, st);
-  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, UB, R, st);
-  return launch_rec<AX, KS, 6>(g, e, mt, P, UB, R, st);
+                              const double* Bface, double* FSo, cudaStream_t st) {
+  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
+  return launch_rec<AX, KS, 6>(g, e, mt, P, UB, R, Bface, FSo, st);
 }
 
 }  // namespace march
 
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                         const double* UB, double* R, cudaStream_t st) {
+                         const double* UB, double* R, cudaStream_t st, const double* Bface, double* FSo) {
   using namespace march;
   if (ks) {
-    if (axis == 0) return launch_der<0, true>(g, e, mt, P, UB, R, st);
-    if (axis == 1) return launch_der<1, true>(g, e, mt, P, UB, R, st);
-    return launch_der<2, true>(g, e, mt, P, UB, R, st);
+    if (axis == 0) return launch_der<0, true>(g, e, mt, P, UB, R, Bface, FSo, st);
+    if (axis == 1) return launch_der<1, true>(g, e, mt, P, UB, R, Bface, FSo, st);
+    return launch_der<2, true>(g, e, mt, P, UB, R, Bface, FSo, st);
   }
-  if (axis == 0) return launch_der<0, false>(g, e, mt, P, UB, R, st);
-  if (axis == 1) return launch_der<1, false>(g, e, mt, P, UB, R, st);
-  return launch_der<2, false>(g, e, mt, P, UB, R, st);
+  if (axis == 0) return launch_der<0, false>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (axis == 1) return launch_der<1, false>(g, e, mt, P, UB, R, Bface, FSo, st);
+  return launch_der<2, false>(g, e, mt, P, UB, R, Bface, FSo, st);
 }
 
 }  // namespace echo

@@ -1,0 +1,298 @@
+// uct.cu — the staggered-field update of divb = 2 (UCT; DESIGN.md
+// readings A37-A41): Minkowski, periodic axes.
+//
+// State: Bst record array, slots 0..2 = b^n, 3..5 = b^s, where b^a = sqrt(gamma) B^a at
+// the face i_a + 1/2 owned by cell i.  The sweeps (march.cu, DM = 2) take the normal
+// field of every face from the stage-input b and leave per owned face, in FS[a] (one
+// record array per axis), the face data of the EMF step: v^1..3 of the left and of the
+// right HLL state, a+ = S_R, a- = -S_L.  Then per stage:
+//   k_uct_emf     E^c at the edge (i_p + 1/2, i_q + 1/2, i_c) owned by each cell, (c, p, q)
+//                 cyclic: 4 quadrant states from double reconstructions of the face data
+//                 (A38) combined by the UCT-HLL formula (A39, A40)          -> Ed slots 0..2
+//   k_uct_induct  L(b^p) = -delta_q Dh_q E^c + delta_c Dh_c E^q (A41) and the literal RK
+//                 form of stage s per face (or L(b) alone for echo_rhs)     -> Bst
+//   k_uct_cell    hydro RK combine from the sweeps' rhs, U_B = I6(b) of the new field (A37),
+//                 con2prim + floors, the CFL rate of the new state           -> U, P
+// One thread per cell; neighbours through the periodic index map (L1/L2).
+#include <cuda_runtime.h>
+
+#include "cell_physics.cuh"
+#include "echo_dev.cuh"
+#include "echo_kernels.h"
+
+namespace echo {
+namespace {
+
+ECHO_D long long rec_shift(const GridP& g, const int x[3], int a, int d) {
+  int y[3] = {x[0], x[1], x[2]};
+  y[a] = map_index(y[a] + d, g.n[a], 0, 0);
+  return rec_base(g, y[0], y[1], y[2]);
+}
+
+// the two one-sided values at +1/2 from samples f[0..5] at -2..3 (A38): lo from f[0..4],
+// hi the mirror from f[5..1] (rec_both of the cells at 0 and +1; the unused halves are dead code)
+template <int REC>
+ECHO_D void rec_pair(const double f[6], double& lo, double& hi) {
+  double dead0, dead1;
+  rec_both<REC>(f[0], f[1], f[2], f[3], f[4], lo, dead0);
+  rec_both<REC>(f[1], f[2], f[3], f[4], f[5], dead1, hi);
+}
+
+template <int REC>
+__global__ void __launch_bounds__(kCellThreads)
+k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restrict__ FSy,
+          const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= g.N) return;
+  int x[3];
+  cell_ijk(g, id, x[0], x[1], x[2]);
+  const double* FS[3] = {FSx, FSy, FSz};
+  const long long vs = g.vs;
+  const long long rb = rec_base(g, x[0], x[1], x[2]);
+#pragma unroll
+  for (int cc = 0; cc < 3; cc++) {
+    const int p = (cc + 1) % 3, q = (cc + 2) % 3;
+    const int comp[2] = {p, q};
+    double f[6];
+    long long oq[6], op[6];
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+      oq[m] = rec_shift(g, x, q, m - 2);
+      op[m] = rec_shift(g, x, p, m - 2);
+    }
+    // p-face states (W: slots 0..2, E: 3..5) along q -> S, N; q-face states (S, N) along p -> W, E
+    double pS[2][2], pN[2][2], qW[2][2], qE[2][2];
+#pragma unroll
+    for (int side = 0; side < 2; side++)
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+#pragma unroll
+        for (int m = 0; m < 6; m++) f[m] = __ldg(FS[p] + oq[m] + (3 * side + comp[k]) * vs);
+        rec_pair<REC>(f, pS[side][k], pN[side][k]);
+#pragma unroll
+        for (int m = 0; m < 6; m++) f[m] = __ldg(FS[q] + op[m] + (3 * side + comp[k]) * vs);
+        rec_pair<REC>(f, qW[side][k], qE[side][k]);
+      }
+    double bpS, bpN, bqW, bqE;
+#pragma unroll
+    for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + oq[m] + p * vs);
+    rec_pair<REC>(f, bpS, bpN);
+#pragma unroll
+    for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + op[m] + q * vs);
+    rec_pair<REC>(f, bqW, bqE);
+    // A40: max over the two faces meeting at the edge (oq[3] = +1 along q, op[3] = +1 along p)
+    const double app = fmax(__ldg(FS[p] + rb + 6 * vs), __ldg(FS[p] + oq[3] + 6 * vs));
+    const double apm = fmax(__ldg(FS[p] + rb + 7 * vs), __ldg(FS[p] + oq[3] + 7 * vs));
+    const double aqp = fmax(__ldg(FS[q] + rb + 6 * vs), __ldg(FS[q] + op[3] + 6 * vs));
+    const double aqm = fmax(__ldg(FS[q] + rb + 7 * vs), __ldg(FS[q] + op[3] + 7 * vs));
+    // A38 quadrant velocities (v^p, v^q), A39 quadrant EMFs E = v^q B^p - v^p B^q
+    double v[4][2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      v[0][k] = 0.5 * (pS[0][k] + qW[0][k]);  // WS
+      v[1][k] = 0.5 * (pN[0][k] + qW[1][k]);  // WN
+      v[2][k] = 0.5 * (pS[1][k] + qE[0][k]);  // ES
+      v[3][k] = 0.5 * (pN[1][k] + qE[1][k]);  // EN
+    }
+    const double EWS = v[0][1] * bpS - v[0][0] * bqW;
+    const double EWN = v[1][1] * bpN - v[1][0] * bqW;
+    const double EES = v[2][1] * bpS - v[2][0] * bqE;
+    const double EEN = v[3][1] * bpN - v[3][0] * bqE;
+    const double sp = app + apm, sq = aqp + aqm;
+    double E;
+    if (sp > 0.0 && sq > 0.0) {
+      const double isp = 1.0 / sp, isq = 1.0 / sq;
+      E = (app * (aqp * EWS + aqm * EWN) + apm * (aqp * EES + aqm * EEN)) * (isp * isq) +
+          app * apm * (bqE - bqW) * isp - aqp * aqm * (bpN - bpS) * isq;
+    } else {  // unreachable for p > 0 (A4): central average
+      E = 0.25 * (EWS + EWN + EES + EEN);
+    }
+    Ed[rb + cc * vs] = E;
+  }
+}
+
+// A41 induction of the three faces owned by a cell; MODE 0: RK stage s into Bst (dt from
+// dtp when set; halted loop: nothing), MODE 1: L(b) into Lout[5 + a][cell] (echo_rhs)
+template <int DER>
+__global__ void __launch_bounds__(kCellThreads)
+k_uct_induct(const GridP g, int mode, int s, double dt, const double* dtp, const double* __restrict__ Ed,
+             double* Bst, double* __restrict__ Lout) {
+  if (dtp) {
+    if (dtp[1] != 0.0) return;
+    dt = dtp[0];
+  }
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= g.N) return;
+  int x[3];
+  cell_ijk(g, id, x[0], x[1], x[2]);
+  const long long vs = g.vs;
+  const long long rb = rec_base(g, x[0], x[1], x[2]);
+#pragma unroll
+  for (int p = 0; p < 3; p++) {
+    const int cc = (p + 2) % 3, q = (p + 1) % 3;
+    double Eq[6], Ec[6];  // E^cc along q, E^q along cc: samples -3..2
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+      Eq[m] = __ldg(Ed + rec_shift(g, x, q, m - 3) + cc * vs);
+      Ec[m] = __ldg(Ed + rec_shift(g, x, cc, m - 3) + q * vs);
+    }
+    const double Lb = -(der5<DER>(Eq[1], Eq[2], Eq[3], Eq[4], Eq[5]) - der5<DER>(Eq[0], Eq[1], Eq[2], Eq[3], Eq[4])) *
+                          g.idx[q] +
+                      (der5<DER>(Ec[1], Ec[2], Ec[3], Ec[4], Ec[5]) - der5<DER>(Ec[0], Ec[1], Ec[2], Ec[3], Ec[4])) *
+                          g.idx[cc];
+    if (mode == 1) {
+      Lout[(5 + p) * g.N + id] = Lb;
+      continue;
+    }
+    const double bn = Bst[rb + p * vs];
+    double bo;
+    if (s == 1) {
+      bo = bn + dt * Lb;
+      Bst[rb + (3 + p) * vs] = bo;
+    } else if (s == 2) {
+      bo = 0.75 * bn + 0.25 * (Bst[rb + (3 + p) * vs] + dt * Lb);
+      Bst[rb + (3 + p) * vs] = bo;
+    } else {
+      bo = (1.0 / 3.0) * bn + (2.0 / 3.0) * (Bst[rb + (3 + p) * vs] + dt * Lb);
+      Bst[rb + p * vs] = bo;
+    }
+  }
+}
+
+// A37: I6 of the face field at slot offset `slot` of Bst, per component, at cell x
+ECHO_D void centre_field(const GridP& g, const double* __restrict__ Bst, int slot, const int x[3], double Bc[3]) {
+  const long long vs = g.vs;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    double f[6];
+#pragma unroll
+    for (int m = 0; m < 6; m++) f[m] = Bst[rec_shift(g, x, a, m - 3) + (slot + a) * vs];
+    Bc[a] = fma(3.0, f[0] + f[5], fma(-25.0, f[1] + f[4], 150.0 * (f[2] + f[3]))) * (1.0 / 256.0);
+  }
+}
+
+__global__ void __launch_bounds__(kCellThreads, 3)
+k_uct_cell(const GridP g, const EosP e, int s, double dt, const double* dtp, const double* __restrict__ R,
+           const double* Un, const double* Us, double* Uout, double* P, const double* __restrict__ Bst,
+           unsigned long long* counters, unsigned long long* cfl_out) {
+  if (dtp) {
+    if (dtp[1] != 0.0) return;  // uniform over the grid (no thread left at a block barrier)
+    dt = dtp[0];
+  }
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int ev = 0;
+  double rate = 0.0;
+  if (id < g.N) {
+    int x[3];
+    cell_ijk(g, id, x[0], x[1], x[2]);
+    const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
+    const FlatMet m;
+    double Pp[8], Uo[8];
+#pragma unroll
+    for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];
+    ld8(Un + rb, vs, Uo);
+    if (s == 1) {
+#pragma unroll
+      for (int q = 0; q < 5; q++) Uo[q] = Uo[q] + dt * R[rb + q * vs];
+    } else {
+      const double c0 = (s == 2) ? 0.75 : (1.0 / 3.0), c1 = (s == 2) ? 0.25 : (2.0 / 3.0);
+#pragma unroll
+      for (int q = 0; q < 5; q++) Uo[q] = c0 * Uo[q] + c1 * (Us[rb + q * vs] + dt * R[rb + q * vs]);
+    }
+    double Bc[3];
+    centre_field(g, Bst, s == 3 ? 0 : 3, x, Bc);  // the field this stage just wrote
+#pragma unroll
+    for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a];
+    double Po[8];
+    ev = c2p_floors(m, e, Uo, Pp, Po);
+#pragma unroll
+    for (int a = 0; a < 3; a++) Po[5 + a] = Uo[5 + a];
+    st8(Uout + rb, vs, Uo);
+    st_prims<false>(P + rb, vs, Po);
+    if (cfl_out) rate = cfl_rate(m, g, e, Po);
+  }
+  if (cfl_out) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rate = fmax(rate, __shfl_xor_sync(0xffffffffu, rate, o));
+    __shared__ double red[kCellThreads / 32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rate;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bm = red[0];
+      for (int w = 1; w < kCellThreads / 32; w++) bm = fmax(bm, red[w]);
+      atomicMax(cfl_out, (unsigned long long)__double_as_longlong(bm));
+    }
+  }
+  const unsigned fl = __reduce_add_sync(0xffffffffu, ev == 1 ? 1u : 0u);
+  const unsigned fa = __reduce_add_sync(0xffffffffu, ev == 2 ? 1u : 0u);
+  if ((threadIdx.x & 31) == 0) {
+    if (fl) atomicAdd(counters + 0, (unsigned long long)fl);
+    if (fa) atomicAdd(counters + 1, (unsigned long long)fa);
+  }
+}
+
+// set: U_B = I6(b^n) and U from the state's hydro primitives (a0 with the new field)
+__global__ void __launch_bounds__(kCellThreads)
+k_uct_centre_p2c(const GridP g, const EosP e, const double* __restrict__ P, double* __restrict__ U,
+                 const double* __restrict__ Bst) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= g.N) return;
+  int x[3];
+  cell_ijk(g, id, x[0], x[1], x[2]);
+  const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
+  double pr[8];
+#pragma unroll
+  for (int v = 0; v < 5; v++) pr[v] = P[rb + v * vs];
+  centre_field(g, Bst, 0, x, pr + 5);
+  State st;
+  const FlatMet m;
+  make_state(m, e, pr, st);
+  double u[8] = {st.D, st.S[0], st.S[1], st.S[2], st.tau, pr[5], pr[6], pr[7]};
+  st8(U + rb, vs, u);
+}
+
+template <int REC>
+cudaError_t emf_rec(const GridP& g, const double* const FS[3], const double* Bin, double* Ed, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
+  k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_uct_emf(const GridP& g, const double* const FS[3], const double* Bin, double* Ed, cudaStream_t st) {
+  switch (g.rec) {
+    case 1: return emf_rec<1>(g, FS, Bin, Ed, st);
+    case 2: return emf_rec<2>(g, FS, Bin, Ed, st);
+    case 3: return emf_rec<3>(g, FS, Bin, Ed, st);
+    case 4: return emf_rec<4>(g, FS, Bin, Ed, st);
+    case 5: return emf_rec<5>(g, FS, Bin, Ed, st);
+    default: return emf_rec<0>(g, FS, Bin, Ed, st);
+  }
+}
+
+cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const double* dtp, const double* Ed,
+                              double* Bst, double* Lout, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
+  if (g.der == 4) k_uct_induct<4><<<blocks, kCellThreads, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
+  else if (g.der == 2) k_uct_induct<2><<<blocks, kCellThreads, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
+  else k_uct_induct<6><<<blocks, kCellThreads, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uct_cell(const GridP& g, const EosP& e, int s, double dt, const double* dtp, const double* R,
+                            const double* Un, const double* Us, double* Uout, double* P, const double* Bst,
+                            unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
+  k_uct_cell<<<blocks, kCellThreads, 0, st>>>(g, e, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uct_centre_p2c(const GridP& g, const EosP& e, const double* P, double* U, const double* Bst,
+                                  cudaStream_t st) {
+  const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
+  k_uct_centre_p2c<<<blocks, kCellThreads, 0, st>>>(g, e, P, U, Bst);
+  return cudaGetLastError();
+}
+
+}  // namespace echo

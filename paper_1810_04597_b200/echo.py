@@ -59,6 +59,8 @@ _sig = {
     "echo_set_prims": (C.c_int, [_P, _P, C.c_int]),
     "echo_get_prims": (C.c_int, [_P, _P, C.c_int]),
     "echo_set_cons": (C.c_int, [_P, _P, C.c_int]),
+    "echo_set_face_field": (C.c_int, [_P, _P, C.c_int]),
+    "echo_get_face_field": (C.c_int, [_P, _P, C.c_int]),
     "echo_get_cons": (C.c_int, [_P, _P, C.c_int]),
     "echo_get_state": (C.c_int, [_P, _P, _P, _P, C.c_int]),
     "echo_rhs": (C.c_int, [_P, _P, C.c_int]),
@@ -165,6 +167,17 @@ def get_prims(ctx, out8):
 def set_cons(ctx, u8):
     p, d = _buf(u8)
     return _check(ctx, _lib.echo_set_cons(ctx, p, d))
+
+
+def set_face_field(ctx, b3):
+    """divb = 2 (UCT): the staggered field sqrt(gamma) B^a at the faces i_a + 1/2, [3][n3][n2][n1]"""
+    p, d = _buf(b3)
+    return _check(ctx, _lib.echo_set_face_field(ctx, p, d))
+
+
+def get_face_field(ctx, out3):
+    p, d = _buf(out3, True)
+    return _check(ctx, _lib.echo_get_face_field(ctx, p, d))
 
 
 def get_cons(ctx, out8):
@@ -340,6 +353,14 @@ class Echo:
     def get_prims(self, out=None):
         out = np.zeros(self.shape(8)) if out is None else out
         get_prims(self.ctx, out)
+        return out
+
+    def set_face_field(self, b3):
+        return set_face_field(self.ctx, b3)
+
+    def get_face_field(self, out=None):
+        out = np.zeros(self.shape(3)) if out is None else out
+        get_face_field(self.ctx, out)
         return out
 
     def get_cons(self, out=None):
