@@ -171,15 +171,28 @@ def run_reference(args, world, rank):
     oracle.build()
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     p = I.problem(args.config, n=(n, n, n))
+    p.rec, p.divb = args.rec, args.divb
     oc = oracle.Cfg(**p.grid_kwargs(), nthreads=cores)
-    U, P = oracle.set_prims(oc, I.initial_prims(p))
-    for _ in range(W):
+    if p.divb == 2:
+        U, P, b = oracle.set_prims_uct(oc, I.initial_prims(p), I.face_field(p))
+    else:
+        U, P = oracle.set_prims(oc, I.initial_prims(p))
+
+    def one_step(U, P):
+        nonlocal b
         dt = oracle.max_dt(oc, U, P, p.cfl)
-        U, P, _ = oracle.step(oc, dt, U, P)
+        if p.divb == 2:
+            U, P, b, _ = oracle.step_uct(oc, dt, U, P, b)
+        else:
+            U, P, _ = oracle.step(oc, dt, U, P)
+        return U, P
+
+    b = None if p.divb != 2 else b
+    for _ in range(W):
+        U, P = one_step(U, P)
     t0 = time.perf_counter()
     for _ in range(K):
-        dt = oracle.max_dt(oc, U, P, p.cfl)
-        U, P, _ = oracle.step(oc, dt, U, P)
+        U, P = one_step(U, P)
     t = time.perf_counter() - t0
     zu = p.ncells * K / t
     sample = (f"each step = CFL + one SSP-RK3 step of the config-{args.config} recipe on a {n}^3 periodic grid "
@@ -193,10 +206,13 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+DIVB_NAMES = {0: "field-CD", 1: "no-divB-control", 2: "UCT (staggered B, edge EMFs)"}
+
+
 def workload_config(args, p, world):
     """The `config` object of both arms (the reference arm times a bounded sample of it)."""
     return {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
-                        f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[args.rec]}+HLL+DER6+field-CD, SSP-RK3",
+                        f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[args.rec]}+HLL+DER6+{DIVB_NAMES[args.divb]}, SSP-RK3",
             "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
             "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
             "step": "CFL reduction -> dt, then one SSP-RK3 step (3 stages x [3 sweeps + update])"}
@@ -224,6 +240,7 @@ def run_decomp(args, world, rank, local):
     K, W = args.steps, args.warmup
     p = I.problem(args.config, n=args.n)
     p.rec = args.rec
+    p.divb = args.divb
     N = p.ncells
     stream = torch.cuda.current_stream(dev)
     P8 = I.initial_prims(p, device=dev)
@@ -310,12 +327,17 @@ def run_ours(args, world, rank, local):
     K, W = args.steps, args.warmup
     p = I.problem(args.config, n=args.n)
     p.rec = args.rec
+    p.divb = args.divb
     N = p.ncells
     stream = torch.cuda.current_stream(dev)
     g = echo.Echo(p)
     echo.set_stream(g.ctx, stream.cuda_stream)
     P8 = I.initial_prims(p, device=dev)
     g.set_prims(P8)
+    B3 = None
+    if p.divb == 2:  # UCT: the staggered field (echo_set_face_field)
+        B3 = I.face_field(p, device=dev)
+        g.set_face_field(B3)
     for _ in range(W):
         g.step(g.max_dt(p.cfl))
     torch.cuda.synchronize()
@@ -382,7 +404,11 @@ def run_ours(args, world, rank, local):
     host_in = torch.empty(P8.shape, dtype=torch.float64, pin_memory=True)
     host_in.copy_(P8 if torch.is_tensor(P8) else torch.from_numpy(P8))
     host_out = torch.empty(P8.shape, dtype=torch.float64, pin_memory=True)
-    del P8
+    host_b = None
+    if B3 is not None:
+        host_b = torch.empty(B3.shape, dtype=torch.float64, pin_memory=True)
+        host_b.copy_(B3 if torch.is_tensor(B3) else torch.from_numpy(B3))
+    del P8, B3
     torch.cuda.empty_cache()
     hin = host_in.numpy()
     hout = host_out.numpy()
@@ -392,6 +418,8 @@ def run_ours(args, world, rank, local):
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     echo.set_prims(g.ctx, hin)          # H2D of the inputs (pinned) + prim2cons
+    if host_b is not None:
+        echo.set_face_field(g.ctx, host_b.numpy())  # UCT: H2D of the staggered field
     if args.loop == "device":
         g.advance(K, p.cfl)             # the K dt values come back at the end (8 B each)
     else:
@@ -402,7 +430,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     te2e = reduce_max(f0.elapsed_time(f1) / 1e3, world, dev)
     e2e = {"value": world * N * K / te2e, "unit": UNIT,
-           "h2d_bytes_per_step": int(8 * N * 8 / K) + 0, "d2h_bytes_per_step": int(8 * N * 8 / K) + 8,
+           "h2d_bytes_per_step": int((8 + (3 if host_b is not None else 0)) * N * 8 / K) + 0, "d2h_bytes_per_step": int(8 * N * 8 / K) + 8,
            "what": "echo_set_prims(pinned host) + " + ("echo_advance(K)" if args.loop == "device" else
                                                         "K x (echo_max_dt + echo_step)") + " + echo_get_prims(pinned host)"}
 
@@ -450,6 +478,8 @@ def main(argv=None):
                     help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5, 3 WENO-Z, 4 MC2, 5 PPM")
     ap.add_argument("--loop", choices=["device", "host"], default="device",
                     help="device: echo_advance (dt on the device, CUDA-graph step); host: echo_max_dt + echo_step per step")
+    ap.add_argument("--divb", type=int, default=0, choices=[0, 1, 2],
+                    help="divergence treatment: 0 field-CD (default, the benchmarked scheme), 1 none, 2 UCT")
     ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")
     ap.add_argument("--ref-n", type=int, default=64)
     ap.add_argument("--cpu-n", type=int, default=64)

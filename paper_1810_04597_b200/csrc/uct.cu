@@ -38,6 +38,69 @@ ECHO_D void rec_pair(const double f[6], double& lo, double& hi) {
   rec_both<REC>(f[1], f[2], f[3], f[4], f[5], dead1, hi);
 }
 
+// E^CC at the edge owned by cell x (one component per thread: the three are independent,
+// and a thread holding all three needs ~170 registers, one CTA per SM)
+template <int REC, int CC>
+ECHO_D double uct_emf_one(const GridP& g, const double* const FS[3], const double* __restrict__ Bin, const int x[3],
+                          long long rb) {
+  constexpr int p = (CC + 1) % 3, q = (CC + 2) % 3;
+  const int comp[2] = {p, q};
+  const long long vs = g.vs;
+  double f[6];
+  long long oq[6], op[6];
+#pragma unroll
+  for (int m = 0; m < 6; m++) {
+    oq[m] = rec_shift(g, x, q, m - 2);
+    op[m] = rec_shift(g, x, p, m - 2);
+  }
+  // p-face states (W: slots 0..2, E: 3..5) along q -> S, N; q-face states (S, N) along p -> W, E
+  double pS[2][2], pN[2][2], qW[2][2], qE[2][2];
+#pragma unroll
+  for (int side = 0; side < 2; side++)
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+#pragma unroll
+      for (int m = 0; m < 6; m++) f[m] = __ldg(FS[p] + oq[m] + (3 * side + comp[k]) * vs);
+      rec_pair<REC>(f, pS[side][k], pN[side][k]);
+#pragma unroll
+      for (int m = 0; m < 6; m++) f[m] = __ldg(FS[q] + op[m] + (3 * side + comp[k]) * vs);
+      rec_pair<REC>(f, qW[side][k], qE[side][k]);
+    }
+  double bpS, bpN, bqW, bqE;
+#pragma unroll
+  for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + oq[m] + p * vs);
+  rec_pair<REC>(f, bpS, bpN);
+#pragma unroll
+  for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + op[m] + q * vs);
+  rec_pair<REC>(f, bqW, bqE);
+  // A40: max over the two faces meeting at the edge (oq[3] = +1 along q, op[3] = +1 along p)
+  const double app = fmax(__ldg(FS[p] + rb + 6 * vs), __ldg(FS[p] + oq[3] + 6 * vs));
+  const double apm = fmax(__ldg(FS[p] + rb + 7 * vs), __ldg(FS[p] + oq[3] + 7 * vs));
+  const double aqp = fmax(__ldg(FS[q] + rb + 6 * vs), __ldg(FS[q] + op[3] + 6 * vs));
+  const double aqm = fmax(__ldg(FS[q] + rb + 7 * vs), __ldg(FS[q] + op[3] + 7 * vs));
+  // A38 quadrant velocities (v^p, v^q), A39 quadrant EMFs E = v^q B^p - v^p B^q
+  double v[4][2];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    v[0][k] = 0.5 * (pS[0][k] + qW[0][k]);  // WS
+    v[1][k] = 0.5 * (pN[0][k] + qW[1][k]);  // WN
+    v[2][k] = 0.5 * (pS[1][k] + qE[0][k]);  // ES
+    v[3][k] = 0.5 * (pN[1][k] + qE[1][k]);  // EN
+  }
+  const double EWS = v[0][1] * bpS - v[0][0] * bqW;
+  const double EWN = v[1][1] * bpN - v[1][0] * bqW;
+  const double EES = v[2][1] * bpS - v[2][0] * bqE;
+  const double EEN = v[3][1] * bpN - v[3][0] * bqE;
+  const double sp = app + apm, sq = aqp + aqm;
+  if (sp > 0.0 && sq > 0.0) {
+    const double isp = 1.0 / sp, isq = 1.0 / sq;
+    return (app * (aqp * EWS + aqm * EWN) + apm * (aqp * EES + aqm * EEN)) * (isp * isq) +
+           app * apm * (bqE - bqW) * isp - aqp * aqm * (bpN - bpS) * isq;
+  }
+  return 0.25 * (EWS + EWN + EES + EEN);  // unreachable for p > 0 (A4): central average
+}
+
+// grid (cells / kCellThreads, 3): blockIdx.y = the EMF component
 template <int REC>
 __global__ void __launch_bounds__(kCellThreads)
 k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restrict__ FSy,
@@ -47,68 +110,13 @@ k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restric
   int x[3];
   cell_ijk(g, id, x[0], x[1], x[2]);
   const double* FS[3] = {FSx, FSy, FSz};
-  const long long vs = g.vs;
   const long long rb = rec_base(g, x[0], x[1], x[2]);
-#pragma unroll
-  for (int cc = 0; cc < 3; cc++) {
-    const int p = (cc + 1) % 3, q = (cc + 2) % 3;
-    const int comp[2] = {p, q};
-    double f[6];
-    long long oq[6], op[6];
-#pragma unroll
-    for (int m = 0; m < 6; m++) {
-      oq[m] = rec_shift(g, x, q, m - 2);
-      op[m] = rec_shift(g, x, p, m - 2);
-    }
-    // p-face states (W: slots 0..2, E: 3..5) along q -> S, N; q-face states (S, N) along p -> W, E
-    double pS[2][2], pN[2][2], qW[2][2], qE[2][2];
-#pragma unroll
-    for (int side = 0; side < 2; side++)
-#pragma unroll
-      for (int k = 0; k < 2; k++) {
-#pragma unroll
-        for (int m = 0; m < 6; m++) f[m] = __ldg(FS[p] + oq[m] + (3 * side + comp[k]) * vs);
-        rec_pair<REC>(f, pS[side][k], pN[side][k]);
-#pragma unroll
-        for (int m = 0; m < 6; m++) f[m] = __ldg(FS[q] + op[m] + (3 * side + comp[k]) * vs);
-        rec_pair<REC>(f, qW[side][k], qE[side][k]);
-      }
-    double bpS, bpN, bqW, bqE;
-#pragma unroll
-    for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + oq[m] + p * vs);
-    rec_pair<REC>(f, bpS, bpN);
-#pragma unroll
-    for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + op[m] + q * vs);
-    rec_pair<REC>(f, bqW, bqE);
-    // A40: max over the two faces meeting at the edge (oq[3] = +1 along q, op[3] = +1 along p)
-    const double app = fmax(__ldg(FS[p] + rb + 6 * vs), __ldg(FS[p] + oq[3] + 6 * vs));
-    const double apm = fmax(__ldg(FS[p] + rb + 7 * vs), __ldg(FS[p] + oq[3] + 7 * vs));
-    const double aqp = fmax(__ldg(FS[q] + rb + 6 * vs), __ldg(FS[q] + op[3] + 6 * vs));
-    const double aqm = fmax(__ldg(FS[q] + rb + 7 * vs), __ldg(FS[q] + op[3] + 7 * vs));
-    // A38 quadrant velocities (v^p, v^q), A39 quadrant EMFs E = v^q B^p - v^p B^q
-    double v[4][2];
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-      v[0][k] = 0.5 * (pS[0][k] + qW[0][k]);  // WS
-      v[1][k] = 0.5 * (pN[0][k] + qW[1][k]);  // WN
-      v[2][k] = 0.5 * (pS[1][k] + qE[0][k]);  // ES
-      v[3][k] = 0.5 * (pN[1][k] + qE[1][k]);  // EN
-    }
-    const double EWS = v[0][1] * bpS - v[0][0] * bqW;
-    const double EWN = v[1][1] * bpN - v[1][0] * bqW;
-    const double EES = v[2][1] * bpS - v[2][0] * bqE;
-    const double EEN = v[3][1] * bpN - v[3][0] * bqE;
-    const double sp = app + apm, sq = aqp + aqm;
-    double E;
-    if (sp > 0.0 && sq > 0.0) {
-      const double isp = 1.0 / sp, isq = 1.0 / sq;
-      E = (app * (aqp * EWS + aqm * EWN) + apm * (aqp * EES + aqm * EEN)) * (isp * isq) +
-          app * apm * (bqE - bqW) * isp - aqp * aqm * (bpN - bpS) * isq;
-    } else {  // unreachable for p > 0 (A4): central average
-      E = 0.25 * (EWS + EWN + EES + EEN);
-    }
-    Ed[rb + cc * vs] = E;
-  }
+  const int cc = blockIdx.y;
+  double E;
+  if (cc == 0) E = uct_emf_one<REC, 0>(g, FS, Bin, x, rb);
+  else if (cc == 1) E = uct_emf_one<REC, 1>(g, FS, Bin, x, rb);
+  else E = uct_emf_one<REC, 2>(g, FS, Bin, x, rb);
+  Ed[rb + cc * g.vs] = E;
 }
 
 // A41 induction of the three faces owned by a cell; MODE 0: RK stage s into Bst (dt from
@@ -253,7 +261,7 @@ k_uct_centre_p2c(const GridP g, const EosP e, const double* __restrict__ P, doub
 
 template <int REC>
 cudaError_t emf_rec(const GridP& g, const double* const FS[3], const double* Bin, double* Ed, cudaStream_t st) {
-  const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
+  const dim3 blocks((unsigned)((g.N + kCellThreads - 1) / kCellThreads), 3);
   k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
   return cudaGetLastError();
 }
