@@ -14,3 +14,14 @@ echo "launches rc=$?" >> gpurun_out/ncu_launches.log
 ncu --set full --clock-control none --import-source on -k regex:"k_march|k_update" -c 4 \
   -o gpurun_out/prof_round $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/ncu_full.log
+# UCT (divb = 2): the edge-EMF kernel, first launch at 512^3
+ncu --set full --clock-control none --import-source on -k regex:"k_uct_emf|k_uct_cell" -c 2 \
+  -o gpurun_out/prof_uct python bench.py --divb 2 --steps 1 --warmup 1 --no-cpu > gpurun_out/ncu_uct.log 2>&1
+echo "uct rc=$?" >> gpurun_out/ncu_uct.log
+# gpurun copies back <= 64 MiB: keep the raw-page CSV exports, drop the reports
+for r in prof_round prof_uct; do
+  if [ -f gpurun_out/$r.ncu-rep ]; then
+    ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/$r.raw.csv 2>/dev/null
+    rm -f gpurun_out/$r.ncu-rep
+  fi
+done

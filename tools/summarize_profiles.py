@@ -21,8 +21,23 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
+        "smsp__inst_executed.sum",
+        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+        "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__thread_inst_executed_per_inst_executed.ratio", "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
+
+
 def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # exported on the GPU box (ncu -i rep --page raw --csv)
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     return rows[0], rows[1], rows[2:]
 
@@ -55,19 +70,12 @@ def main(tag):
                 f.write(f"{k:60s} {len(v):8d} {statistics.mean(v) / 1e6:10.3f} {sum(v) / tot:7.3f}\n")
     # full capture
     rep = os.path.join(OUT, "prof_round.ncu-rep")
+    if not os.path.exists(rep):
+        rep = os.path.join(OUT, "prof_round.raw.csv")
     if os.path.exists(rep):
         hdr, units, data = raw(rep)
         ix = {h: i for i, h in enumerate(hdr)}
-        keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-                "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
-                "sm__warps_active.avg.pct_of_peak_sustained_active",
-                "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-                "smsp__issue_active.avg.pct_of_peak_sustained_active",
-                "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
-                "smsp__inst_executed.sum",
-                "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
-                "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-                "smsp__thread_inst_executed_per_inst_executed.ratio"]
+        keys = KEYS
         sweeps = []
         with open(os.path.join(PROF, f"{tag}_kernels.txt"), "w") as f:
             f.write("ncu --set full --clock-control none, 512^3 config 3 (bench workload), first stage\n")
@@ -95,6 +103,18 @@ def main(tag):
             with open(os.path.join(PROF, "sweep_traffic.json"), "w") as f:
                 json.dump({"bytes_per_launch": statistics.mean(sweeps), "per_axis": sweeps,
                            "source": f"profiles/{tag}_kernels.txt (ncu --set full, dram__bytes_read+write)"}, f, indent=1)
+    # UCT kernels (divb = 2)
+    urep = os.path.join(OUT, "prof_uct.raw.csv")
+    if os.path.exists(urep):
+        hdr, units, data = raw(urep)
+        ix = {h: i for i, h in enumerate(hdr)}
+        with open(os.path.join(PROF, f"{tag}_kernels_uct.txt"), "w") as f:
+            f.write("ncu --set full --clock-control none, 512^3 config 3 with divb = 2 (UCT), first stage\n")
+            for d in data:
+                f.write(f"== {d[ix['Kernel Name']]}\n")
+                for k in KEYS:
+                    if k in ix:
+                        f.write(f"   {k:62s} {d[ix[k]]:>16s} {units[ix[k]]}\n")
     for fn in ("bench_default.json", "bench_small.json", "gpu.txt"):
         p = os.path.join(OUT, fn)
         if os.path.exists(p):
