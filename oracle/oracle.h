@@ -10,7 +10,8 @@
  * What it computes: one SSP-RK3 step of the 3+1 ideal-GRMHD finite-difference
  * scheme named by BASELINE.json:north_star — ghost fill, WENO5 reconstruction
  * of primitives, fast-speed bound + HLL flux, DER flux derivative, metric
- * sources, field-CD divergence-preserving B update, RK stage combine, per-cell
+ * sources, field-CD divergence-preserving B update (or, divb = 2, the staggered
+ * field with upwind constrained transport, A37-A41), RK stage combine, per-cell
  * Newton con2prim with floors, CFL reduction.  The paper (PAPER.md:19,
  * "solve the equations of magneto-hydrodynamic in General Relativity, using
  * 3D finite-differences method and high-order reconstruction algorithms")
