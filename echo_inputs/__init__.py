@@ -408,7 +408,8 @@ def face_field(p: Problem, device=None, direction=None):
     [3][n3][n2][n1], the ANALYTIC field of the config's initial condition sampled at the
     faces (turbulence: B0 x-hat + the exact curl of the same seeded vector potential,
     whose cell-centred counterpart ic_turbulence takes as a D2 curl; CP Alfven: the
-    exact wave, along `direction` = integer (k1, k2, k3) if given, else (1, 1, 1))."""
+    exact wave, along `direction` = integer (k1, k2, k3) if given, else (1, 1, 1); blast: the
+    uniform B = Bx x-hat)."""
     torch = _backend(device)
     cfg = p.params["cfg"]
     out = []
@@ -424,8 +425,11 @@ def face_field(p: Problem, device=None, direction=None):
         for a in range(3):
             X, Y, Z = _coords_face(p, a, None, None)
             out.append(cp_alfven_fields(p, X, Y, Z, 0.0, direction)[1][a])
+    elif cfg == 2:
+        for a in range(3):
+            out.append(np.full((1, 1, 1), p.params["Bx"] if a == 0 else 0.0))
     else:
-        raise ValueError("face_field: UCT inputs exist for the periodic Minkowski configs 0, 1, 3")
+        raise ValueError("face_field: UCT inputs exist for the Minkowski configs 0-3")
     shape = (p.n[2], p.n[1], p.n[0])
     if torch is None:
         return np.ascontiguousarray(np.stack([np.broadcast_to(f, shape) for f in out]).astype(np.float64))

@@ -136,8 +136,8 @@ int echo_set_prims(echo_ctx* ctx, const double* p8, int on_device);
 /* Current user prims P8 (B = U_B / sqrt(gamma), v = u~ / W). */
 int echo_get_prims(echo_ctx* ctx, double* p8, int on_device);
 
-/* UCT (grid.divb = 2; readings A37-A41; Minkowski, periodic axes only,
- * refused at echo_create otherwise): the magnetic state is the staggered field
+/* UCT (grid.divb = 2; readings A37-A41; Minkowski, periodic or outflow
+ * axes (A42), refused at echo_create otherwise): the magnetic state is the staggered field
  * b3[a][n3][n2][n1] = sqrt(gamma) B^a at the centre of the face i_a + 1/2 of cell
  * (i1, i2, i3) (point values).  After echo_set_prims (which supplies the hydro
  * primitives; its B is replaced), echo_set_face_field sets b, the cell-centred field

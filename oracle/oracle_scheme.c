@@ -855,8 +855,8 @@ int orc_get_prims(const orc_cfg* c, const double* U8, const double* P5, double* 
 
 /* ------------------------------------------------------------------ */
 /* UCT: staggered field + upwind constrained transport (divb = 2;      */
-/* SURVEY.md §8(f) f2; readings A37-A41).  Minkowski,        */
-/* periodic axes.  b3[a][N]: sqrt(gamma) B^a at the face i_a + 1/2     */
+/* SURVEY.md §8(f) f2; readings A37-A42).  Minkowski,        */
+/* periodic or outflow axes.  b3[a][N]: sqrt(gamma) B^a at the face i_a + 1/2     */
 /* owned by cell i (x1 fastest); E3[c][N]: EMF E^c at the edge         */
 /* (i_p + 1/2, i_q + 1/2, i_c) owned by cell i, (c, p, q) cyclic.      */
 /* ------------------------------------------------------------------ */
@@ -966,12 +966,10 @@ static void uct_emf_induction(const orc_cfg* c, const double* FS, const double* 
   free(E3);
 }
 
-static int uct_ok(const orc_cfg* c) {
-  if (c->divb != 2 || c->metric != ORC_MINKOWSKI) return 0;
-  for (int a = 0; a < 3; a++)
-    if (c->bc[a][0] != ORC_BC_PERIODIC) return 0;
-  return 1;
-}
+/* UCT scope (A37): Minkowski; periodic or outflow axes.  On an outflow side every
+ * staggered quantity (b, the face data, the EMFs) takes the ghost rule of A13 through
+ * lin_shift: the nearest owned face / edge (zero gradient). */
+static int uct_ok(const orc_cfg* c) { return c->divb == 2 && c->metric == ORC_MINKOWSKI; }
 
 /* A37: cell-centred field from the staggered one, 6-point midpoint interpolation
  * B^a(i) = (3 b_{i-5/2} - 25 b_{i-3/2} + 150 b_{i-1/2} + 150 b_{i+1/2} - 25 b_{i+3/2} + 3 b_{i+5/2}) / 256 */

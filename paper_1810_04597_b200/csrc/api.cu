@@ -255,11 +255,11 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   if (grid->rec < 0 || grid->rec > 5) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..5");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
   if (grid->divb < 0 || grid->divb > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0, 1 or 2");
-  if (grid->divb == 2) {  // UCT (A37): Minkowski, periodic axes
-    bool per = true;
-    for (int a = 0; a < 3; a++) per = per && grid->bc[a][0] == ECHO_BC_PERIODIC && grid->bc[a][1] == ECHO_BC_PERIODIC;
-    if (!per || metric->kind != ECHO_METRIC_MINKOWSKI)
-      return fail(nullptr, ECHO_E_ARG, "echo_create: divb = 2 (UCT) needs a Minkowski metric and periodic axes");
+  if (grid->divb == 2) {  // UCT (A37, A42): Minkowski, periodic or outflow axes (no slabs)
+    bool ok = metric->kind == ECHO_METRIC_MINKOWSKI;
+    for (int a = 0; a < 3; a++) ok = ok && grid->bc[a][0] != ECHO_BC_HALO && grid->bc[a][1] != ECHO_BC_HALO;
+    if (!ok)
+      return fail(nullptr, ECHO_E_ARG, "echo_create: divb = 2 (UCT) needs a Minkowski metric and periodic or outflow axes");
   }
   if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");
   if (!(eos->rho_floor > 0.0) || !(eos->p_floor > 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: floors > 0 violated");

@@ -430,7 +430,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
             hll_face(load_met(rec), e, pl, qR, AX, F);
           } else if constexpr (UCT) {
             // A37: both states take the staggered normal field of face xf + 1/2 (owned by cell xf)
-            const long long fo = lb + (long long)map_index(xf, lg.na, 0, 0) * as;
+            const long long fo = lb + (long long)map_index(xf, lg.na, g.bc[AX][0], g.bc[AX][1]) * as;
             const double bnv = Bface[fo + AX * vs];
             pl[5 + AX] = bnv;
             qR[5 + AX] = bnv;

@@ -1,5 +1,6 @@
 // uct.cu — the staggered-field update of divb = 2 (UCT; DESIGN.md
-// readings A37-A41): Minkowski, periodic axes.
+// readings A37-A42): Minkowski, periodic or outflow axes (A42: on an outflow side the staggered
+// quantities take the nearest owned face / edge, as the cell ghosts do, A13).
 //
 // State: Bst record array, slots 0..2 = b^n, 3..5 = b^s, where b^a = sqrt(gamma) B^a at
 // the face i_a + 1/2 owned by cell i.  The sweeps (march.cu, DM = 2) take the normal
@@ -13,7 +14,7 @@
 //                 form of stage s per face (or L(b) alone for echo_rhs)     -> Bst
 //   k_uct_cell    hydro RK combine from the sweeps' rhs, U_B = I6(b) of the new field (A37),
 //                 con2prim + floors, the CFL rate of the new state           -> U, P
-// One thread per cell; neighbours through the periodic index map (L1/L2).
+// One thread per cell; neighbours through the ghost index map (L1/L2).
 #include <cuda_runtime.h>
 
 #include "cell_physics.cuh"
@@ -25,7 +26,7 @@ namespace {
 
 ECHO_D long long rec_shift(const GridP& g, const int x[3], int a, int d) {
   int y[3] = {x[0], x[1], x[2]};
-  y[a] = map_index(y[a] + d, g.n[a], 0, 0);
+  y[a] = map_index(y[a] + d, g.n[a], g.bc[a][0], g.bc[a][1]);  // A13 / A42: wrap or nearest owned
   return rec_base(g, y[0], y[1], y[2]);
 }
 
