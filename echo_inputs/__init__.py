@@ -312,6 +312,11 @@ def torus_hydro(p: Problem, r, th):
 
 def ic_torus(p: Problem, device=None):
     """config 4: constant-ell thick torus on Kerr-Schild (SURVEY §8(d) cfg 4, reading A15)."""
+    return _torus(p)[0]
+
+
+def _torus(p: Problem):
+    """(prims8, rho_max, field scale) of config 4"""
     prm = p.params
     n1, n2, n3 = p.n
     d1 = (p.hi[0] - p.lo[0]) / n1
@@ -343,6 +348,7 @@ def ic_torus(p: Problem, device=None):
     vB = g11 * v1 * B1 + g13 * v3 * B1
     b2 = Bsq / W2 + vB * vB
     bmax = float(np.max(np.where(inside, b2, 0.0)))
+    scale = 1.0
     if bmax > 0:
         pmax = float(np.max(np.where(inside, prs, 0.0)))
         scale = math.sqrt(pmax / (prm["beta"] * 0.5 * bmax))
@@ -359,7 +365,25 @@ def ic_torus(p: Problem, device=None):
     zero = np.zeros(shape)
     out = [np.broadcast_to(rho, shape), np.broadcast_to(v1, shape), zero, np.broadcast_to(v3, shape), prs3,
            np.broadcast_to(B1, shape), np.broadcast_to(B2, shape), zero]
-    return np.ascontiguousarray(np.stack(out).astype(np.float64))
+    return np.ascontiguousarray(np.stack(out).astype(np.float64)), rho_max, scale
+
+
+def _torus_face_field(p: Problem):
+    """config 4 staggered field: A_phi = max(rho - 0.2 rho_max, 0) at the cell corners
+    (x1 face, x2 face), its staggered curl sqrt(g) B^1 = d_theta A_phi at the x1 faces and
+    sqrt(g) B^2 = -d_x1 A_phi at the x2 faces, with the cell-centred IC's beta scale"""
+    _, rho_max, scale = _torus(p)
+    n1, n2, n3 = p.n
+    d1 = (p.hi[0] - p.lo[0]) / n1
+    d2 = (p.hi[1] - p.lo[1]) / n2
+    x1c = p.lo[0] + np.arange(n1 + 1) * d1   # faces -1/2 .. n1 - 1/2
+    x2c = p.lo[1] + np.arange(n2 + 1) * d2
+    rho_c = torus_hydro(p, np.exp(x1c)[None, :], x2c[:, None])[0]
+    A = np.maximum(rho_c - 0.2 * rho_max, 0.0) * scale      # [n2 + 1][n1 + 1]
+    b1 = (A[1:, 1:] - A[:-1, 1:]) / d2                      # face i + 1/2 = corner column i + 1
+    b2 = -(A[1:, 1:] - A[1:, :-1]) / d1                     # face j + 1/2 = corner row j + 1
+    shape = (n3, n2, n1)
+    return [np.broadcast_to(b1, shape), np.broadcast_to(b2, shape), np.zeros(shape)]
 
 
 def initial_prims(p: Problem, device=None, **kw):
@@ -409,7 +433,7 @@ def face_field(p: Problem, device=None, direction=None):
     faces (turbulence: B0 x-hat + the exact curl of the same seeded vector potential,
     whose cell-centred counterpart ic_turbulence takes as a D2 curl; CP Alfven: the
     exact wave, along `direction` = integer (k1, k2, k3) if given, else (1, 1, 1); blast: the
-    uniform B = Bx x-hat)."""
+    uniform B = Bx x-hat; torus: the staggered curl of A_phi at the cell corners)."""
     torch = _backend(device)
     cfg = p.params["cfg"]
     out = []
@@ -428,12 +452,15 @@ def face_field(p: Problem, device=None, direction=None):
     elif cfg == 2:
         for a in range(3):
             out.append(np.full((1, 1, 1), p.params["Bx"] if a == 0 else 0.0))
+    elif cfg == 4:
+        out = _torus_face_field(p)
     else:
-        raise ValueError("face_field: UCT inputs exist for the Minkowski configs 0-3")
+        raise ValueError(f"face_field: no staggered-field recipe for config {cfg}")
     shape = (p.n[2], p.n[1], p.n[0])
     if torch is None:
         return np.ascontiguousarray(np.stack([np.broadcast_to(f, shape) for f in out]).astype(np.float64))
-    return torch.stack([torch.as_tensor(f, dtype=torch.float64, device=device).expand(shape) for f in out]).contiguous()
+    return torch.stack([torch.as_tensor(np.ascontiguousarray(f) if isinstance(f, np.ndarray) else f,
+                                        dtype=torch.float64, device=device).expand(shape) for f in out]).contiguous()
 
 
 def cp_alfven_fields(p: Problem, X, Y, Z, t, direction=None):

@@ -136,12 +136,12 @@ int echo_set_prims(echo_ctx* ctx, const double* p8, int on_device);
 /* Current user prims P8 (B = U_B / sqrt(gamma), v = u~ / W). */
 int echo_get_prims(echo_ctx* ctx, double* p8, int on_device);
 
-/* UCT (grid.divb = 2; readings A37-A41; Minkowski, periodic or outflow
- * axes (A42), refused at echo_create otherwise): the magnetic state is the staggered field
+/* UCT (grid.divb = 2; readings A37-A43; periodic or outflow axes (A42), any
+ * metric (A43); slab boundaries are refused at echo_create): the magnetic state is the staggered field
  * b3[a][n3][n2][n1] = sqrt(gamma) B^a at the centre of the face i_a + 1/2 of cell
  * (i1, i2, i3) (point values).  After echo_set_prims (which supplies the hydro
  * primitives; its B is replaced), echo_set_face_field sets b, the cell-centred field
- * U_B = I6(b) (6-point midpoint interpolation along a) and U.  Every step then
+ * U_B = I6(b) (6-point midpoint interpolation along a; B = U_B / sqrt(gamma)) and U.  Every step then
  * updates b by the UCT-HLL edge EMFs with the DER operator along the
  * differentiation direction, which keeps sum_a delta_a Dh_a b^a at roundoff.
  * Stepping a divb = 2 context before echo_set_face_field is ECHO_E_ORDER, as is

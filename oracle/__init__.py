@@ -157,6 +157,7 @@ def lib():
             "orc_con2prim": (C.c_int, [P, _D, _D, C.POINTER(_Counts)]),
             "orc_divb": (C.c_double, [P, _D]),
             "orc_uct_centre": (C.c_int, [P, _D, _D]),
+            "orc_set_prims_uct": (C.c_int, [P, _D, _D, _D, _D, _LL]),
             "orc_uct_divh": (C.c_int, [P, _D, _D]),
             "orc_rhs_uct": (C.c_int, [P, _D, _D, _D, _D]),
             "orc_stage_uct": (C.c_int, [P, C.c_int, C.c_double, _D, _D, _D, _D, _D, _D, _D, _D,
@@ -374,11 +375,16 @@ def uct_divh(cfg: Cfg, b3) -> np.ndarray:
 
 def set_prims_uct(cfg: Cfg, P8, b3):
     """state of a UCT run: the hydro primitives of P8 and the staggered field b3 (the
-    cell-centred B of the state is I6(b3); P8's B slots are ignored)."""
-    P = _v(P8).copy()
-    P[5:8] = uct_centre(cfg, b3)
-    U, P5 = set_prims(cfg, P)
-    return U, P5, _v(b3).copy()
+    cell-centred sqrt(gamma) B of the state is I6(b3); P8's B slots are ignored)."""
+    P8 = _v(P8)
+    b = _v(b3).copy()
+    U8 = np.zeros(cfg.shape(8))
+    P5 = np.zeros(cfg.shape(5))
+    bad = C.c_longlong(-1)
+    rc = lib().orc_set_prims_uct(C.byref(cfg.c()), _p(P8), _p(b), _p(U8), _p(P5), C.byref(bad))
+    if rc:
+        raise OracleError(f"orc_set_prims_uct rc={rc} (cell {bad.value})")
+    return U8, P5, b
 
 
 def rhs_uct(cfg: Cfg, U8, P5, b3) -> np.ndarray:

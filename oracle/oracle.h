@@ -61,8 +61,8 @@ typedef struct {
   int der;           /* 6 DER6, 4 DER4, 2 plain difference (A5) */
   int divb;          /* 0 field-CD (A6), 1 none: plain flux difference for B,
                         2 UCT: staggered field + upwind constrained transport (A37-A41;
-                        Minkowski, periodic or outflow axes (A42); the *_uct
-                        entry points) */
+                        periodic or outflow axes (A42), any metric (A43);
+                        the *_uct entry points) */
   double der_jump;   /* A31 DER switch: the DER correction at a face is dropped (H = F) when a face
                         of its 5-face stencil joins cells whose rho or p differ by more than
                         der_jump x the smaller value; <= 0 disables the switch */
@@ -137,7 +137,9 @@ double orc_divb(const orc_cfg* c, const double* U8);
 /* ---------------- UCT (divb = 2; A37-A41) -------------------
  * b3 [3][n3][n2][n1]: sqrt(gamma) B^a at the face i_a + 1/2 of cell (i1,i2,i3).
  * The state's U8 slots 5..7 hold the cell-centred field I6(b3) (A37).
- * Return -1 unless divb = 2 and Minkowski. */
+ * Return -1 unless divb = 2. */
+/* UCT state: hydro prims from P8 (its B ignored), U_B = I6(b3), B = U_B / sqrt(gamma) */
+int orc_set_prims_uct(const orc_cfg* c, const double* P8, const double* b3, double* U8, double* P5, long long* bad);
 /* A37 centring: Bc3[a] = 6-point midpoint interpolation of b3[a] along a */
 int orc_uct_centre(const orc_cfg* c, const double* b3, double* Bc3);
 /* the preserved divergence sum_a delta_a Dh_a b^a at every cell (A41) */

@@ -241,10 +241,11 @@ static void der_face(const orc_cfg* c, const double F5[5][8], const int rough5[5
 
 /* Face flux at face i+1/2 from the stencil st[m][v] = prims of cells i-2+m,
  * m = 0..5, v = 0..7; xf = face coordinates; a = axis.  Shared by both paths.
- * UCT (divb = 2, A37): bnorm -> the staggered sqrt(gamma) B^a of this face, which
- * replaces both reconstructed normal components (Minkowski: sqrt(gamma) = 1), and
- * fs (if not NULL) receives the face data of the EMF step (A38): v^1..3 of the left
- * state, v^1..3 of the right state, a+ = S_R, a- = -S_L of the HLL flux (A4).
+ * UCT (divb = 2, A37): bnorm -> the staggered sqrt(gamma) B^a of this face, whose
+ * B^a = bnorm / sqrt(gamma_face) replaces both reconstructed normal components, and
+ * fs (if not NULL) receives the face data of the EMF step (A38, A43): V^1..3 =
+ * alpha v^i - beta^i of the left state, V^1..3 of the right state, a+ = S_R,
+ * a- = -S_L of the HLL flux (A4).
  * Returns the A31 roughness flag of the face. */
 static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8],
                      const double* bnorm, double fs[8]) {
@@ -262,9 +263,9 @@ static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3]
   if (!(qL[4] > 0.0)) qL[4] = st[2][4];
   if (!(qR[0] > 0.0)) qR[0] = st[3][0];
   if (!(qR[4] > 0.0)) qR[4] = st[3][4];
-  if (bnorm) qL[5 + a] = qR[5 + a] = *bnorm;
   orc_met m;
   orc_met_eval(c, xf, &m);
+  if (bnorm) qL[5 + a] = qR[5 + a] = *bnorm / m.sqrtg; /* b = sqrt(gamma) B at the face (A37) */
   orc_hll(&m, c->gamma, qL, qR, a, F);
   if (fs) {
     orc_aux al, ar;
@@ -273,9 +274,9 @@ static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3]
     double lmL, lpL, lmR, lpR;
     orc_speeds(&m, c->gamma, qL, a, &lmL, &lpL);
     orc_speeds(&m, c->gamma, qR, a, &lmR, &lpR);
-    for (int i = 0; i < 3; i++) {
-      fs[i] = al.v[i];
-      fs[3 + i] = ar.v[i];
+    for (int i = 0; i < 3; i++) { /* A43: the transport velocity V^i = alpha v^i - beta^i */
+      fs[i] = m.alpha * al.v[i] - m.beta[i];
+      fs[3 + i] = m.alpha * ar.v[i] - m.beta[i];
     }
     fs[6] = fmax(0.0, fmax(lpL, lpR));   /* a+ = S_R */
     fs[7] = -fmin(0.0, fmin(lmL, lmR));  /* a- = -S_L */
@@ -855,8 +856,8 @@ int orc_get_prims(const orc_cfg* c, const double* U8, const double* P5, double* 
 
 /* ------------------------------------------------------------------ */
 /* UCT: staggered field + upwind constrained transport (divb = 2;      */
-/* SURVEY.md §8(f) f2; readings A37-A42).  Minkowski,        */
-/* periodic or outflow axes.  b3[a][N]: sqrt(gamma) B^a at the face i_a + 1/2     */
+/* SURVEY.md §8(f) f2; readings A37-A43).  Periodic or     */
+/* outflow axes, any metric.  b3[a][N]: sqrt(gamma) B^a at the face i_a + 1/2     */
 /* owned by cell i (x1 fastest); E3[c][N]: EMF E^c at the edge         */
 /* (i_p + 1/2, i_q + 1/2, i_c) owned by cell i, (c, p, q) cyclic.      */
 /* ------------------------------------------------------------------ */
@@ -878,8 +879,9 @@ static void rec_pair(const orc_cfg* c, const double f[6], double* lo, double* hi
 }
 
 /* A39: UCT-HLL EMF E^cc at the edge owned by cell x.  p = cc+1, q = cc+2; W/E =
- * left/right along p, S/N = left/right along q.  E^cc = v^q B^p - v^p B^q, the flux
- * along q of B^p and minus the flux along p of B^q. */
+ * left/right along p, S/N = left/right along q.  E^cc = V^q b^p - V^p b^q (A43: V =
+ * alpha v - beta, b = sqrt(gamma) B), the densitised flux along q of b^p and minus the
+ * flux along p of b^q. */
 static double uct_emf(const orc_cfg* c, const double* FS, const double* b3, int cc, const long long x[3]) {
   const long long N = ncells(c);
   const int p = (cc + 1) % 3, q = (cc + 2) % 3;
@@ -966,10 +968,10 @@ static void uct_emf_induction(const orc_cfg* c, const double* FS, const double* 
   free(E3);
 }
 
-/* UCT scope (A37): Minkowski; periodic or outflow axes.  On an outflow side every
+/* UCT scope (A37): any metric; periodic or outflow axes.  On an outflow side every
  * staggered quantity (b, the face data, the EMFs) takes the ghost rule of A13 through
  * lin_shift: the nearest owned face / edge (zero gradient). */
-static int uct_ok(const orc_cfg* c) { return c->divb == 2 && c->metric == ORC_MINKOWSKI; }
+static int uct_ok(const orc_cfg* c) { return c->divb == 2; }
 
 /* A37: cell-centred field from the staggered one, 6-point midpoint interpolation
  * B^a(i) = (3 b_{i-5/2} - 25 b_{i-3/2} + 150 b_{i-1/2} + 150 b_{i+1/2} - 25 b_{i+3/2} + 3 b_{i+5/2}) / 256 */
@@ -1008,6 +1010,37 @@ int orc_uct_divh(const orc_cfg* c, const double* b3, double* out) {
         out[lin(c, i, j, k)] = d;
       }
   return 0;
+}
+
+/* state of a UCT run: the hydro prims of P8 and b3; B = I6(b3) / sqrt(gamma) at the centres */
+int orc_set_prims_uct(const orc_cfg* c, const double* P8, const double* b3, double* U8, double* P5, long long* bad) {
+  if (!uct_ok(c)) return -1;
+  const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
+  double* Q = (double*)malloc(sizeof(double) * 8 * N);
+  double* Bc = (double*)malloc(sizeof(double) * 3 * N);
+  if (!Q || !Bc) {
+    free(Q);
+    free(Bc);
+    return -3;
+  }
+  memcpy(Q, P8, sizeof(double) * 5 * N);
+  orc_uct_centre(c, b3, Bc);
+  for (long long k = 0; k < n2; k++)
+    for (long long j = 0; j < n1; j++)
+      for (long long i = 0; i < n0; i++) {
+        const long long id = lin(c, i, j, k);
+        double x[3] = {centre_of(c, 0, i), centre_of(c, 1, j), centre_of(c, 2, k)};
+        orc_met m;
+        orc_met_eval(c, x, &m);
+        for (int a = 0; a < 3; a++) Q[(5 + a) * N + id] = Bc[a * N + id] / m.sqrtg;
+      }
+  int rc = orc_set_prims(c, Q, U8, P5, bad);
+  /* U_B exactly I6(b) (the division and re-densitisation above may round) */
+  if (!rc)
+    for (long long e = 0; e < 3 * N; e++) U8[5 * N + e] = Bc[e];
+  free(Q);
+  free(Bc);
+  return rc;
 }
 
 int orc_rhs_uct(const orc_cfg* c, const double* U8, const double* P5, const double* b3, double* L8) {

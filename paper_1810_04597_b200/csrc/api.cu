@@ -203,7 +203,8 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
     });
     if (e == cudaSuccess)
       e = launch(c, kUctCell, [&] {
-        return launch_uct_cell(c->g, c->e, s, dt, dtp, c->R, c->Un, Uin, Uout, c->P, c->Bst, c->dcnt, cfl, c->st);
+        return launch_uct_cell(c->ks, c->g, c->e, c->mt, s, dt, dtp, c->R, c->Un, Uin, Uout, c->P, c->Bst, c->dcnt,
+                               cfl, c->st);
       });
     if (e != cudaSuccess) return cuda_fail(c, e, "uct update launch");
     c->cfl_valid = (s == 3);
@@ -255,11 +256,10 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   if (grid->rec < 0 || grid->rec > 5) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..5");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
   if (grid->divb < 0 || grid->divb > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0, 1 or 2");
-  if (grid->divb == 2) {  // UCT (A37, A42): Minkowski, periodic or outflow axes (no slabs)
-    bool ok = metric->kind == ECHO_METRIC_MINKOWSKI;
+  if (grid->divb == 2) {  // UCT (A37, A42, A43): periodic or outflow axes (no slabs), any metric
+    bool ok = true;
     for (int a = 0; a < 3; a++) ok = ok && grid->bc[a][0] != ECHO_BC_HALO && grid->bc[a][1] != ECHO_BC_HALO;
-    if (!ok)
-      return fail(nullptr, ECHO_E_ARG, "echo_create: divb = 2 (UCT) needs a Minkowski metric and periodic or outflow axes");
+    if (!ok) return fail(nullptr, ECHO_E_ARG, "echo_create: divb = 2 (UCT) needs periodic or outflow axes (no slabs)");
   }
   if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");
   if (!(eos->rho_floor > 0.0) || !(eos->p_floor > 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: floors > 0 violated");
@@ -512,7 +512,7 @@ int echo_set_face_field(echo_ctx* c, const double* b3, int on_device) {
     src = c->scratch;
   }
   CK(launch(c, kLayout, [&] { return launch_layout(c->g, src, c->Bst, 3, false, c->st); }), "echo_set_face_field");
-  CK(launch(c, kPrim2Cons, [&] { return launch_uct_centre_p2c(c->g, c->e, c->P, c->Un, c->Bst, c->st); }),
+  CK(launch(c, kPrim2Cons, [&] { return launch_uct_centre_p2c(c->ks, c->g, c->e, c->mt, c->P, c->Un, c->Bst, c->st); }),
      "echo_set_face_field");
   if (!on_device) CK(cudaStreamSynchronize(c->st), "echo_set_face_field");
   c->have_faces = true;

@@ -242,7 +242,8 @@ ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, 
 }
 
 // densitised HLL flux (7 comps) between two reconstructed states at one face (A4)
-// fs (UCT, A38): if not NULL, v^1..3 of the left and of the right state, a+ = S_R, a- = -S_L
+// fs (UCT, A38, A43): if not NULL, V^1..3 = alpha v^i - beta^i of the left and of the right
+// state, a+ = S_R, a- = -S_L
 template <class M>
 ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* pr, int AX, double* F,
                      double* fs = nullptr) {
@@ -257,11 +258,11 @@ ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* 
   speeds(m, e, pr, sr, AX, lmR, lpR);
   const double sL = dmin(0.0, dmin(lmL, lmR));
   const double sR = dmax(0.0, dmax(lpL, lpR));
-  if (fs) {
+  if (fs) {  // A43: the transport velocity V^i = alpha v^i - beta^i of each state
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-      fs[i] = sl.v[i];
-      fs[3 + i] = sr.v[i];
+      fs[i] = fma(m.alpha(), sl.v[i], -m.beta(i));
+      fs[3 + i] = fma(m.alpha(), sr.v[i], -m.beta(i));
     }
     fs[6] = sR;
     fs[7] = -sL;

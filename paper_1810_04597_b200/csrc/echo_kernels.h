@@ -76,12 +76,14 @@ cudaError_t launch_uct_emf(const GridP& g, const double* const FS[3], const doub
 // Lout[5 + a][cell]
 cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const double* dtp, const double* Ed,
                               double* Bst, double* Lout, cudaStream_t st);
-// hydro RK combine (rhs from the sweeps in R), U_B = I6(b), con2prim + floors, CFL rate
-cudaError_t launch_uct_cell(const GridP& g, const EosP& e, int s, double dt, const double* dtp, const double* R,
-                            const double* Un, const double* Us, double* Uout, double* P, const double* Bst,
-                            unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st);
-// U_B = I6(b^n) and U recomputed from the state's hydro primitives (echo_set_face_field)
-cudaError_t launch_uct_centre_p2c(const GridP& g, const EosP& e, const double* P, double* U, const double* Bst,
-                                  cudaStream_t st);
+// hydro RK combine (rhs from the sweeps in R, + KS sources), U_B = I6(b), con2prim + floors, CFL rate
+cudaError_t launch_uct_cell(bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
+                            const double* dtp, const double* R, const double* Un, const double* Us, double* Uout,
+                            double* P, const double* Bst, unsigned long long* counters, unsigned long long* cfl_out,
+                            cudaStream_t st);
+// U_B = I6(b^n) and U recomputed from the state's hydro primitives (echo_set_face_field;
+// KS: also B = U_B / sqrt(g) into P)
+cudaError_t launch_uct_centre_p2c(bool ks, const GridP& g, const EosP& e, const MetTables& mt, double* P, double* U,
+                                  const double* Bst, cudaStream_t st);
 
 }  // namespace echo

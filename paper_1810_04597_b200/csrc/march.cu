@@ -421,27 +421,34 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
         const int xf = B + 2 + i;
         if (xf >= -3) {
           double F[7];
+          // the face metric (KS: 2-D tables; Minkowski: flat)
+          auto face_hll = [&](const auto& mf) {
+            if constexpr (UCT) {
+              // A37: both states take the staggered normal field of face xf + 1/2 (owned by
+              // cell xf; A42 ghost rule), b = sqrt(g) B
+              const long long fo = lb + (long long)map_index(xf, lg.na, g.bc[AX][0], g.bc[AX][1]) * as;
+              const double bnv = Bface[fo + AX * vs] * (KS ? frcp(mf.sqrtg()) : 1.0);
+              pl[5 + AX] = bnv;
+              qR[5 + AX] = bnv;
+              double fsv[8];
+              hll_face(mf, e, pl, qR, AX, F, fsv);
+              if (xf >= 0 && xf < lg.na && line_ok) {
+#pragma unroll
+                for (int m = 0; m < 8; m++) FSo[lb + (long long)xf * as + m * vs] = fsv[m];
+              }
+            } else {
+              hll_face(mf, e, pl, qR, AX, F);
+            }
+          };
           if (KS) {
             const int af = max(-kG, min(xf + 1, lg.na + kG));  // face af - 1/2
             const double* rec;
             if (AX == 0) rec = f0_rec(mt, af, tt);
             else if (AX == 1) rec = f1_rec(mt, tt, af);
             else rec = cen_rec(mt, tt, zz);
-            hll_face(load_met(rec), e, pl, qR, AX, F);
-          } else if constexpr (UCT) {
-            // A37: both states take the staggered normal field of face xf + 1/2 (owned by cell xf)
-            const long long fo = lb + (long long)map_index(xf, lg.na, g.bc[AX][0], g.bc[AX][1]) * as;
-            const double bnv = Bface[fo + AX * vs];
-            pl[5 + AX] = bnv;
-            qR[5 + AX] = bnv;
-            double fsv[8];
-            hll_face(FlatMet(), e, pl, qR, AX, F, fsv);
-            if (xf >= 0 && xf < lg.na && line_ok) {
-#pragma unroll
-              for (int m = 0; m < 8; m++) FSo[lb + (long long)xf * as + m * vs] = fsv[m];
-            }
+            face_hll(load_met(rec));
           } else {
-            hll_face(FlatMet(), e, pl, qR, AX, F);
+            face_hll(FlatMet());
           }
           const int fp = loff<AX, RINGF>(t, wrapf<AX>(rbf + 2 + i));
 #pragma unroll
@@ -497,10 +504,7 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
 template <int AX, bool KS, int DER, int REC>
 static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
                              const double* Bface, double* FSo, cudaStream_t st) {
-  if (g.divb == 2) {
-    if constexpr (KS) return cudaErrorInvalidValue;  // UCT: Minkowski only (A37)
-    else return launch_one<AX, KS, DER, REC, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
-  }
+  if (g.divb == 2) return launch_one<AX, KS, DER, REC, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
   if (g.divb == 1) return launch_one<AX, KS, DER, REC, 1>(g, e, mt, P, UB, R, nullptr, nullptr, st);
   return launch_one<AX, KS, DER, REC, 0>(g, e, mt, P, UB, R, nullptr, nullptr, st);
 }

@@ -1,18 +1,19 @@
 // uct.cu — the staggered-field update of divb = 2 (UCT; DESIGN.md
-// readings A37-A42): Minkowski, periodic or outflow axes (A42: on an outflow side the staggered
-// quantities take the nearest owned face / edge, as the cell ghosts do, A13).
+// readings A37-A43): periodic or outflow axes (A42: on an outflow side the staggered
+// quantities take the nearest owned face / edge, as the cell ghosts do, A13), any metric
+// (A43: the face data carry V = alpha v - beta, so the EMF step needs no metric).
 //
 // State: Bst record array, slots 0..2 = b^n, 3..5 = b^s, where b^a = sqrt(gamma) B^a at
 // the face i_a + 1/2 owned by cell i.  The sweeps (march.cu, DM = 2) take the normal
 // field of every face from the stage-input b and leave per owned face, in FS[a] (one
 // record array per axis), the face data of the EMF step: v^1..3 of the left and of the
-// right HLL state, a+ = S_R, a- = -S_L.  Then per stage:
+// right HLL state (V = alpha v - beta), a+ = S_R, a- = -S_L.  Then per stage:
 //   k_uct_emf     E^c at the edge (i_p + 1/2, i_q + 1/2, i_c) owned by each cell, (c, p, q)
 //                 cyclic: 4 quadrant states from double reconstructions of the face data
 //                 (A38) combined by the UCT-HLL formula (A39, A40)          -> Ed slots 0..2
 //   k_uct_induct  L(b^p) = -delta_q Dh_q E^c + delta_c Dh_c E^q (A41) and the literal RK
 //                 form of stage s per face (or L(b) alone for echo_rhs)     -> Bst
-//   k_uct_cell    hydro RK combine from the sweeps' rhs, U_B = I6(b) of the new field (A37),
+//   k_uct_cell    hydro RK combine from the sweeps' rhs (+ KS sources), U_B = I6(b) (A37),
 //                 con2prim + floors, the CFL rate of the new state           -> U, P
 // One thread per cell; neighbours through the ghost index map (L1/L2).
 #include <cuda_runtime.h>
@@ -180,10 +181,11 @@ ECHO_D void centre_field(const GridP& g, const double* __restrict__ Bst, int slo
   }
 }
 
+template <bool KS>
 __global__ void __launch_bounds__(kCellThreads, 3)
-k_uct_cell(const GridP g, const EosP e, int s, double dt, const double* dtp, const double* __restrict__ R,
-           const double* Un, const double* Us, double* Uout, double* P, const double* __restrict__ Bst,
-           unsigned long long* counters, unsigned long long* cfl_out) {
+k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, const double* dtp,
+           const double* __restrict__ R, const double* Un, const double* Us, double* Uout, double* P,
+           const double* __restrict__ Bst, unsigned long long* counters, unsigned long long* cfl_out) {
   if (dtp) {
     if (dtp[1] != 0.0) return;  // uniform over the grid (no thread left at a block barrier)
     dt = dtp[0];
@@ -195,18 +197,21 @@ k_uct_cell(const GridP g, const EosP e, int s, double dt, const double* dtp, con
     int x[3];
     cell_ijk(g, id, x[0], x[1], x[2]);
     const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
-    const FlatMet m;
-    double Pp[8], Uo[8];
+    const auto m = MetAt<KS>::get(mt, x[0], x[1]);
+    double Pp[8], Uo[8], L[8];
 #pragma unroll
-    for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];
+    for (int v = 0; v < (KS ? 8 : 5); v++) Pp[v] = P[rb + v * vs];  // KS: B for the sources
+#pragma unroll
+    for (int q = 0; q < 5; q++) L[q] = R[rb + q * vs];
+    if constexpr (KS) add_sources(m, der_rec(mt, x[0], x[1]), e, Pp, L);  // a6
     ld8(Un + rb, vs, Uo);
     if (s == 1) {
 #pragma unroll
-      for (int q = 0; q < 5; q++) Uo[q] = Uo[q] + dt * R[rb + q * vs];
+      for (int q = 0; q < 5; q++) Uo[q] = Uo[q] + dt * L[q];
     } else {
       const double c0 = (s == 2) ? 0.75 : (1.0 / 3.0), c1 = (s == 2) ? 0.25 : (2.0 / 3.0);
 #pragma unroll
-      for (int q = 0; q < 5; q++) Uo[q] = c0 * Uo[q] + c1 * (Us[rb + q * vs] + dt * R[rb + q * vs]);
+      for (int q = 0; q < 5; q++) Uo[q] = c0 * Uo[q] + c1 * (Us[rb + q * vs] + dt * L[q]);
     }
     double Bc[3];
     centre_field(g, Bst, s == 3 ? 0 : 3, x, Bc);  // the field this stage just wrote
@@ -214,10 +219,11 @@ k_uct_cell(const GridP g, const EosP e, int s, double dt, const double* dtp, con
     for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a];
     double Po[8];
     ev = c2p_floors(m, e, Uo, Pp, Po);
+    const double isg = !KS ? 1.0 : frcp(m.sqrtg());
 #pragma unroll
-    for (int a = 0; a < 3; a++) Po[5 + a] = Uo[5 + a];
+    for (int a = 0; a < 3; a++) Po[5 + a] = Uo[5 + a] * isg;
     st8(Uout + rb, vs, Uo);
-    st_prims<false>(P + rb, vs, Po);
+    st_prims<KS>(P + rb, vs, Po);
     if (cfl_out) rate = cfl_rate(m, g, e, Po);
   }
   if (cfl_out) {
@@ -241,23 +247,28 @@ k_uct_cell(const GridP g, const EosP e, int s, double dt, const double* dtp, con
 }
 
 // set: U_B = I6(b^n) and U from the state's hydro primitives (a0 with the new field)
+template <bool KS>
 __global__ void __launch_bounds__(kCellThreads)
-k_uct_centre_p2c(const GridP g, const EosP e, const double* __restrict__ P, double* __restrict__ U,
+k_uct_centre_p2c(const GridP g, const EosP e, const MetTables mt, double* __restrict__ P, double* __restrict__ U,
                  const double* __restrict__ Bst) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= g.N) return;
   int x[3];
   cell_ijk(g, id, x[0], x[1], x[2]);
   const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
-  double pr[8];
+  const auto m = MetAt<KS>::get(mt, x[0], x[1]);
+  double pr[8], Bc[3];
 #pragma unroll
   for (int v = 0; v < 5; v++) pr[v] = P[rb + v * vs];
-  centre_field(g, Bst, 0, x, pr + 5);
+  centre_field(g, Bst, 0, x, Bc);
+  const double sg = m.sqrtg(), isg = !KS ? 1.0 : 1.0 / sg;
+#pragma unroll
+  for (int a = 0; a < 3; a++) pr[5 + a] = Bc[a] * isg;
   State st;
-  const FlatMet m;
   make_state(m, e, pr, st);
-  double u[8] = {st.D, st.S[0], st.S[1], st.S[2], st.tau, pr[5], pr[6], pr[7]};
+  double u[8] = {sg * st.D, sg * st.S[0], sg * st.S[1], sg * st.S[2], sg * st.tau, Bc[0], Bc[1], Bc[2]};
   st8(U + rb, vs, u);
+  if (KS) st8(P + rb, vs, pr);
 }
 
 template <int REC>
@@ -289,18 +300,23 @@ cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_uct_cell(const GridP& g, const EosP& e, int s, double dt, const double* dtp, const double* R,
-                            const double* Un, const double* Us, double* Uout, double* P, const double* Bst,
-                            unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st) {
+cudaError_t launch_uct_cell(bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
+                            const double* dtp, const double* R, const double* Un, const double* Us, double* Uout,
+                            double* P, const double* Bst, unsigned long long* counters, unsigned long long* cfl_out,
+                            cudaStream_t st) {
   const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
-  k_uct_cell<<<blocks, kCellThreads, 0, st>>>(g, e, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
+  if (ks)
+    k_uct_cell<true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
+  else
+    k_uct_cell<false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_uct_centre_p2c(const GridP& g, const EosP& e, const double* P, double* U, const double* Bst,
-                                  cudaStream_t st) {
+cudaError_t launch_uct_centre_p2c(bool ks, const GridP& g, const EosP& e, const MetTables& mt, double* P, double* U,
+                                  const double* Bst, cudaStream_t st) {
   const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
-  k_uct_centre_p2c<<<blocks, kCellThreads, 0, st>>>(g, e, P, U, Bst);
+  if (ks) k_uct_centre_p2c<true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, U, Bst);
+  else k_uct_centre_p2c<false><<<blocks, kCellThreads, 0, st>>>(g, e, mt, P, U, Bst);
   return cudaGetLastError();
 }
 

@@ -50,7 +50,8 @@ def start(E, orc, p):
     return oc, g, U, P, ob
 
 
-CASES = [(0, (32, 32, 32)), (0, (70, 13, 36)), (1, (24, 20, 28)), (2, (45, 38, 41)), (3, (40, 40, 40))]
+CASES = [(0, (32, 32, 32)), (0, (70, 13, 36)), (1, (24, 20, 28)), (2, (45, 38, 41)), (3, (40, 40, 40)),
+         (4, (72, 35, 24))]
 
 
 @pytest.mark.parametrize("cfg,n", CASES)
@@ -85,7 +86,8 @@ def test_uct_rhs_and_stage_parity(E, orc, cfg, n):
 
 @pytest.mark.parametrize("cfg,n,steps,rec", [(0, (32, 32, 32), 10, 0), (1, (32, 32, 32), 10, 0),
                                               (0, (24, 28, 20), 10, 2), (0, (24, 28, 20), 6, 5),
-                                              (2, (40, 36, 34), 10, 0), (2, (40, 36, 34), 10, 2)])
+                                              (2, (40, 36, 34), 10, 0), (2, (40, 36, 34), 10, 2),
+                                              (4, (64, 32, 16), 10, 0)])
 def test_uct_multistep_parity(E, orc, cfg, n, steps, rec):
     p = uct_problem(cfg, n, rec)
     oc, g, U, P, ob = start(E, orc, p)
@@ -101,7 +103,7 @@ def test_uct_multistep_parity(E, orc, cfg, n, steps, rec):
     assert_groups(g.get_face_field(), ob, FACE, TOL_10, what=f"{steps} steps b")
     st = g.stats()
     assert [st["floor_events"], st["c2p_failures"]] == ocnt  # counted, identical (A9)
-    if cfg != 2:  # the blast's floors may fire; the smooth configs' never
+    if cfg not in (2, 4):  # blast / torus atmosphere floors may fire; the smooth configs' never
         assert ocnt == [0, 0]
 
 
@@ -144,7 +146,8 @@ def test_uct_api_rules(E):
     h.set_prims(P8)
     with pytest.raises(E.EchoError):
         h.set_face_field(I.face_field(p))
-    r = I.problem(4, n=(16, 16, 16))  # Kerr-Schild: UCT refused at create
+    r = I.problem(0, n=(16, 16, 16))  # slab (halo) boundaries: UCT refused at create
     r.divb = 2
+    r.bc = ((0, 0), (0, 0), (2, 2))
     with pytest.raises(E.EchoError):
         E.Echo(r)
