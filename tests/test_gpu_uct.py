@@ -151,3 +151,53 @@ def test_uct_api_rules(E):
     r.bc = ((0, 0), (0, 0), (2, 2))
     with pytest.raises(E.EchoError):
         E.Echo(r)
+
+
+def test_uct_full_size_conservation_and_divh(E):
+    """Properties that hold at any size, at BASELINE.json's 512^3 (config 3) with UCT:
+    the sums of sqrt(g) U (hydro) and of every staggered component are conserved to
+    roundoff over 2 steps, and div_H b (A41: sum_a delta_a Dh_a b^a) changes only by
+    roundoff.  The reductions and the DER6 divergence are test-side torch ops."""
+    import torch
+
+    p = uct_problem(3, None)
+    g = E.Echo(p)
+    g.set_prims(I.initial_prims(p, device="cuda"))
+    g.set_face_field(I.face_field(p, device="cuda"))
+    N = p.ncells
+    U = torch.empty((8, N), dtype=torch.float64, device="cuda")
+    b = torch.empty((3, p.n[2], p.n[1], p.n[0]), dtype=torch.float64, device="cuda")
+    c0, c1, c2 = 1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0
+
+    def divh():
+        out = torch.zeros_like(b[0])
+        for a in range(3):
+            ax = 2 - a
+            f = b[a]
+            D = c0 * f + c1 * (torch.roll(f, 1, ax) + torch.roll(f, -1, ax)) + c2 * (torch.roll(f, 2, ax) + torch.roll(f, -2, ax))
+            out += (D - torch.roll(D, 1, ax)) * p.n[a]
+            del D
+        return out
+
+    def state():
+        E.get_cons(g.ctx, U)
+        E.get_face_field(g.ctx, b)
+        torch.cuda.synchronize()
+        s = [float(U[q].sum()) for q in range(5)] + [float(b[a].sum()) for a in range(3)]
+        m = [float(U[q].abs().sum()) for q in range(5)] + [float(b[a].abs().sum()) for a in range(3)]
+        return s, m
+
+    s0, m0 = state()
+    d0 = divh()
+    bmax = float(b.abs().max())
+    for _ in range(2):
+        g.step(g.max_dt(p.cfl))
+    s1, _ = state()
+    d1 = divh()
+    change = float((d1 - d0).abs().max())
+    assert change < 200 * 2.2e-16 * bmax * p.n[0], (change, bmax)
+    for q in range(8):
+        assert abs(s1[q] - s0[q]) <= 1e-12 * m0[q], (q, s0[q], s1[q], m0[q])
+    st = g.stats()
+    assert st["floor_events"] == 0 and st["c2p_failures"] == 0
+    g.close()
