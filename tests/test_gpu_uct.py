@@ -201,3 +201,27 @@ def test_uct_full_size_conservation_and_divh(E):
     st = g.stats()
     assert st["floor_events"] == 0 and st["c2p_failures"] == 0
     g.close()
+
+
+@pytest.mark.parametrize("n,bc", [((33, 1, 1), ((0, 0), (0, 0), (0, 0))), ((1, 24, 7), ((0, 0), (0, 0), (0, 0))),
+                                  ((5, 3, 9), ((1, 1), (0, 0), (1, 1))), ((1, 1, 1), ((0, 0), (0, 0), (0, 0)))])
+def test_uct_degenerate_grids_parity(E, orc, n, bc):
+    """UCT edge cases: single-cell axes (edges whose transverse stencils wrap onto one
+    cell), lines shorter than a chunk or the halo, outflow sides on short axes; rhs and
+    3 steps against the oracle."""
+    p = uct_problem(0, n)
+    p.bc = bc
+    oc, g, U, P, ob = start(E, orc, p)
+    dt = orc.max_dt(oc, U, P, p.cfl)
+    L = orc.rhs_uct(oc, U, P, ob)
+    Lg = g.rhs()
+    assert_rhs_groups(Lg[:5], L[:5], U[:5], dt, HYDRO, TOL_STAGE, what=f"uct rhs {n}")
+    assert_rhs_groups(Lg[5:], L[5:], ob, dt, FACE, TOL_STAGE, what=f"uct L(b) {n}")
+    for _ in range(3):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        U, P, ob, _ = orc.step_uct(oc, dt, U, P, ob)
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"3 steps U {n}")
+    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"3 steps P {n}")
+    assert_groups(g.get_face_field(), ob, FACE, TOL_10, what=f"3 steps b {n}")
