@@ -28,10 +28,21 @@ struct MetAt<true> {
 };
 
 // ----------------------------------------------------------- con2prim (A8)
-// 1-D Newton in Z = rho h W^2 with the oracle's iteration rules (A8, A27, A28).
-// u: non-densitised (D, S_i, tau, B^i); guess: (rho, u~^i, p); out: (rho, u~^i, p).
+// The Newton guess of A8: Z0 = rho h W^2 = (rho + Gamma/(Gamma-1) p)(1 + u~.u~) of the previous
+// stage's primitives pr = (rho, u~^i, p).  In Minkowski K3 stores it in the otherwise unused P
+// slot 5 when it writes the new primitives, so the next stage reads 8 bytes instead of 40.
 template <class M>
-ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* guess, double* out) {
+ECHO_D double guess_Z(const M& m, const EosP& e, const double* pr) {
+  double gu[3] = {pr[1], pr[2], pr[3]}, gl[3];
+  m.lower(gu, gl);
+  return (pr[0] + e.gfac * pr[4]) * (1.0 + gu[0] * gl[0] + gu[1] * gl[1] + gu[2] * gl[2]);
+}
+constexpr int kSlotZ = 5;  // P slot of the stored guess (Minkowski only: KS keeps B^i in slots 5..7)
+
+// 1-D Newton in Z = rho h W^2 with the oracle's iteration rules (A8, A27, A28).
+// u: non-densitised (D, S_i, tau, B^i); Z0: guess_Z of the previous primitives; out: (rho, u~^i, p).
+template <class M>
+ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, double Z0, double* out) {
   const double D = u[0], tau = u[4];
   const double S[3] = {u[1], u[2], u[3]};
   const double B[3] = {u[5], u[6], u[7]};
@@ -43,9 +54,7 @@ ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* 
   const double B2 = B[0] * Bl[0] + B[1] * Bl[1] + B[2] * Bl[2];
   const double SB = S[0] * B[0] + S[1] * B[1] + S[2] * B[2];
   const double SB2 = SB * SB;
-  double gu[3] = {guess[1], guess[2], guess[3]}, gl[3];
-  m.lower(gu, gl);
-  double Z = (guess[0] + e.gfac * guess[4]) * (1.0 + gu[0] * gl[0] + gu[1] * gl[1] + gu[2] * gl[2]);
+  double Z = Z0;
   bool polish = false, ok = false;
   for (int it = 1; it <= e.maxit; it++) {
     // 1/Z and 1/(Z + B^2) through one reciprocal; 1/sqrt(1 - v^2) from the rsqrt that gives sqrt(1 - v^2)
@@ -96,18 +105,21 @@ ECHO_D int c2p_newton(const M& m, const EosP& e, const double* u, const double* 
   return 0;
 }
 
-// A9 floors on the densitised cons Uc (8); Pprev (5) in, Pout (5) out.
+// A9 floors on the densitised cons Uc (8); Z0 = guess_Z of the previous primitives; prev(P5)
+// fills the previous primitives (called only when the Newton fails); Pout (5) out.
 // Returns 0 (nothing), 1 (floor event), 2 (failure).
-template <class M>
-ECHO_D int c2p_floors(const M& m, const EosP& e, double* Uc, const double* Pprev, double* Pout) {
+template <class M, class Prev>
+ECHO_D int c2p_floors(const M& m, const EosP& e, double* Uc, double Z0, const Prev& prev, double* Pout) {
   const double isg = 1.0 / m.sqrtg();
   double u[8];
 #pragma unroll
   for (int q = 0; q < 8; q++) u[q] = M::kFlat ? Uc[q] : Uc[q] * isg;
   double pr[5];
-  int status = c2p_newton(m, e, u, Pprev, pr);
+  int status = c2p_newton(m, e, u, Z0, pr);
   int ev = 0;
   if (status != 0) {
+    double Pprev[5];
+    prev(Pprev);
     double up[3] = {Pprev[1], Pprev[2], Pprev[3]}, ul[3];
     m.lower(up, ul);
     double Wp = sqrt(1.0 + up[0] * ul[0] + up[1] * ul[1] + up[2] * ul[2]);
@@ -291,11 +303,12 @@ ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s,
   const auto m = MetAt<KS>::get(mt, i, j);
   const long long rb = rec_base(g, i, j, k), vs = g.vs;
   double Pp[8];
+  double Z0;
   if (KS) {
     ld8(P + rb, vs, Pp);  // rho, u~, p, B of the stage input (B for the sources)
+    Z0 = guess_Z(m, e, Pp);
   } else {
-#pragma unroll
-    for (int v = 0; v < 5; v++) Pp[v] = P[rb + v * vs];  // the con2prim guess only
+    Z0 = P[rb + kSlotZ * vs];  // the stored Newton guess (the primitives only on a failure)
   }
   double L[8];
   cell_L<KS, DIVB_NONE>(g, e, mt, m, R, rb, i, j, k, Pp, L);
@@ -316,12 +329,16 @@ ECHO_D int stage_cell(const GridP& g, const EosP& e, const MetTables& mt, int s,
     }
   }
   double Po[8];
-  const int ev = c2p_floors(m, e, Uo, Pp, Po);
+  const int ev = c2p_floors(m, e, Uo, Z0, [&](double* pv) {
+#pragma unroll
+    for (int v = 0; v < 5; v++) pv[v] = KS ? Pp[v] : P[rb + v * vs];
+  }, Po);
   const double isg = !KS ? 1.0 : frcp(m.sqrtg());
 #pragma unroll
   for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
   st8(Uout + rb, vs, Uo);
   st_prims<KS>(P + rb, vs, Po);
+  if (!KS) P[rb + kSlotZ * vs] = guess_Z(m, e, Po);  // the next stage's Newton guess
   if (want_rate) rate = fmax(rate, cfl_rate(m, g, e, Po));  // a9 fused: CFL rate of the new state
   if (gl && gl->on) {  // slab mode: the fused ghost exchange (echo_halo_link) and outflow replication
     const long long plane = (long long)g.n[1] * g.pitch;

@@ -199,8 +199,13 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
     const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
     const auto m = MetAt<KS>::get(mt, x[0], x[1]);
     double Pp[8], Uo[8], L[8];
-#pragma unroll
-    for (int v = 0; v < (KS ? 8 : 5); v++) Pp[v] = P[rb + v * vs];  // KS: B for the sources
+    double Z0;
+    if (KS) {
+      ld8(P + rb, vs, Pp);  // B for the sources
+      Z0 = guess_Z(m, e, Pp);
+    } else {
+      Z0 = P[rb + kSlotZ * vs];  // the stored Newton guess
+    }
 #pragma unroll
     for (int q = 0; q < 5; q++) L[q] = R[rb + q * vs];
     if constexpr (KS) add_sources(m, der_rec(mt, x[0], x[1]), e, Pp, L);  // a6
@@ -218,12 +223,16 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
 #pragma unroll
     for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a];
     double Po[8];
-    ev = c2p_floors(m, e, Uo, Pp, Po);
+    ev = c2p_floors(m, e, Uo, Z0, [&](double* pv) {
+#pragma unroll
+      for (int v = 0; v < 5; v++) pv[v] = KS ? Pp[v] : P[rb + v * vs];
+    }, Po);
     const double isg = !KS ? 1.0 : frcp(m.sqrtg());
 #pragma unroll
     for (int a = 0; a < 3; a++) Po[5 + a] = Uo[5 + a] * isg;
     st8(Uout + rb, vs, Uo);
     st_prims<KS>(P + rb, vs, Po);
+    if (!KS) P[rb + kSlotZ * vs] = guess_Z(m, e, Po);
     if (cfl_out) rate = cfl_rate(m, g, e, Po);
   }
   if (cfl_out) {

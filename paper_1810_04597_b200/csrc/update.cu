@@ -71,12 +71,16 @@ k_update(const GridP g, const EosP e, const MetTables mt, const int s, const dou
       } else {  // c2p
         double Uo[8], Po[8];
         ld8(Un + rb, vs, Uo);
-        ev = c2p_floors(m, e, Uo, Pp, Po);
+        ev = c2p_floors(m, e, Uo, guess_Z(m, e, Pp), [&](double* pv) {
+#pragma unroll
+          for (int v = 0; v < 5; v++) pv[v] = Pp[v];
+        }, Po);
         const double isg = !KS ? 1.0 : frcp(m.sqrtg());
 #pragma unroll
         for (int c = 0; c < 3; c++) Po[5 + c] = !KS ? Uo[5 + c] : Uo[5 + c] * isg;
         st8(Uout + rb, vs, Uo);
         st_prims<KS>(P + rb, vs, Po);
+        if (!KS) P[rb + kSlotZ * vs] = guess_Z(m, e, Po);
         if (cfl_out) rate = cfl_rate(m, g, e, Po);
       }
     }
@@ -207,6 +211,7 @@ k_prim2cons(const GridP g, const EosP e, const MetTables mt, const double* __res
   const double sg = m.sqrtg();
   double u[8] = {sg * s.D, sg * s.S[0], sg * s.S[1], sg * s.S[2], sg * s.tau, sg * pr[5], sg * pr[6], sg * pr[7]};
   st8(U + rec_base(g, i, j, k), g.vs, u);
+  if (!KS) pr[kSlotZ] = guess_Z(m, e, pr);  // Minkowski: B lives in U; slot 5 holds the Newton guess
   st8(P + rec_base(g, i, j, k), g.vs, pr);
 }
 
