@@ -62,12 +62,18 @@ def main(tag):
                 ns = v * {"ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "nsecond": 1}.get(unit, 1)
                 f.write(f"{r['ID']},{name},{ns:.0f}\n")
                 per.setdefault(name, []).append(ns)
-        tot = sum(sum(v) for v in per.values())
+        ours = {k: v for k, v in per.items() if k.startswith(("march::", "echo::"))}
+        tot = sum(sum(v) for v in ours.values())
         with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
             f.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised; compare shares)\n")
+            f.write("shares over this library's kernels; torch kernels (the on-device initial condition) listed after\n")
             f.write(f"{'kernel':60s} {'launches':>8s} {'mean_ms':>10s} {'share':>7s}\n")
-            for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+            for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
                 f.write(f"{k:60s} {len(v):8d} {statistics.mean(v) / 1e6:10.3f} {sum(v) / tot:7.3f}\n")
+            f.write("-- not ours (input generation, outside the timed region):\n")
+            for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+                if k not in ours:
+                    f.write(f"{k[:60]:60s} {len(v):8d} {statistics.mean(v) / 1e6:10.3f}\n")
     # full capture
     rep = os.path.join(OUT, "prof_round.ncu-rep")
     if not os.path.exists(rep):
