@@ -66,10 +66,18 @@ struct Geo {
   static constexpr int CH = S.ch;                             // cells per chunk = threads per line
   static constexpr int LOG_NL = ilog2(NL);
   static constexpr int LOG_CH = ilog2(CH);
-  // ring length for primitives and face fluxes: >= CH + 10 live entries (a power of two when cheap)
-  static constexpr int RING = (CH + 10 <= 16) ? 16 : (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
+  // ring length for primitives and face fluxes: >= CH + 10 live entries (a power of two when cheap;
+  // -DECHO_TIGHT_RINGS: exactly the live length, less shared memory per CTA for more CTAs per SM)
+#ifdef ECHO_TIGHT_RINGS
+  static constexpr bool TIGHT = AX != 0;  // y/z only (the x rings stay powers of two)
+#else
+  static constexpr bool TIGHT = false;
+#endif
+  static constexpr int RING = TIGHT ? CH + 10
+                                    : (CH + 10 <= 16) ? 16 : (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
   // face-flux ring: B(c) writes faces B+2..B+CH+1 while faces B-2..B+1 are still needed by D(c+1)
-  static constexpr int RINGF = (CH + 4 <= 8) ? 8 : (CH + 4 <= 32) ? 32 : (CH + 4 <= 64) ? 64 : CH + 16;
+  static constexpr int RINGF = TIGHT ? CH + 4
+                                     : (CH + 4 <= 8) ? 8 : (CH + 4 <= 32) ? 32 : (CH + 4 <= 64) ? 64 : CH + 16;
   // first chunk: its A phase reaches down to the ghost cell -3 (WENO of cells -3.. for faces -3..)
   static constexpr int C_FIRST = -((6 + CH - 1) / CH);
   static constexpr int B_FIRST = C_FIRST * CH;
@@ -334,8 +342,14 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       unsigned fm = 0u;  // this chunk's CH flags of line t
       if constexpr (kBallot) {
         const unsigned b = __ballot_sync(0xffffffffu, rgh);
-        if constexpr (AX == 0) fm = b;  // lane = slot
-        else fm = (((b >> t) & 0x01010101u) * 0x10204080u) >> 28;  // lanes i*8 + t, i = 0..3
+        if constexpr (AX == 0) {
+          fm = b;  // lane = slot
+        } else if constexpr (GE::NL == 8 && CH == 4) {
+          fm = (((b >> t) & 0x01010101u) * 0x10204080u) >> 28;  // lanes i*8 + t, i = 0..3
+        } else {  // lanes i*NL + t, i = 0..CH-1
+#pragma unroll
+          for (int i2 = 0; i2 < CH; i2++) fm |= ((b >> (i2 * GE::NL + t)) & 1u) << i2;
+        }
       }
       // ---- D1: DER flux (a4) at the right face X0+i+1/2 of cell X0+i (faces X0+i-2..X0+i+2) ----
       double H[7];
