@@ -45,6 +45,16 @@ namespace march {
 #define ECHO_X_CH 32
 #define ECHO_X_BPS 6
 #endif
+// -DECHO_YZ_LINE_MAJOR: the y/z sweeps take the x sweep's thread mapping (one warp per
+// line, lanes = consecutive cells along it; NL lines adjacent in x share their 32-byte
+// sectors through L1) instead of lanes alternating between 8 adjacent x-lines
+#ifdef ECHO_YZ_LINE_MAJOR
+#ifndef ECHO_YZ_NL
+#define ECHO_YZ_NL 4
+#define ECHO_YZ_CH 32
+#define ECHO_YZ_BPS 6
+#endif
+#endif
 #ifndef ECHO_YZ_NL
 #define ECHO_YZ_NL 8
 #define ECHO_YZ_CH 4
@@ -59,9 +69,17 @@ constexpr GeomSpec kGeomYZ{ECHO_YZ_NL, ECHO_YZ_CH, ECHO_YZ_BPS};
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 constexpr bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
+#ifdef ECHO_YZ_LINE_MAJOR
+constexpr bool kYzLineMajor = true;
+#else
+constexpr bool kYzLineMajor = false;
+#endif
+
 template <int AX>
 struct Geo {
   static constexpr GeomSpec S = (AX == 0) ? kGeomX : kGeomYZ;
+  // line-major thread mapping (slot fastest): the x sweep, and y/z with ECHO_YZ_LINE_MAJOR
+  static constexpr bool LM = (AX == 0) || kYzLineMajor;
   static constexpr int NL = S.nl;
   static constexpr int CH = S.ch;                             // cells per chunk = threads per line
   static constexpr int LOG_NL = ilog2(NL);
@@ -86,7 +104,7 @@ struct Geo {
   static constexpr int RR = (2 * CH + 5 <= 16) ? 16 : (2 * CH + 5 <= 64) ? 64 : (2 * CH + 5 <= 128) ? 128 : 256;
   static constexpr int THREADS = NL * CH;
   static constexpr int BPS = S.bps;
-  static constexpr int DELTA = (AX == 0) ? 1 : NL;           // lane distance between slots i and i+1
+  static constexpr int DELTA = LM ? 1 : NL;                   // lane distance between slots i and i+1
   static constexpr int SLOTS_PER_WARP = 32 / DELTA;           // consecutive slots inside one warp
   static constexpr int NEDGE = CH / SLOTS_PER_WARP;           // warp-edge slots per line
   static constexpr int VP = NL * RING;                        // variable stride, primitive ring
@@ -103,9 +121,9 @@ struct Geo {
   // x sweep with one warp per line: every exchange of the march (ring, edges, flags, loads) stays
   // inside the warp, so the chunk barriers are warp barriers and the warps run decoupled
   // (likewise any one-warp CTA, e.g. y/z: 8 lines x 4 cells)
-  static constexpr bool WARP_LOCAL = (AX == 0 && CH == 32) || THREADS == 32;
+  static constexpr bool WARP_LOCAL = (LM && CH == 32) || THREADS == 32;
   static_assert(is_pow2(NL) && is_pow2(CH), "NL and CH must be powers of two");
-  static_assert(CH >= 4 && THREADS <= 1024 && THREADS >= 32 && (AX == 0 ? CH >= 32 : NL <= 32),
+  static_assert(CH >= 4 && THREADS <= 1024 && THREADS >= 32 && (LM ? CH >= 32 : NL <= 32),
                 "unsupported line geometry");
   static_assert(AX != 0 || NL * CH <= 1024, "x geometry");
   // a ring position of cell/face x (x may be negative)
@@ -135,7 +153,7 @@ ECHO_HD int wrapf(int p) {
 
 template <int AX, int LEN>
 ECHO_HD int loff(int t, int pos) {  // conflict-free: slot/position fastest for x, line fastest for y/z
-  return AX == 0 ? t * LEN + pos : pos * Geo<AX>::NL + t;
+  return Geo<AX>::LM ? t * LEN + pos : pos * Geo<AX>::NL + t;
 }
 
 ECHO_HD int first_axis(int comp) { return comp == 0 ? 1 : 0; }
@@ -225,7 +243,7 @@ ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int 
   using GE = Geo<AX>;
   int t0, zz;
   unit_origin<AX>(lg, unit, t0, zz);
-  const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
+  const bool vec = !GE::LM && lg.vec16 && (t0 + GE::NL <= lg.nt);
   if (vec && (t & 1)) return;
   const long long lb = line_base<AX>(g, lg, t0, zz, t);
 #pragma unroll
@@ -244,13 +262,13 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
   constexpr bool UCT = DM == 2;
   constexpr int CH = GE::CH, RING = GE::RING, RINGF = GE::RINGF, RR = GE::RR;
   // A31 flags as ballots: warp-local kernels whose chunk of a line lies in one warp
-  constexpr bool kBallot = ECHO_BALLOT_FLAGS && GE::WARP_LOCAL && (AX == 0 ? CH == 32 : CH * GE::NL == 32);
+  constexpr bool kBallot = ECHO_BALLOT_FLAGS && GE::WARP_LOCAL && (GE::LM ? CH == 32 : CH * GE::NL == 32);
   extern __shared__ double smem[];
   unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RR] face flags
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const int tid = threadIdx.x;
-  const int t = (AX == 0) ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));  // line in the group
-  const int i = (AX == 0) ? (tid & (CH - 1)) : (tid >> GE::LOG_NL);      // slot along the line
+  const int t = GE::LM ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));  // line in the group
+  const int i = GE::LM ? (tid & (CH - 1)) : (tid >> GE::LOG_NL);      // slot along the line
   const bool edge_in = (i % GE::SLOTS_PER_WARP) == 0;                            // left neighbour in another warp/chunk
   const bool edge_out = (i % GE::SLOTS_PER_WARP) == GE::SLOTS_PER_WARP - 1;       // right neighbour in another warp/chunk
   const int eslot_out = ((i + 1) & (CH - 1)) / GE::SLOTS_PER_WARP;               // edge slot this thread publishes
@@ -269,7 +287,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
     const long long lb = line_base<AX>(g, lg, t0, zz, t);
     const long long as = axis_stride<AX>(g);
     const int tt = min(t0 + t, lg.nt - 1);
-    const bool vec = (AX != 0) && lg.vec16 && (t0 + GE::NL <= lg.nt);
+    const bool vec = !GE::LM && lg.vec16 && (t0 + GE::NL <= lg.nt);
     unsigned long long fhist = 0ull;  // A31 flags of this line's faces, newest chunk in the top CH bits
     int rb = GE::ring(GE::B_FIRST);  // primitive-ring position of the chunk base B
     int rbf = ringf<AX>(GE::B_FIRST);  // face-flux-ring position of B
@@ -308,7 +326,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       // inactive lanes' values are shuffled but never used; the x sweep zero-fills them all the
       // same (without it ptxas spills at 80 registers), the y/z sweeps skip the fill
       if (!(ab && B + 3 + i >= -3)) {  // the prologue needs cells -3..2 only
-        if constexpr (AX == 0) {
+        if constexpr (GE::LM) {
 #pragma unroll
           for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
         }
@@ -342,7 +360,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       unsigned fm = 0u;  // this chunk's CH flags of line t
       if constexpr (kBallot) {
         const unsigned b = __ballot_sync(0xffffffffu, rgh);
-        if constexpr (AX == 0) {
+        if constexpr (GE::LM) {
           fm = b;  // lane = slot
         } else if constexpr (GE::NL == 8 && CH == 4) {
           fm = (((b >> t) & 0x01010101u) * 0x10204080u) >> 28;  // lanes i*8 + t, i = 0..3
@@ -376,7 +394,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 #pragma unroll
           for (int q = 0; q < 7; q++) smem[GE::OFF_HE + dpar * 7 * GE::VE + q * GE::VE + eslot_out * GE::NL + t] = H[q];
         }
-      } else if constexpr (AX == 0) {
+      } else if constexpr (GE::LM) {
 #pragma unroll
         for (int q = 0; q < 7; q++) H[q] = 0.0;
       }
