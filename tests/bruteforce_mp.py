@@ -391,3 +391,150 @@ class Scheme:
                 j, k = (i + 1) % 3, (i + 2) % 3
                 L[5 + i] = -(om(j, 1, k) - om(j, -1, k)) / (2 * G.d(j)) + (om(k, 1, j) - om(k, -1, j)) / (2 * G.d(k))
         return L
+
+
+# ------------------------------------------------------------- UCT (divb = 2)
+class SchemeUCT(Scheme):
+    """UCT (readings A37-A43) written out from the readings: the staggered field
+    b^a = sqrt(gamma) B^a at the face cell[a]+1/2, face data (V = alpha v - beta of both HLL
+    states, a+ = max(0, lam+_L, lam+_R), a- = max(0, -lam-_L, -lam-_R)), the four-state
+    UCT-HLL edge EMF with quadrant velocities averaged over the two double reconstructions,
+    and L(b^p) = -d_q Dh E^c + d_c Dh E^q with (c, p, q) cyclic.  The hydro rhs is the
+    base scheme's with the normal field of every face taken from b."""
+
+    def __init__(self, G: Grid, U8, P5, b3):
+        super().__init__(G, U8, P5)
+        self.b3 = b3
+        self._fd = {}
+        self._E = {}
+
+    def wrapc(self, cell):
+        return [self.G.wrap(a, cell[a]) for a in range(3)]
+
+    def b(self, a, cell):  # b^a at the face cell[a]+1/2
+        i, j, k = self.wrapc(cell)
+        return mp.mpf(float(self.b3[a, k, j, i]))
+
+    def face_flux(self, ax, cell):
+        key = (ax, tuple(cell))
+        if key in self._face:
+            return self._face[key]
+        G = self.G
+        st = []
+        for mm in range(6):
+            cc = list(cell)
+            cc[ax] = cell[ax] - 2 + mm
+            st.append(self.prim(*cc))
+        qL = [rec_left([st[mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        qR = [rec_left([st[5 - mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        if not qL[0] > 0:
+            qL[0] = st[2][0]
+        if not qL[4] > 0:
+            qL[4] = st[2][4]
+        if not qR[0] > 0:
+            qR[0] = st[3][0]
+        if not qR[4] > 0:
+            qR[4] = st[3][4]
+        x = [G.centre(b, cell[b]) for b in range(3)]
+        x[ax] = G.face(ax, cell[ax])
+        m = Met(G, x)
+        qL[5 + ax] = qR[5 + ax] = self.b(ax, cell) / m.sqrtg
+        F = hll(m, G.gamma, qL, qR, ax)
+        aL, aR = aux(m, G.gamma, qL), aux(m, G.gamma, qR)
+        lmL, lpL = speeds(m, G.gamma, qL, ax)
+        lmR, lpR = speeds(m, G.gamma, qR, ax)
+        VL = [m.alpha * aL["v"][i] - m.beta[i] for i in range(3)]
+        VR = [m.alpha * aR["v"][i] - m.beta[i] for i in range(3)]
+        if list(cell) == self.wrapc(cell):  # face data of owned faces only (A42: ghosts = nearest owned)
+            self._fd[(ax, tuple(cell))] = (VL, VR, max(0, lpL, lpR), max(0, -lmL, -lmR))
+        a, bb = st[2], st[3]
+        dj = G.der_jump
+        rough = dj > 0 and (abs(bb[0] - a[0]) > dj * min(a[0], bb[0]) or abs(bb[4] - a[4]) > dj * min(a[4], bb[4]))
+        self._face[key] = (F, rough)
+        return self._face[key]
+
+    def fd(self, ax, cell):
+        key = (ax, tuple(self.wrapc(cell)))
+        if key not in self._fd:
+            w = self.wrapc(cell)
+            self._face.pop((ax, tuple(w)), None)
+            self.face_flux(ax, w)
+        return self._fd[key]
+
+    def emf(self, c, cell):
+        """E^c at the edge (cell[p]+1/2, cell[q]+1/2, cell[c]), p = c+1, q = c+2; a ghost edge
+        is the nearest owned one (A42: the cell ghost rule applied to the edge's cell)"""
+        cell = self.wrapc(cell)
+        key = (c, tuple(cell))
+        if key in self._E:
+            return self._E[key]
+        G = self.G
+        p, q = (c + 1) % 3, (c + 2) % 3
+
+        def at(ax, d):
+            cc = list(cell)
+            cc[ax] += d
+            return cc
+
+        def pair(samples):  # one-sided values at +1/2 from samples at -2..3
+            return rec_left(samples[0:5], G.rec), rec_left(samples[5:0:-1], G.rec)
+
+        # p-faces: W = left state, E = right state, reconstructed along q -> (S, N)
+        Wst = {}
+        for side in (0, 1):
+            for comp in (p, q):
+                s = [self.fd(p, at(q, mm - 2))[side][comp] for mm in range(6)]
+                Wst[(side, comp)] = pair(s)
+        # q-faces: S = left state, N = right state, reconstructed along p -> (W, E)
+        Sst = {}
+        for side in (0, 1):
+            for comp in (p, q):
+                s = [self.fd(q, at(p, mm - 2))[side][comp] for mm in range(6)]
+                Sst[(side, comp)] = pair(s)
+        bpS, bpN = pair([self.b(p, at(q, mm - 2)) for mm in range(6)])
+        bqW, bqE = pair([self.b(q, at(p, mm - 2)) for mm in range(6)])
+        app = max(self.fd(p, cell)[2], self.fd(p, at(q, 1))[2])
+        apm = max(self.fd(p, cell)[3], self.fd(p, at(q, 1))[3])
+        aqp = max(self.fd(q, cell)[2], self.fd(q, at(p, 1))[2])
+        aqm = max(self.fd(q, cell)[3], self.fd(q, at(p, 1))[3])
+
+        def vel(we, sn, comp):  # quadrant (we: 0 W / 1 E, sn: 0 S / 1 N)
+            return (Wst[(we, comp)][sn] + Sst[(sn, comp)][we]) / 2
+
+        def equad(we, sn):
+            bp = bpN if sn else bpS
+            bq = bqE if we else bqW
+            return vel(we, sn, q) * bp - vel(we, sn, p) * bq
+
+        sp, sq = app + apm, aqp + aqm
+        if sp > 0 and sq > 0:
+            E = ((app * aqp * equad(0, 0) + app * aqm * equad(0, 1) + apm * aqp * equad(1, 0) + apm * aqm * equad(1, 1))
+                 / (sp * sq) + app * apm * (bqE - bqW) / sp - aqp * aqm * (bpN - bpS) / sq)
+        else:
+            E = (equad(0, 0) + equad(0, 1) + equad(1, 0) + equad(1, 1)) / 4
+        self._E[key] = E
+        return E
+
+    def rhs_cell(self, cell):
+        G = self.G
+        L, _ = self.axes(cell)
+        x = [G.centre(b, cell[b]) for b in range(3)]
+        if G.metric != 0:
+            m = Met(G, x, derivs=True)
+            s = sources(m, G.gamma, self.prim(*cell))
+            for q in range(1, 5):
+                L[q] += m.sqrtg * s[q]
+
+        def Dh(c, ax, base, shift):
+            vals = []
+            for mm in range(5):
+                cc = list(base)
+                cc[ax] += mm - 2 + shift
+                vals.append(self.emf(c, cc))
+            return derf(vals, G.der)
+
+        for p in range(3):
+            c, q = (p + 2) % 3, (p + 1) % 3
+            L[5 + p] = (-(Dh(c, q, cell, 0) - Dh(c, q, cell, -1)) / G.d(q)
+                        + (Dh(q, c, cell, 0) - Dh(q, c, cell, -1)) / G.d(c))
+        return L

@@ -75,3 +75,47 @@ def test_bruteforce_kerr_schild_patch(orc):
     c = orc.Cfg(**{**p.grid_kwargs(), "lo": lo, "hi": hi, "bc": bc})
     G = B.Grid(n, lo, hi, bc, metric=1, M=1, a=0.9)
     _compare(orc, c, G, P8, tol=1e-12)
+
+
+def _compare_uct(orc, c, G, P8, b3, tol=1e-13):
+    U, P, b = orc.set_prims_uct(c, np.ascontiguousarray(P8), np.ascontiguousarray(b3))
+    L = orc.rhs_uct(c, U, P, b)
+    S = B.SchemeUCT(G, U, P, b)
+    n = c.n
+    Lmp = np.zeros_like(L)
+    for k in range(n[2]):
+        for j in range(n[1]):
+            for i in range(n[0]):
+                Lmp[:, k, j, i] = [float(v) for v in S.rhs_cell([i, j, k])]
+    errs = group_errors(L, Lmp, {"D": [0], "S": [1, 2, 3], "tau": [4], "b": [5, 6, 7]})
+    assert all(e <= tol for e in errs.values()), errs
+    return errs
+
+
+@pytest.mark.parametrize("rec", [0, 2])
+def test_bruteforce_uct_periodic(orc, rec):
+    # f2 / A37-A41: the oracle's UCT rhs (hydro with staggered normal fields + L(b) from the
+    # edge EMFs) against the independent mpmath transcription in bruteforce_mp.SchemeUCT
+    p = I.problem(0, n=(4, 4, 4), seed=13)
+    p.params.update(amp=0.2, vmax=0.5)
+    p.divb, p.rec = 2, rec
+    c = orc.Cfg(**p.grid_kwargs())
+    G = B.Grid(p.n, p.lo, p.hi, p.bc, divb=2, rec=rec)
+    _compare_uct(orc, c, G, I.initial_prims(p), I.face_field(p))
+
+
+def test_bruteforce_uct_outflow_and_kerr_schild(orc):
+    # A42 ghost rule on outflow sides, A43 transport velocity and face metric (a = 0.9 patch)
+    n = (4, 4, 4)
+    lo = (math.log(9.0), 1.3, 0.0)
+    hi = (math.log(11.0), 1.8, 0.4)
+    bc = ((1, 1), (1, 1), (0, 0))
+    p = I.problem(4, n=n)
+    p.lo, p.hi = lo, hi
+    P8 = I.initial_prims(p)
+    b3 = np.ascontiguousarray(np.stack([2e-1 * (1 + 0.3 * I.white_noise(17, 64).reshape(4, 4, 4)),
+                                        3e-1 * (1 + 0.3 * I.white_noise(18, 64).reshape(4, 4, 4)),
+                                        np.full((4, 4, 4), 0.1)]))
+    c = orc.Cfg(**{**p.grid_kwargs(), "lo": lo, "hi": hi, "bc": bc, "divb": 2})
+    G = B.Grid(n, lo, hi, bc, metric=1, M=1, a=0.9, divb=2)
+    _compare_uct(orc, c, G, P8, b3, tol=1e-12)
