@@ -40,6 +40,34 @@ ECHO_D void rec_pair(const double f[6], double& lo, double& hi) {
   rec_both<REC>(f[1], f[2], f[3], f[4], f[5], dead1, hi);
 }
 
+// A38 quadrant velocities (V^p, V^q) = the mean of the two double reconstructions, A39
+// quadrant EMFs E = V^q b^p - V^p b^q and the UCT-HLL combination.  pS/pN[side][k]: the p-face
+// state side (0 W, 1 E) component k (0 p, 1 q) at the edge from below / above along q;
+// qW/qE[side][k]: the q-face state side (0 S, 1 N) from the W / E side along p.
+ECHO_D double emf_combine(const double pS[2][2], const double pN[2][2], const double qW[2][2], const double qE[2][2],
+                          double bpS, double bpN, double bqW, double bqE, double app, double apm, double aqp,
+                          double aqm) {
+  double v[4][2];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    v[0][k] = 0.5 * (pS[0][k] + qW[0][k]);  // WS
+    v[1][k] = 0.5 * (pN[0][k] + qW[1][k]);  // WN
+    v[2][k] = 0.5 * (pS[1][k] + qE[0][k]);  // ES
+    v[3][k] = 0.5 * (pN[1][k] + qE[1][k]);  // EN
+  }
+  const double EWS = v[0][1] * bpS - v[0][0] * bqW;
+  const double EWN = v[1][1] * bpN - v[1][0] * bqW;
+  const double EES = v[2][1] * bpS - v[2][0] * bqE;
+  const double EEN = v[3][1] * bpN - v[3][0] * bqE;
+  const double sp = app + apm, sq = aqp + aqm;
+  if (sp > 0.0 && sq > 0.0) {
+    const double isp = 1.0 / sp, isq = 1.0 / sq;
+    return (app * (aqp * EWS + aqm * EWN) + apm * (aqp * EES + aqm * EEN)) * (isp * isq) +
+           app * apm * (bqE - bqW) * isp - aqp * aqm * (bpN - bpS) * isq;
+  }
+  return 0.25 * (EWS + EWN + EES + EEN);  // unreachable for p > 0 (A4): central average
+}
+
 // E^CC at the edge owned by cell x (one component per thread: the three are independent,
 // and a thread holding all three needs ~170 registers, one CTA per SM)
 template <int REC, int CC>
@@ -80,45 +108,124 @@ ECHO_D double uct_emf_one(const GridP& g, const double* const FS[3], const doubl
   const double apm = fmax(__ldg(FS[p] + rb + 7 * vs), __ldg(FS[p] + oq[3] + 7 * vs));
   const double aqp = fmax(__ldg(FS[q] + rb + 6 * vs), __ldg(FS[q] + op[3] + 6 * vs));
   const double aqm = fmax(__ldg(FS[q] + rb + 7 * vs), __ldg(FS[q] + op[3] + 7 * vs));
-  // A38 quadrant velocities (v^p, v^q), A39 quadrant EMFs E = v^q B^p - v^p B^q
-  double v[4][2];
-#pragma unroll
-  for (int k = 0; k < 2; k++) {
-    v[0][k] = 0.5 * (pS[0][k] + qW[0][k]);  // WS
-    v[1][k] = 0.5 * (pN[0][k] + qW[1][k]);  // WN
-    v[2][k] = 0.5 * (pS[1][k] + qE[0][k]);  // ES
-    v[3][k] = 0.5 * (pN[1][k] + qE[1][k]);  // EN
-  }
-  const double EWS = v[0][1] * bpS - v[0][0] * bqW;
-  const double EWN = v[1][1] * bpN - v[1][0] * bqW;
-  const double EES = v[2][1] * bpS - v[2][0] * bqE;
-  const double EEN = v[3][1] * bpN - v[3][0] * bqE;
-  const double sp = app + apm, sq = aqp + aqm;
-  if (sp > 0.0 && sq > 0.0) {
-    const double isp = 1.0 / sp, isq = 1.0 / sq;
-    return (app * (aqp * EWS + aqm * EWN) + apm * (aqp * EES + aqm * EEN)) * (isp * isq) +
-           app * apm * (bqE - bqW) * isp - aqp * aqm * (bpN - bpS) * isq;
-  }
-  return 0.25 * (EWS + EWN + EES + EEN);  // unreachable for p > 0 (A4): central average
+  return emf_combine(pS, pN, qW, qE, bpS, bpN, bqW, bqE, app, apm, aqp, aqm);
 }
 
 // grid (cells / kCellThreads, 3): blockIdx.y = the EMF component
 template <int REC>
 __global__ void __launch_bounds__(kCellThreads)
 k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restrict__ FSy,
-          const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed) {
+          const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed, int cc0) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= g.N) return;
   int x[3];
   cell_ijk(g, id, x[0], x[1], x[2]);
   const double* FS[3] = {FSx, FSy, FSz};
   const long long rb = rec_base(g, x[0], x[1], x[2]);
-  const int cc = blockIdx.y;
+  const int cc = blockIdx.y + cc0;
   double E;
   if (cc == 0) E = uct_emf_one<REC, 0>(g, FS, Bin, x, rb);
   else if (cc == 1) E = uct_emf_one<REC, 1>(g, FS, Bin, x, rb);
   else E = uct_emf_one<REC, 2>(g, FS, Bin, x, rb);
   Ed[rb + cc * g.vs] = E;
+}
+
+// E^x (CC = 0: q = z) and E^y (CC = 1: p = z) marching along z: one thread per (i, j)
+// column and z segment keeps the samples along z of the face data and b that these two
+// components reconstruct along z in 6-entry register windows (one new load per stream and
+// step instead of six from planes far apart); the in-plane samples (z-face data and b^z along
+// y or x) are loaded per step.  Same arithmetic as uct_emf_one.
+constexpr int kZSeg = 16;  // planes per thread
+#ifndef ECHO_EMF_ZM_BPS
+#define ECHO_EMF_ZM_BPS 3
+#endif
+template <int REC, int CC>
+__global__ void __launch_bounds__(128, ECHO_EMF_ZM_BPS)
+k_uct_emf_zm(const GridP g, const double* __restrict__ FSx, const double* __restrict__ FSy,
+             const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed) {
+  constexpr int p = (CC + 1) % 3, q = (CC + 2) % 3;
+  constexpr bool ZQ = (q == 2);   // CC 0: z is q; CC 1: z is p
+  constexpr int ip = ZQ ? p : q;  // the in-plane direction of the other pairs (y for CC 0, x for CC 1)
+  const double* __restrict__ Fz = (CC == 0) ? FSy : FSx;  // face data reconstructed along z
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= g.n[0]) return;
+  const int k0 = blockIdx.z * kZSeg;
+  const int k1 = min(k0 + kZSeg, g.n[2]);
+  const long long vs = g.vs;
+  // along-z windows: 4 face-data streams (slot 3 side + comp), b (slot bz), speeds (slots 6, 7) at k, k+1
+  const int comp[2] = {p, q};
+  const int bz = ZQ ? p : q;
+  double wv[4][6], wb[6], ws[2][2];
+  {
+    int x[3] = {i, j, k0};
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+      const long long o = rec_shift(g, x, 2, m - 2);
+#pragma unroll
+      for (int s2 = 0; s2 < 4; s2++) wv[s2][m] = __ldg(Fz + o + (3 * (s2 >> 1) + comp[s2 & 1]) * vs);
+      wb[m] = __ldg(Bin + o + bz * vs);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const long long o = rec_shift(g, x, 2, h);
+      ws[0][h] = __ldg(Fz + o + 6 * vs);
+      ws[1][h] = __ldg(Fz + o + 7 * vs);
+    }
+  }
+  for (int k = k0; k < k1; k++) {
+    const int x[3] = {i, j, k};
+    const long long rb = rec_base(g, i, j, k);
+    // pairs along z from the windows
+    double zlo[2][2], zhi[2][2];
+#pragma unroll
+    for (int s2 = 0; s2 < 4; s2++) rec_pair<REC>(wv[s2], zlo[s2 >> 1][s2 & 1], zhi[s2 >> 1][s2 & 1]);
+    double bzlo, bzhi;
+    rec_pair<REC>(wb, bzlo, bzhi);
+    const double az_p = fmax(ws[0][0], ws[0][1]), az_m = fmax(ws[1][0], ws[1][1]);
+    // in-plane pairs: z-face data and b^z along ip
+    long long oi[6];
+#pragma unroll
+    for (int m = 0; m < 6; m++) oi[m] = rec_shift(g, x, ip, m - 2);
+    double ilo[2][2], ihi[2][2], f[6];
+#pragma unroll
+    for (int side = 0; side < 2; side++)
+#pragma unroll
+      for (int kk = 0; kk < 2; kk++) {
+#pragma unroll
+        for (int m = 0; m < 6; m++) f[m] = __ldg(FSz + oi[m] + (3 * side + comp[kk]) * vs);
+        rec_pair<REC>(f, ilo[side][kk], ihi[side][kk]);
+      }
+    double bilo, bihi;
+#pragma unroll
+    for (int m = 0; m < 6; m++) f[m] = __ldg(Bin + oi[m] + 2 * vs);
+    rec_pair<REC>(f, bilo, bihi);
+    const double ai_p = fmax(__ldg(FSz + rb + 6 * vs), __ldg(FSz + oi[3] + 6 * vs));
+    const double ai_m = fmax(__ldg(FSz + rb + 7 * vs), __ldg(FSz + oi[3] + 7 * vs));
+    double E;
+    if constexpr (ZQ)  // z-pairs: p-face (y-face) states along q = z; in-plane: q-face (z-face) states along p = y
+      E = emf_combine(zlo, zhi, ilo, ihi, bzlo, bzhi, bilo, bihi, az_p, az_m, ai_p, ai_m);
+    else               // z-pairs: q-face (x-face) states along p = z; in-plane: p-face (z-face) states along q = x
+      E = emf_combine(ilo, ihi, zlo, zhi, bilo, bihi, bzlo, bzhi, ai_p, ai_m, az_p, az_m);
+    Ed[rb + CC * vs] = E;
+    if (k + 1 < k1) {  // slide the windows by one plane
+      const long long o = rec_shift(g, x, 2, 4);
+#pragma unroll
+      for (int s2 = 0; s2 < 4; s2++) {
+#pragma unroll
+        for (int m = 0; m < 5; m++) wv[s2][m] = wv[s2][m + 1];
+        wv[s2][5] = __ldg(Fz + o + (3 * (s2 >> 1) + comp[s2 & 1]) * vs);
+      }
+#pragma unroll
+      for (int m = 0; m < 5; m++) wb[m] = wb[m + 1];
+      wb[5] = __ldg(Bin + o + bz * vs);
+      const long long o2 = rec_shift(g, x, 2, 2);
+      ws[0][0] = ws[0][1];
+      ws[1][0] = ws[1][1];
+      ws[0][1] = __ldg(Fz + o2 + 6 * vs);
+      ws[1][1] = __ldg(Fz + o2 + 7 * vs);
+    }
+  }
 }
 
 // A41 induction of the three faces owned by a cell; MODE 0: RK stage s into Bst (dt from
@@ -280,10 +387,21 @@ k_uct_centre_p2c(const GridP g, const EosP e, const MetTables mt, double* __rest
   if (KS) st8(P + rb, vs, pr);
 }
 
+#ifndef ECHO_EMF_ZMARCH
+#define ECHO_EMF_ZMARCH 1
+#endif
 template <int REC>
 cudaError_t emf_rec(const GridP& g, const double* const FS[3], const double* Bin, double* Ed, cudaStream_t st) {
-  const dim3 blocks((unsigned)((g.N + kCellThreads - 1) / kCellThreads), 3);
-  k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
+  if (ECHO_EMF_ZMARCH) {  // E^x, E^y marching along z; E^z one thread per edge
+    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSeg - 1) / kZSeg));
+    k_uct_emf_zm<REC, 0><<<zb, 128, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
+    k_uct_emf_zm<REC, 1><<<zb, 128, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
+    const dim3 blocks((unsigned)((g.N + kCellThreads - 1) / kCellThreads), 1);
+    k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed, 2);
+  } else {
+    const dim3 blocks((unsigned)((g.N + kCellThreads - 1) / kCellThreads), 3);
+    k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed, 0);
+  }
   return cudaGetLastError();
 }
 
