@@ -37,6 +37,9 @@ namespace march {
 // Line-group geometry per sweep axis: NL lines x CH cells per chunk
 // (THREADS = NL CH), BPS CTAs per SM.  Overridable at build time for tuning
 // runs (-DECHO_YZ_NL=8 -DECHO_YZ_CH=32 -DECHO_YZ_BPS=2, likewise ECHO_X_*).
+#ifndef ECHO_PDL
+#define ECHO_PDL 0  // programmatic dependent launch of the y and z sweeps (-DECHO_PDL=1; no gain measured)
+#endif
 #ifndef ECHO_BALLOT_FLAGS
 #define ECHO_BALLOT_FLAGS 1  // A31 flags as warp ballots + a per-line bit history (warp-local kernels)
 #endif
@@ -276,6 +279,11 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
   const double idxa = g.idx[AX];
   const long long vs = g.vs;
 
+  // programmatic dependent launch (ECHO_PDL): the next sweep's CTAs may start as this grid's
+  // CTAs retire, and run their first chunks (which read only P and U) over its tail; a y/z
+  // sweep waits for the previous sweep's grid before its first access to R
+  if constexpr (ECHO_PDL && AX != 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  bool dep_waited = !(ECHO_PDL && AX != 0);
   long long unit = blockIdx.x;
   if (unit < lg.nunits) load_window<AX>(g, lg, unit, t, i, P, UB, sbase);
   cp_async_commit();
@@ -305,6 +313,10 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
       if constexpr (GE::WARP_LOCAL) __syncwarp();
       else __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
       if (AX != 0 && d2) {  // old rhs/EMF values of the output cells (accumulated in D)
+        if (!dep_waited) {  // the previous sweep's R (uniform: every thread reaches it at the same chunk)
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          dep_waited = true;
+        }
         if (!(vec && (t & 1))) {
           const int a = min(X0 + i, lg.na - 1) + lg.coff;
           const double* src = R + lb + a * as;
@@ -529,6 +541,19 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
   lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
   lg.nunits = (long long)lg.tt_groups * lg.nz;
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
+  if (ECHO_PDL && AX != 0) {  // y/z: may start over the previous sweep's tail (griddepcontrol)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(GE::THREADS);
+    cfg.dynamicSmemBytes = GE::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, g, e, mt, lg, P, UB, R, Bface, FSo);
+  }
   kern<<<blocks, GE::THREADS, GE::SMEM, st>>>(g, e, mt, lg, P, UB, R, Bface, FSo);
   return cudaGetLastError();
 }
