@@ -486,7 +486,7 @@ def main(argv=None):
                     help="divergence treatment: 0 field-CD (default, the benchmarked scheme), 1 none, 2 UCT")
     ap.add_argument("--n", type=int, nargs=3, default=None, help="override the grid (not a bench value)")
     ap.add_argument("--ref-n", type=int, default=64)
-    ap.add_argument("--cpu-n", type=int, default=64)
+    ap.add_argument("--cpu-n", type=int, default=96)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args(argv)
