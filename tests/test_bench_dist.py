@@ -45,14 +45,18 @@ def test_max_over_ranks_gloo():
         assert dict(out) == {0: 2.0, 1: 2.0}
 
 
-def test_reference_arm_cli_runs_on_cpu():
-    # --impl reference times the oracle (the reference arm of this tier) and prints one JSON line
+@pytest.mark.parametrize("extra", [[], ["--divb", "2"], ["--rec", "2"]])
+def test_reference_arm_cli_runs_on_cpu(extra):
+    # --impl reference times the oracle (the reference arm of this tier) and prints one JSON line;
+    # the UCT (--divb 2) and reconstruction switches reach the oracle too
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
-                        "--ref-n", "16"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+                        "--ref-n", "16", *extra], cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+    if extra[:2] == ["--divb", "2"]:
+        assert "UCT" in d["config"]["workload"]
 
 
 def test_reference_arm_other_ranks_exit_quietly():
