@@ -313,10 +313,14 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
     } else {
       Z0 = P[rb + kSlotZ * vs];  // the stored Newton guess
     }
+    // the centred new field first (its 18 neighbour loads overlap the hydro loads below)
+    double Bc[3];
+    centre_field(g, Bst, s == 3 ? 0 : 3, x, Bc);  // the field this stage just wrote
 #pragma unroll
     for (int q = 0; q < 5; q++) L[q] = R[rb + q * vs];
     if constexpr (KS) add_sources(m, der_rec(mt, x[0], x[1]), e, Pp, L);  // a6
-    ld8(Un + rb, vs, Uo);
+#pragma unroll
+    for (int q = 0; q < 5; q++) Uo[q] = Un[rb + q * vs];  // hydro only: U_B comes from b
     if (s == 1) {
 #pragma unroll
       for (int q = 0; q < 5; q++) Uo[q] = Uo[q] + dt * L[q];
@@ -325,8 +329,6 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
 #pragma unroll
       for (int q = 0; q < 5; q++) Uo[q] = c0 * Uo[q] + c1 * (Us[rb + q * vs] + dt * L[q]);
     }
-    double Bc[3];
-    centre_field(g, Bst, s == 3 ? 0 : 3, x, Bc);  // the field this stage just wrote
 #pragma unroll
     for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a];
     double Po[8];
