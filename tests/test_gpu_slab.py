@@ -77,6 +77,8 @@ def test_slab_api_errors(E):
         g.step(1e-3)  # a slab needs an exchange before every stage
     assert ei.value.code == E.E_ORDER
     with pytest.raises(E.EchoError):
+        g.advance(1, 0.4)  # so does the device-driven loop
+    with pytest.raises(E.EchoError):
         E.halo_fill(g.ctx, 0)  # a halo side is imported, not filled
     with pytest.raises(E.EchoError):
         E.create(n=(8, 8, 4), lo=(0, 0, 0), hi=(1, 1, 1), bc=((0, 0), (0, 0), (2, 2)))  # thinner than the halo
