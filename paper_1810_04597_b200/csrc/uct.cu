@@ -276,6 +276,79 @@ k_uct_induct(const GridP g, int mode, int s, double dt, const double* dtp, const
   }
 }
 
+// The same induction marching along z: one thread per (i, j) column and kZSeg planes keeps
+// the two along-z EMF streams (E^y for b^x, E^x for b^y) in 6-entry register windows.
+template <int DER>
+__global__ void __launch_bounds__(128)
+k_uct_induct_zm(const GridP g, int mode, int s, double dt, const double* dtp, const double* __restrict__ Ed,
+                double* Bst, double* __restrict__ Lout) {
+  if (dtp) {
+    if (dtp[1] != 0.0) return;
+    dt = dtp[0];
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= g.n[0]) return;
+  const int k0 = blockIdx.z * kZSeg;
+  const int k1 = min(k0 + kZSeg, g.n[2]);
+  const long long vs = g.vs;
+  double wy[6], wx[6];  // E^y and E^x at (i, j, k-3 .. k+2)
+  {
+    const int x[3] = {i, j, k0};
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+      const long long o = rec_shift(g, x, 2, m - 3);
+      wy[m] = __ldg(Ed + o + 1 * vs);
+      wx[m] = __ldg(Ed + o + 0 * vs);
+    }
+  }
+  for (int k = k0; k < k1; k++) {
+    const int x[3] = {i, j, k};
+    const long long rb = rec_base(g, i, j, k);
+    const long long id = ((long long)k * g.n[1] + j) * g.n[0] + i;
+    double Lb[3];
+#pragma unroll
+    for (int p = 0; p < 3; p++) {
+      const int cc = (p + 2) % 3, q = (p + 1) % 3;
+      double Eq[6], Ec[6];  // E^cc along q, E^q along cc: samples -3..2
+#pragma unroll
+      for (int m = 0; m < 6; m++) {
+        if (q == 2) Eq[m] = wx[m];  // p = y: E^x along z
+        else Eq[m] = __ldg(Ed + rec_shift(g, x, q, m - 3) + cc * vs);
+        if (cc == 2) Ec[m] = wy[m];  // p = x: E^y along z
+        else Ec[m] = __ldg(Ed + rec_shift(g, x, cc, m - 3) + q * vs);
+      }
+      Lb[p] = -(der5<DER>(Eq[1], Eq[2], Eq[3], Eq[4], Eq[5]) - der5<DER>(Eq[0], Eq[1], Eq[2], Eq[3], Eq[4])) * g.idx[q] +
+              (der5<DER>(Ec[1], Ec[2], Ec[3], Ec[4], Ec[5]) - der5<DER>(Ec[0], Ec[1], Ec[2], Ec[3], Ec[4])) * g.idx[cc];
+    }
+#pragma unroll
+    for (int p = 0; p < 3; p++) {
+      if (mode == 1) {
+        Lout[(5 + p) * g.N + id] = Lb[p];
+        continue;
+      }
+      const double bn = Bst[rb + p * vs];
+      if (s == 1) {
+        Bst[rb + (3 + p) * vs] = bn + dt * Lb[p];
+      } else if (s == 2) {
+        Bst[rb + (3 + p) * vs] = 0.75 * bn + 0.25 * (Bst[rb + (3 + p) * vs] + dt * Lb[p]);
+      } else {
+        Bst[rb + p * vs] = (1.0 / 3.0) * bn + (2.0 / 3.0) * (Bst[rb + (3 + p) * vs] + dt * Lb[p]);
+      }
+    }
+    if (k + 1 < k1) {  // slide: the next plane's window ends at k + 3
+      const long long o = rec_shift(g, x, 2, 3);
+#pragma unroll
+      for (int m = 0; m < 5; m++) {
+        wy[m] = wy[m + 1];
+        wx[m] = wx[m + 1];
+      }
+      wy[5] = __ldg(Ed + o + 1 * vs);
+      wx[5] = __ldg(Ed + o + 0 * vs);
+    }
+  }
+}
+
 // A37: I6 of the face field at slot offset `slot` of Bst, per component, at cell x
 ECHO_D void centre_field(const GridP& g, const double* __restrict__ Bst, int slot, const int x[3], double Bc[3]) {
   const long long vs = g.vs;
@@ -420,8 +493,18 @@ cudaError_t launch_uct_emf(const GridP& g, const double* const FS[3], const doub
   }
 }
 
+#ifndef ECHO_INDUCT_ZMARCH
+#define ECHO_INDUCT_ZMARCH 1
+#endif
 cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const double* dtp, const double* Ed,
                               double* Bst, double* Lout, cudaStream_t st) {
+  if (ECHO_INDUCT_ZMARCH) {
+    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSeg - 1) / kZSeg));
+    if (g.der == 4) k_uct_induct_zm<4><<<zb, 128, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
+    else if (g.der == 2) k_uct_induct_zm<2><<<zb, 128, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
+    else k_uct_induct_zm<6><<<zb, 128, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
+    return cudaGetLastError();
+  }
   const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
   if (g.der == 4) k_uct_induct<4><<<blocks, kCellThreads, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
   else if (g.der == 2) k_uct_induct<2><<<blocks, kCellThreads, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
