@@ -361,6 +361,75 @@ ECHO_D void centre_field(const GridP& g, const double* __restrict__ Bst, int slo
   }
 }
 
+// one cell of the UCT update (Bc = I6 of the field this stage wrote): hydro RK combine
+// (+ KS sources), U_B = Bc, con2prim + floors; returns the A9 event code
+template <bool KS>
+ECHO_D int uct_cell_body(const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
+                         const double* __restrict__ R, const double* Un, const double* Us, double* Uout, double* P,
+                         const int x[3], const double Bc[3], bool want_rate, double& rate) {
+  const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
+  const auto m = MetAt<KS>::get(mt, x[0], x[1]);
+  double Pp[8], Uo[8], L[8];
+  double Z0;
+  if (KS) {
+    ld8(P + rb, vs, Pp);  // B for the sources
+    Z0 = guess_Z(m, e, Pp);
+  } else {
+    Z0 = P[rb + kSlotZ * vs];  // the stored Newton guess
+  }
+#pragma unroll
+  for (int q = 0; q < 5; q++) L[q] = R[rb + q * vs];
+  if constexpr (KS) add_sources(m, der_rec(mt, x[0], x[1]), e, Pp, L);  // a6
+#pragma unroll
+  for (int q = 0; q < 5; q++) Uo[q] = Un[rb + q * vs];  // hydro only: U_B comes from b
+  if (s == 1) {
+#pragma unroll
+    for (int q = 0; q < 5; q++) Uo[q] = Uo[q] + dt * L[q];
+  } else {
+    const double c0 = (s == 2) ? 0.75 : (1.0 / 3.0), c1 = (s == 2) ? 0.25 : (2.0 / 3.0);
+#pragma unroll
+    for (int q = 0; q < 5; q++) Uo[q] = c0 * Uo[q] + c1 * (Us[rb + q * vs] + dt * L[q]);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a];
+  double Po[8];
+  const int ev = c2p_floors(m, e, Uo, Z0, [&](double* pv) {
+#pragma unroll
+    for (int v = 0; v < 5; v++) pv[v] = KS ? Pp[v] : P[rb + v * vs];
+  }, Po);
+  const double isg = !KS ? 1.0 : frcp(m.sqrtg());
+#pragma unroll
+  for (int a = 0; a < 3; a++) Po[5 + a] = Uo[5 + a] * isg;
+  st8(Uout + rb, vs, Uo);
+  st_prims<KS>(P + rb, vs, Po);
+  if (!KS) P[rb + kSlotZ * vs] = guess_Z(m, e, Po);
+  if (want_rate) rate = fmax(rate, cfl_rate(m, g, e, Po));
+  return ev;
+}
+
+// block-level max of the CFL rate -> one atomic; warp-aggregated event counters
+ECHO_D void uct_reduce(double rate, int nfl, int nfa, unsigned long long* counters, unsigned long long* cfl_out) {
+  if (cfl_out) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rate = fmax(rate, __shfl_xor_sync(0xffffffffu, rate, o));
+    __shared__ double red[32];
+    const int nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rate;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bm = red[0];
+      for (int w = 1; w < nw; w++) bm = fmax(bm, red[w]);
+      atomicMax(cfl_out, (unsigned long long)__double_as_longlong(bm));
+    }
+  }
+  const unsigned fl = __reduce_add_sync(0xffffffffu, (unsigned)nfl);
+  const unsigned fa = __reduce_add_sync(0xffffffffu, (unsigned)nfa);
+  if ((threadIdx.x & 31) == 0) {
+    if (fl) atomicAdd(counters + 0, (unsigned long long)fl);
+    if (fa) atomicAdd(counters + 1, (unsigned long long)fa);
+  }
+}
+
 template <bool KS>
 __global__ void __launch_bounds__(kCellThreads, 3)
 k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, const double* dtp,
@@ -376,65 +445,61 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
   if (id < g.N) {
     int x[3];
     cell_ijk(g, id, x[0], x[1], x[2]);
-    const long long rb = rec_base(g, x[0], x[1], x[2]), vs = g.vs;
-    const auto m = MetAt<KS>::get(mt, x[0], x[1]);
-    double Pp[8], Uo[8], L[8];
-    double Z0;
-    if (KS) {
-      ld8(P + rb, vs, Pp);  // B for the sources
-      Z0 = guess_Z(m, e, Pp);
-    } else {
-      Z0 = P[rb + kSlotZ * vs];  // the stored Newton guess
-    }
-    // the centred new field first (its 18 neighbour loads overlap the hydro loads below)
     double Bc[3];
     centre_field(g, Bst, s == 3 ? 0 : 3, x, Bc);  // the field this stage just wrote
+    ev = uct_cell_body<KS>(g, e, mt, s, dt, R, Un, Us, Uout, P, x, Bc, cfl_out != nullptr, rate);
+  }
+  uct_reduce(rate, ev == 1, ev == 2, counters, cfl_out);
+}
+
+// the same marching along z (one thread per (i, j) column and kZSeg planes): the centring's
+// b^z samples along z come from a 6-entry register window
+template <bool KS>
+__global__ void __launch_bounds__(128, 6)
+k_uct_cell_zm(const GridP g, const EosP e, const MetTables mt, int s, double dt, const double* dtp,
+              const double* __restrict__ R, const double* Un, const double* Us, double* Uout, double* P,
+              const double* __restrict__ Bst, unsigned long long* counters, unsigned long long* cfl_out) {
+  if (dtp) {
+    if (dtp[1] != 0.0) return;  // uniform over the grid
+    dt = dtp[0];
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k0 = blockIdx.z * kZSeg;
+  const int k1 = min(k0 + kZSeg, g.n[2]);
+  const int slot = s == 3 ? 0 : 3;
+  const long long vs = g.vs;
+  int nfl = 0, nfa = 0;
+  double rate = 0.0;
+  if (i < g.n[0]) {
+    double wz[6];  // b^z at faces k-3 .. k+2 (owned by cells k-3 .. k+2)
+    {
+      const int x[3] = {i, j, k0};
 #pragma unroll
-    for (int q = 0; q < 5; q++) L[q] = R[rb + q * vs];
-    if constexpr (KS) add_sources(m, der_rec(mt, x[0], x[1]), e, Pp, L);  // a6
-#pragma unroll
-    for (int q = 0; q < 5; q++) Uo[q] = Un[rb + q * vs];  // hydro only: U_B comes from b
-    if (s == 1) {
-#pragma unroll
-      for (int q = 0; q < 5; q++) Uo[q] = Uo[q] + dt * L[q];
-    } else {
-      const double c0 = (s == 2) ? 0.75 : (1.0 / 3.0), c1 = (s == 2) ? 0.25 : (2.0 / 3.0);
-#pragma unroll
-      for (int q = 0; q < 5; q++) Uo[q] = c0 * Uo[q] + c1 * (Us[rb + q * vs] + dt * L[q]);
+      for (int m = 0; m < 6; m++) wz[m] = Bst[rec_shift(g, x, 2, m - 3) + (slot + 2) * vs];
     }
+    for (int k = k0; k < k1; k++) {
+      const int x[3] = {i, j, k};
+      double Bc[3];
 #pragma unroll
-    for (int a = 0; a < 3; a++) Uo[5 + a] = Bc[a];
-    double Po[8];
-    ev = c2p_floors(m, e, Uo, Z0, [&](double* pv) {
+      for (int a = 0; a < 2; a++) {
+        double f[6];
 #pragma unroll
-      for (int v = 0; v < 5; v++) pv[v] = KS ? Pp[v] : P[rb + v * vs];
-    }, Po);
-    const double isg = !KS ? 1.0 : frcp(m.sqrtg());
+        for (int m = 0; m < 6; m++) f[m] = Bst[rec_shift(g, x, a, m - 3) + (slot + a) * vs];
+        Bc[a] = fma(3.0, f[0] + f[5], fma(-25.0, f[1] + f[4], 150.0 * (f[2] + f[3]))) * (1.0 / 256.0);
+      }
+      Bc[2] = fma(3.0, wz[0] + wz[5], fma(-25.0, wz[1] + wz[4], 150.0 * (wz[2] + wz[3]))) * (1.0 / 256.0);
+      const int ev = uct_cell_body<KS>(g, e, mt, s, dt, R, Un, Us, Uout, P, x, Bc, cfl_out != nullptr, rate);
+      nfl += ev == 1;
+      nfa += ev == 2;
+      if (k + 1 < k1) {
 #pragma unroll
-    for (int a = 0; a < 3; a++) Po[5 + a] = Uo[5 + a] * isg;
-    st8(Uout + rb, vs, Uo);
-    st_prims<KS>(P + rb, vs, Po);
-    if (!KS) P[rb + kSlotZ * vs] = guess_Z(m, e, Po);
-    if (cfl_out) rate = cfl_rate(m, g, e, Po);
-  }
-  if (cfl_out) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rate = fmax(rate, __shfl_xor_sync(0xffffffffu, rate, o));
-    __shared__ double red[kCellThreads / 32];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rate;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double bm = red[0];
-      for (int w = 1; w < kCellThreads / 32; w++) bm = fmax(bm, red[w]);
-      atomicMax(cfl_out, (unsigned long long)__double_as_longlong(bm));
+        for (int m = 0; m < 5; m++) wz[m] = wz[m + 1];
+        wz[5] = Bst[rec_shift(g, x, 2, 3) + (slot + 2) * vs];
+      }
     }
   }
-  const unsigned fl = __reduce_add_sync(0xffffffffu, ev == 1 ? 1u : 0u);
-  const unsigned fa = __reduce_add_sync(0xffffffffu, ev == 2 ? 1u : 0u);
-  if ((threadIdx.x & 31) == 0) {
-    if (fl) atomicAdd(counters + 0, (unsigned long long)fl);
-    if (fa) atomicAdd(counters + 1, (unsigned long long)fa);
-  }
+  uct_reduce(rate, nfl, nfa, counters, cfl_out);
 }
 
 // set: U_B = I6(b^n) and U from the state's hydro primitives (a0 with the new field)
@@ -512,10 +577,21 @@ cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const 
   return cudaGetLastError();
 }
 
+#ifndef ECHO_CELL_ZMARCH
+#define ECHO_CELL_ZMARCH 1
+#endif
 cudaError_t launch_uct_cell(bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
                             const double* dtp, const double* R, const double* Un, const double* Us, double* Uout,
                             double* P, const double* Bst, unsigned long long* counters, unsigned long long* cfl_out,
                             cudaStream_t st) {
+  if (ECHO_CELL_ZMARCH) {
+    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSeg - 1) / kZSeg));
+    if (ks)
+      k_uct_cell_zm<true><<<zb, 128, 0, st>>>(g, e, mt, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
+    else
+      k_uct_cell_zm<false><<<zb, 128, 0, st>>>(g, e, mt, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
+    return cudaGetLastError();
+  }
   const unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
   if (ks)
     k_uct_cell<true><<<blocks, kCellThreads, 0, st>>>(g, e, mt, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
