@@ -41,6 +41,7 @@ struct echo_ctx {
   // cell-interleaved device state (echo_kernels.h): 8 doubles per cell each
   double* alloc_base[4] = {nullptr, nullptr, nullptr, nullptr};  // allocations (slab mode: incl. ghost planes)
   echo_ctx* link[2] = {nullptr, nullptr};  // slab mode: neighbours whose ghost planes K3 writes (echo_halo_link)
+  std::vector<echo_ctx*> linked_by;         // contexts whose link[] points here (cleared by echo_destroy)
   // ... or a neighbour in another process: its P, Un, Us (plane 0) mapped by CUDA IPC
   struct Remote {
     double* base[3] = {nullptr, nullptr, nullptr};  // opened allocation bases (P, Un, Us)
@@ -378,8 +379,23 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   return ECHO_OK;
 }
 
+static void drop_backref(echo_ctx* peer, echo_ctx* c) {
+  auto& v = peer->linked_by;
+  for (size_t i = 0; i < v.size(); i++)
+    if (v[i] == c) {
+      v.erase(v.begin() + i);
+      return;
+    }
+}
+
 void echo_destroy(echo_ctx* c) {
   if (!c) return;
+  // unlink both ways: no surviving context may keep storing into this one's ghost planes
+  for (echo_ctx* x : c->linked_by)
+    for (auto& l : x->link)
+      if (l == c) l = nullptr;
+  for (auto& l : c->link)
+    if (l && l != c) drop_backref(l, c);
   for (auto& rm : c->rlink) ipc_close(rm);
   for (double* b : c->alloc_base) cudaFree(b);
   cudaFree(c->scratch);
@@ -542,6 +558,7 @@ int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
   }
   CK(launch(c, kLayout, [&] { return launch_layout(c->g, src, c->Un, 8, false, c->st); }), "echo_set_cons");
   c->next_stage = 1;
+  c->swept = 0;  // a half-done stage (echo_stage_sweeps) of the old state is void
   return echo_con2prim(c, nullptr);
 }
 
@@ -862,6 +879,7 @@ int echo_halo_pull(echo_ctx* c, int side) {
 int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
   if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_link: bad argument") : ECHO_E_ARG;
   if (!peer) {
+    if (c->link[side]) drop_backref(c->link[side], c);
     c->link[side] = nullptr;
     return ECHO_OK;
   }
@@ -869,7 +887,9 @@ int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
     return fail(c, ECHO_E_ARG, "echo_halo_link: both facing sides must be halo boundaries");
   if (peer->g.n[0] != c->g.n[0] || peer->g.n[1] != c->g.n[1] || peer->g.pitch != c->g.pitch || peer->ks != c->ks)
     return fail(c, ECHO_E_ARG, "echo_halo_link: the slabs must share n[0], n[1] and the metric");
+  if (c->link[side]) drop_backref(c->link[side], c);
   c->link[side] = peer;
+  peer->linked_by.push_back(c);
   return ECHO_OK;
 }
 

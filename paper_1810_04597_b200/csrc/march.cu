@@ -28,6 +28,8 @@
 // (fixed per-lane operation order).
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "echo_dev.cuh"
 #include "echo_kernels.h"
 
@@ -509,15 +511,21 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
                               double* R, const double* Bface, double* FSo, cudaStream_t st) {
   using GE = Geo<AX>;
   auto kern = k_march<AX, KS, DER, REC, DM>;
-  static int grid_cap = 0;
+  // per device (the attribute and the occupancy are per-device properties); the cache is
+  // written at most once per device, racing writers store the same value
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> grid_caps[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int grid_cap = dev < kMaxDev ? grid_caps[dev].load(std::memory_order_relaxed) : 0;
   if (!grid_cap) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GE::SMEM);
     if (err != cudaSuccess) return err;
-    int dev, sms, per = 0;
-    cudaGetDevice(&dev);
+    int sms, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GE::THREADS, GE::SMEM);
     grid_cap = sms * (per > 0 ? per : 1);
+    if (dev < kMaxDev) grid_caps[dev].store(grid_cap, std::memory_order_relaxed);
   }
   LineGeom lg;
   lg.na = g.n[AX];

@@ -1,0 +1,95 @@
+"""Multi-step GPU-vs-oracle parity at BASELINE.json's FULL sizes (north_star: "all
+five configs match the CPU oracle within ... 1e-10 after 10 steps"; SURVEY.md §8(d)
+"Parity for config 3 still needs the full 5 steps once"; reading A17).
+
+Every config runs in the bench's launch configuration (the persistent sweeps' multi-unit
+path: at these sizes every CTA marches many line groups) with the oracle's dt sequence;
+the state after the last step is compared element by element on every cell, per A16
+group, and the floor / Newton-failure counters must be equal.  The GPU's own CFL dt is
+checked against the oracle's at every step.
+
+* config 1 (128^3 CP Alfven wave), config 2 (256^3 blast, A31 active at the shock),
+  config 4 (256 x 128 x 256 Kerr-Schild torus, floors firing in the atmosphere): 10 steps.
+* config 3 (512^3): 5 steps.  The oracle needs ~45 GB of host RAM and ~10 min of host
+  CPU for it, so it runs only with ECHO_FULL_CFG3=1 (the committed log of that run is
+  profiles/r02_fullsize_cfg3.txt).
+"""
+import os
+import time
+
+import numpy as np
+import pytest
+
+import echo_inputs as I
+from tests.util import CONS_GROUPS, PRIM5_GROUPS, PRIM8_GROUPS, group_errors
+
+pytestmark = pytest.mark.gpu
+
+TOL_10 = 1e-10
+
+
+@pytest.fixture(scope="module")
+def E():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1810_04597_b200 import build
+
+    build.build()
+    from paper_1810_04597_b200 import echo
+
+    return echo
+
+
+def _run(E, orc, cfg, steps):
+    p = I.problem(cfg)
+    oc = orc.Cfg(**p.grid_kwargs())
+    t0 = time.time()
+    P8 = I.initial_prims(p)
+    U, P = orc.set_prims(oc, P8)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    del P8
+    ocnt = [0, 0]
+    dts = []
+    for _ in range(steps):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        dt_g = g.max_dt(p.cfl)
+        assert dt_g == pytest.approx(dt, rel=1e-13), (dt_g, dt)
+        dts.append(dt)
+        U, P, cnt = orc.step(oc, dt, U, P)
+        ocnt[0] += cnt[0]
+        ocnt[1] += cnt[1]
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    eu = group_errors(gn, U, CONS_GROUPS)
+    ep = group_errors(gp, P, PRIM5_GROUPS)
+    e8 = group_errors(g.get_prims(), orc.get_prims(oc, U, P), PRIM8_GROUPS)
+    st = g.stats()
+    g.close()
+    line = (f"cfg{cfg} {p.n} {steps} steps ({time.time() - t0:.0f} s): U {eu} P {ep} prims {e8} "
+            f"counters gpu ({st['floor_events']}, {st['c2p_failures']}) oracle {tuple(ocnt)} dt[0] {dts[0]:.6e}")
+    print(line)
+    log = os.environ.get("ECHO_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write("fullsize " + line + "\n")
+    for name, errs in (("U", eu), ("P", ep), ("prims", e8)):
+        bad = {k: v for k, v in errs.items() if not v <= TOL_10}
+        assert not bad, f"cfg{cfg} {steps} steps {name}: {errs}"
+    assert (st["floor_events"], st["c2p_failures"]) == tuple(ocnt)
+    if cfg in (1, 3):
+        assert ocnt == [0, 0]
+    return ocnt
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_full_size_10_step_parity(E, orc, cfg):
+    _run(E, orc, cfg, 10)
+
+
+@pytest.mark.skipif(os.environ.get("ECHO_FULL_CFG3") != "1",
+                    reason="512^3 oracle: ~45 GB host RAM, ~10 min; set ECHO_FULL_CFG3=1 (log in profiles/)")
+def test_full_size_cfg3_5_step_parity(E, orc):
+    _run(E, orc, 3, 5)

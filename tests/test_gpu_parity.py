@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import echo_inputs as I
-from tests.util import CONS_GROUPS, PRIM5_GROUPS, PRIM8_GROUPS, assert_groups, assert_rhs_groups
+from tests.util import CONS_GROUPS, PRIM5_GROUPS, PRIM8_GROUPS, assert_groups, assert_rhs_groups, flux_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -80,7 +80,8 @@ def test_rhs_and_stage_parity(E, orc, cfg, n):
     dt_o = orc.max_dt(oc, gun, gp, p.cfl)
     # rhs on identical inputs
     L = orc.rhs(oc, gun, gp)
-    assert_rhs_groups(g.rhs(), L, gun, dt_o, CONS_GROUPS, TOL_STAGE, what=f"rhs cfg{cfg}")
+    assert_rhs_groups(g.rhs(), L, gun, dt_o, CONS_GROUPS, TOL_STAGE, what=f"rhs cfg{cfg} {n}",
+                      fscale=flux_scale(orc, oc, gun, gp))
     dt_g = g.max_dt(p.cfl)
     assert dt_g == pytest.approx(dt_o, rel=1e-14)
     # stage-chained parity: each oracle stage starts from the GPU's own input state
@@ -182,7 +183,8 @@ def test_switches_parity(E, orc):
         g = E.Echo(p)
         g.set_prims(P8)
         dt = orc.max_dt(oc, U, P, 0.4)
-        assert_rhs_groups(g.rhs(), orc.rhs(oc, U, P), U, dt, CONS_GROUPS, TOL_STAGE, what=f"rhs {kw}")
+        assert_rhs_groups(g.rhs(), orc.rhs(oc, U, P), U, dt, CONS_GROUPS, TOL_STAGE, what=f"rhs {kw}",
+                          fscale=flux_scale(orc, oc, U, P))
         p = small_problem(0, (70, 9, 10))
 
 
@@ -298,7 +300,8 @@ def test_degenerate_grids_parity(E, orc, n, bc):
     g.set_prims(P8)
     dt = orc.max_dt(oc, U, P, p.cfl)
     assert g.max_dt(p.cfl) == pytest.approx(dt, rel=1e-14)
-    assert_rhs_groups(g.rhs(), orc.rhs(oc, U, P), U, dt, CONS_GROUPS, TOL_STAGE, what=f"rhs {n}")
+    assert_rhs_groups(g.rhs(), orc.rhs(oc, U, P), U, dt, CONS_GROUPS, TOL_STAGE, what=f"rhs {n}",
+                      fscale=flux_scale(orc, oc, U, P))
     for _ in range(3):
         dt = orc.max_dt(oc, U, P, p.cfl)
         U, P, _ = orc.step(oc, dt, U, P)

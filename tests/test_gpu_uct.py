@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import echo_inputs as I
-from tests.util import CONS_GROUPS, PRIM5_GROUPS, assert_groups, assert_rhs_groups
+from tests.util import CONS_GROUPS, PRIM5_GROUPS, assert_groups, assert_rhs_groups, flux_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -65,8 +65,9 @@ def test_uct_rhs_and_stage_parity(E, orc, cfg, n):
     assert g.max_dt(p.cfl) == pytest.approx(dt, rel=1e-14)
     L = orc.rhs_uct(oc, gun, gp, ob)
     Lg = g.rhs()
-    assert_rhs_groups(Lg[:5], L[:5], gun[:5], dt, HYDRO, TOL_STAGE, what=f"uct rhs hydro cfg{cfg}")
-    assert_rhs_groups(Lg[5:], L[5:], ob, dt, FACE, TOL_STAGE, what=f"uct rhs L(b) cfg{cfg}")
+    fs = flux_scale(orc, oc, gun, gp)
+    assert_rhs_groups(Lg[:5], L[:5], gun[:5], dt, HYDRO, TOL_STAGE, what=f"uct rhs hydro cfg{cfg}", fscale=fs)
+    assert_rhs_groups(Lg[5:], L[5:], ob, dt, FACE, TOL_STAGE, what=f"uct rhs L(b) cfg{cfg}", fscale={"b": fs["B"]})
     # stage-chained: each oracle stage starts from the GPU's own input state
     bn = g.get_face_field()
     bs = bn
@@ -215,8 +216,9 @@ def test_uct_degenerate_grids_parity(E, orc, n, bc):
     dt = orc.max_dt(oc, U, P, p.cfl)
     L = orc.rhs_uct(oc, U, P, ob)
     Lg = g.rhs()
-    assert_rhs_groups(Lg[:5], L[:5], U[:5], dt, HYDRO, TOL_STAGE, what=f"uct rhs {n}")
-    assert_rhs_groups(Lg[5:], L[5:], ob, dt, FACE, TOL_STAGE, what=f"uct L(b) {n}")
+    fs = flux_scale(orc, oc, U, P)
+    assert_rhs_groups(Lg[:5], L[:5], U[:5], dt, HYDRO, TOL_STAGE, what=f"uct rhs {n}", fscale=fs)
+    assert_rhs_groups(Lg[5:], L[5:], ob, dt, FACE, TOL_STAGE, what=f"uct L(b) {n}", fscale={"b": fs["B"]})
     for _ in range(3):
         dt = orc.max_dt(oc, U, P, p.cfl)
         U, P, ob, _ = orc.step_uct(oc, dt, U, P, ob)
