@@ -50,7 +50,8 @@ typedef enum {
   ECHO_E_OOM = -3,         /* device allocation failed */
   ECHO_E_ORDER = -4,       /* call out of order, e.g. echo_step before echo_set_prims */
   ECHO_E_UNPHYSICAL = -5,  /* rho <= 0, p <= 0 or v^2 >= 1 in echo_set_prims */
-  ECHO_E_NONFINITE = -6    /* all CFL speeds zero / non-finite (echo_max_dt) */
+  ECHO_E_NONFINITE = -6    /* all CFL speeds zero / non-finite (echo_max_dt), or a NaN/Inf in the
+                              state (echo_check_finite; debug mode ECHO_DEBUG_NANSCAN) */
 } echo_status;
 
 typedef enum { ECHO_BC_PERIODIC = 0, ECHO_BC_OUTFLOW = 1, ECHO_BC_HALO = 2 } echo_bc;  /* A13; HALO: slabs */
@@ -238,6 +239,22 @@ int echo_halo_link_ipc(echo_ctx* ctx, int side, const void* handles, int peer_nz
 int echo_halo_export(echo_ctx* ctx, int side, double* buf, int on_device);
 int echo_halo_import(echo_ctx* ctx, int side, const double* buf, int on_device);
 int echo_halo_fill(echo_ctx* ctx, int side);
+
+/* ---- failure detection (SURVEY.md §8(b) "Errors": ECHO_E_NONFINITE comes from a NaN scan
+ * naming the first bad cell; §5 "Failure detection") ----
+ * echo_check_finite: scan the current state, U (8 slots) and the state primitives (rho, u~^i,
+ * p; + B^i in a curved metric) of every owned cell for NaN / Inf.  Synchronises.  ECHO_OK, or
+ * ECHO_E_NONFINITE with echo_last_error naming the first bad value in linear cell order:
+ * "U[q]" or "P[q]", its value and the cell (i,j,k).
+ * echo_set_debug(ctx, ECHO_DEBUG_NANSCAN): from then on every RK stage ends with that scan
+ * of its new state (one extra kernel per stage, stream-ordered).  echo_stage / echo_step then
+ * synchronise after each stage and return ECHO_E_NONFINITE at the first stage that produced a
+ * non-finite value; echo_advance halts on the device (later updates are skipped, the state is
+ * that after the offending stage) and reports it at its end.  flags = 0 turns it off.  The
+ * environment variable ECHO_DEBUG_NANSCAN=1 at echo_create sets the flag. */
+enum { ECHO_DEBUG_NANSCAN = 1 };
+int echo_set_debug(echo_ctx* ctx, int flags);
+int echo_check_finite(echo_ctx* ctx);
 
 /* Text of the last error of ctx ("" if none); NULL ctx gives the last echo_create error. */
 const char* echo_last_error(const echo_ctx* ctx);

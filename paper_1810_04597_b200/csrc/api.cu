@@ -7,6 +7,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -22,11 +23,11 @@ namespace {
 
 enum KernelClass {
   kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kLayout,
-  kCflDt, kUctEmf, kUctInduct, kUctCell, kNumClasses
+  kCflDt, kUctEmf, kUctInduct, kUctCell, kNanScan, kNumClasses
 };
 const char* kNames[kNumClasses] = {"sweep_x",   "sweep_y",   "sweep_z",   "update_stage", "update_rhs",
                                    "con2prim",  "max_speed", "prim2cons", "get_prims",    "layout",
-                                   "cfl_dt",    "uct_emf",   "uct_induct", "uct_cell"};
+                                   "cfl_dt",    "uct_emf",   "uct_induct", "uct_cell", "nan_scan"};
 
 std::string g_create_error;
 
@@ -64,6 +65,8 @@ struct echo_ctx {
   double* scratch = nullptr;  // 8N, lazily for layout conversions / host-buffer transfers
   unsigned long long* dcnt = nullptr;  // [0] floors [1] failures [2] max speed bits
   long long* dbad = nullptr;
+  long long* dnan = nullptr;  // first non-finite value (cell id * 16 + slot) of the debug scan
+  int debug = 0;              // ECHO_DEBUG_* flags
   unsigned long long* hpin = nullptr;  // pinned readback
   cudaStream_t st = nullptr;
   bool have_state = false;
@@ -208,6 +211,10 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
                                cfl, c->st);
       });
     if (e != cudaSuccess) return cuda_fail(c, e, "uct update launch");
+    if (c->debug & ECHO_DEBUG_NANSCAN) {
+      e = launch(c, kNanScan, [&] { return launch_nanscan(c->g, Uout, c->P, c->ks ? 8 : 5, c->dnan, dtp ? c->dadv : nullptr, c->st); });
+      if (e != cudaSuccess) return cuda_fail(c, e, "nan scan launch");
+    }
     c->cfl_valid = (s == 3);
     c->stages++;
     c->next_stage = (s == 3) ? 1 : s + 1;
@@ -220,6 +227,10 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
                          c->dcnt, cfl, c->st, &gl, dtp);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
+  if (c->debug & ECHO_DEBUG_NANSCAN) {
+    e = launch(c, kNanScan, [&] { return launch_nanscan(c->g, Uout, c->P, c->ks ? 8 : 5, c->dnan, dtp ? c->dadv : nullptr, c->st); });
+    if (e != cudaSuccess) return cuda_fail(c, e, "nan scan launch");
+  }
   c->cfl_valid = (s == 3);
   c->stages++;
   c->next_stage = (s == 3) ? 1 : s + 1;
@@ -227,10 +238,34 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
   return ECHO_OK;
 }
 
+// the debug scan's verdict (synchronises): ECHO_E_NONFINITE naming the first bad value
+static int nan_report(echo_ctx* c, const char* where) {
+  long long code = LLONG_MAX;
+  CK(cudaMemcpyAsync(&code, c->dnan, sizeof code, cudaMemcpyDeviceToHost, c->st), where);
+  CK(cudaStreamSynchronize(c->st), where);
+  if (code == LLONG_MAX) return ECHO_OK;
+  const long long id = code / 16;
+  const int q = (int)(code % 16);
+  double v = 0.0;
+  const long long r = id / c->g.n[0];
+  const long long off = r * c->g.pitch + (id - r * c->g.n[0]) + (long long)(q % 8) * c->g.vs;
+  cudaMemcpy(&v, (q < 8 ? (const double*)ucur(c) : c->P) + off, sizeof v, cudaMemcpyDeviceToHost);
+  const long long i = id % c->g.n[0], j = (id / c->g.n[0]) % c->g.n[1], k = id / ((long long)c->g.n[0] * c->g.n[1]);
+  char buf[300];
+  std::snprintf(buf, sizeof buf, "%s: non-finite state value %s[%d] = %g at cell (%lld,%lld,%lld)", where,
+                q < 8 ? "U" : "P", q % 8, v, i, j, k);
+  const long long init = LLONG_MAX;
+  cudaMemcpy(c->dnan, &init, sizeof init, cudaMemcpyHostToDevice);
+  return fail(c, ECHO_E_NONFINITE, buf);
+}
+
 static int run_stage(echo_ctx* c, int s, double dt) {
   int rc = run_sweeps(c);
   if (rc) return rc;
-  return run_update(c, s, dt);
+  rc = run_update(c, s, dt);
+  if (rc) return rc;
+  if (c->debug & ECHO_DEBUG_NANSCAN) return nan_report(c, s == 1 ? "stage 1" : (s == 2 ? "stage 2" : "stage 3"));
+  return ECHO_OK;
 }
 
 extern "C" {
@@ -329,7 +364,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   if (alloc(0, &c->Un) != cudaSuccess || alloc(1, &c->Us) != cudaSuccess || alloc(2, &c->P) != cudaSuccess ||
       alloc(3, &c->R) != cudaSuccess ||
       cudaMalloc(&c->dcnt, 4 * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&c->dbad, sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&c->dbad, sizeof(long long)) != cudaSuccess || cudaMalloc(&c->dnan, sizeof(long long)) != cudaSuccess ||
       cudaMallocHost(&c->hpin, 4 * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     echo_destroy(c);
@@ -370,6 +405,12 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     c->mt.f1 = p;
     c->mt.w0 = t.w0;
   }
+  {
+    const long long init = LLONG_MAX;
+    cudaMemcpy(c->dnan, &init, sizeof init, cudaMemcpyHostToDevice);
+    const char* dbg = std::getenv("ECHO_DEBUG_NANSCAN");
+    if (dbg && dbg[0] == '1') c->debug = ECHO_DEBUG_NANSCAN;
+  }
   ce = cudaDeviceSynchronize();
   if (ce != cudaSuccess) {
     echo_destroy(c);
@@ -401,6 +442,7 @@ void echo_destroy(echo_ctx* c) {
   cudaFree(c->scratch);
   cudaFree(c->dcnt);
   cudaFree(c->dbad);
+  cudaFree(c->dnan);
   cudaFree(c->tables);
   cudaFree(c->dadv);
   cudaFree(c->Bst);
@@ -732,7 +774,10 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
   if (!c->dadv || cap > c->dlog_cap) {  // adv block + log; a new buffer invalidates the captured step
     cudaFree(c->dadv);
     c->dadv = nullptr;
-    const long long ncap = cap > c->dlog_cap ? cap : c->dlog_cap;
+    // at least 4096 entries: a later call with a longer log (e.g. warm-up without a log, then a
+    // timed loop with one) does not reallocate and re-capture the step
+    long long ncap = cap > c->dlog_cap ? cap : c->dlog_cap;
+    if (ncap < 4096) ncap = 4096;
     if (cudaMalloc(&c->dadv, sizeof(double) * (4 + ncap)) != cudaSuccess)
       return fail(c, ECHO_E_OOM, "echo_advance: dt log allocation failed");
     c->dlog_cap = ncap;
@@ -773,6 +818,10 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
   c->steps += done;
   c->stages = stages0 + 3ull * done;
   if (steps_done) *steps_done = done;
+  if (adv[1] == 2.0) {  // the debug scan halted the loop
+    c->cfl_valid = false;
+    return nan_report(c, "echo_advance (debug scan)");
+  }
   if (adv[1] != 0.0) {
     c->cfl_valid = false;
     return fail(c, ECHO_E_NONFINITE,
@@ -781,6 +830,30 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
   }
   c->cfl_valid = true;
   return ECHO_OK;
+}
+
+int echo_set_debug(echo_ctx* c, int flags) {
+  if (!c) return ECHO_E_ARG;
+  if (flags & ~ECHO_DEBUG_NANSCAN) return fail(c, ECHO_E_ARG, "echo_set_debug: unknown flag");
+  const long long init = LLONG_MAX;
+  CK(cudaMemcpyAsync(c->dnan, &init, sizeof init, cudaMemcpyHostToDevice, c->st), "echo_set_debug");
+  CK(cudaStreamSynchronize(c->st), "echo_set_debug");
+  if (flags != c->debug && c->step_exec) {  // the captured step holds (or lacks) the scans
+    cudaGraphExecDestroy(c->step_exec);
+    c->step_exec = nullptr;
+  }
+  c->debug = flags;
+  return ECHO_OK;
+}
+
+int echo_check_finite(echo_ctx* c) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_check_finite: no state");
+  const long long init = LLONG_MAX;
+  CK(cudaMemcpyAsync(c->dnan, &init, sizeof init, cudaMemcpyHostToDevice, c->st), "echo_check_finite");
+  cudaError_t e = launch(c, kNanScan, [&] { return launch_nanscan(c->g, ucur(c), c->P, c->ks ? 8 : 5, c->dnan, nullptr, c->st); });
+  if (e != cudaSuccess) return cuda_fail(c, e, "nan scan launch");
+  return nan_report(c, "echo_check_finite");
 }
 
 int echo_stats(echo_ctx* c, echo_stats_t* out) {

@@ -54,6 +54,12 @@ cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, cons
 cudaError_t launch_cfl_dt(double cfl, const unsigned long long* maxbits, double* adv, double* log, long long cap,
                           cudaStream_t st);
 
+// debug NaN/Inf scan of U (8 slots) and P (np slots) of the owned cells: first bad value's
+// (cell id * 16 + slot, P slots 8..) atomicMin'd into *first (init LLONG_MAX); a hit sets adv[1] = 2
+// when adv is given (device-driven loop: halts it)
+cudaError_t launch_nanscan(const GridP& g, const double* U, const double* P, int np, long long* first, double* adv,
+                           cudaStream_t st);
+
 // a9: per-cell sum_a max|lambda_a|/Delta_a, max-reduced into *out (u64 bit pattern, zeroed by caller)
 cudaError_t launch_max_speed(bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
                              const double* U, unsigned long long* out, cudaStream_t st);

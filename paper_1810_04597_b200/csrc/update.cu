@@ -184,6 +184,43 @@ cudaError_t launch_cfl_dt(double cfl, const unsigned long long* maxbits, double*
   return cudaGetLastError();
 }
 
+// ------------------------------------------------ debug NaN / Inf scan (SURVEY §8(b) "Errors")
+// first non-finite value of the state: U (8 slots) and the primitives P (slots 0..4; 0..7 in a
+// curved metric) of every owned cell; *first = min over bad values of (linear cell id) * 16 + slot
+// (slots 0..7 U, 8..15 P), init LLONG_MAX.  adv (device loop, may be NULL): a hit sets the halt
+// flag adv[1] = 2, after which the loop's later updates do nothing (the state is kept for the report).
+__global__ void __launch_bounds__(kCellThreads)
+k_nanscan(const GridP g, const double* __restrict__ U, const double* __restrict__ P, int np, long long* first,
+          double* adv) {
+  const long long N = g.N;
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long code = LLONG_MAX;
+  if (id < N) {
+    const long long rb = rec_base_id(g, id), vs = g.vs;
+    for (int q = 15; q >= 0; q--) {  // the lowest bad slot wins
+      if (q >= 8 && q - 8 >= np) continue;
+      const double v = q < 8 ? U[rb + q * vs] : P[rb + (q - 8) * vs];
+      if (!isfinite(v)) code = id * 16 + q;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long other = __shfl_xor_sync(0xffffffffu, code, o);
+    code = other < code ? other : code;
+  }
+  if ((threadIdx.x & 31) == 0 && code != LLONG_MAX) {
+    atomicMin((unsigned long long*)first, (unsigned long long)code);
+    if (adv) adv[1] = 2.0;
+  }
+}
+
+cudaError_t launch_nanscan(const GridP& g, const double* U, const double* P, int np, long long* first, double* adv,
+                           cudaStream_t st) {
+  unsigned blocks = (unsigned)((g.N + kCellThreads - 1) / kCellThreads);
+  k_nanscan<<<blocks, kCellThreads, 0, st>>>(g, U, P, np, first, adv);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ a0 and back
 // user prims [8][cell] (rho, v^i, p, B^i) -> P[cell][8] (rho, u~^i, p, B^i), Un[cell][8]
 template <bool KS>

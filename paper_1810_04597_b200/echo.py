@@ -26,6 +26,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 OK, E_ARG, E_CUDA, E_OOM, E_ORDER, E_UNPHYSICAL, E_NONFINITE = 0, -1, -2, -3, -4, -5, -6
+DEBUG_NANSCAN = 1
 BC_PERIODIC, BC_OUTFLOW, BC_HALO = 0, 1, 2
 HALO_PLANES = 6
 METRIC_MINKOWSKI, METRIC_KERR_SCHILD = 0, 1
@@ -86,6 +87,8 @@ _sig = {
     "echo_halo_export": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_import": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_fill": (C.c_int, [_P, C.c_int]),
+    "echo_set_debug": (C.c_int, [_P, C.c_int]),
+    "echo_check_finite": (C.c_int, [_P]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -263,6 +266,14 @@ def kernel_name(i: int) -> str:
     return _lib.echo_kernel_name(i).decode()
 
 
+def set_debug(ctx, flags: int):
+    return _check(ctx, _lib.echo_set_debug(ctx, int(flags)))
+
+
+def check_finite(ctx):
+    return _check(ctx, _lib.echo_check_finite(ctx))
+
+
 def launch_count(ctx) -> int:
     return int(_lib.echo_launch_count(ctx))
 
@@ -395,3 +406,9 @@ class Echo:
 
     def stats(self):
         return stats(self.ctx)
+
+    def set_debug(self, flags=DEBUG_NANSCAN):
+        return set_debug(self.ctx, flags)
+
+    def check_finite(self):
+        return check_finite(self.ctx)
