@@ -12,7 +12,7 @@ checked against the oracle's at every step.
   config 4 (256 x 128 x 256 Kerr-Schild torus, floors firing in the atmosphere): 10 steps.
 * config 3 (512^3): 5 steps.  The oracle needs ~45 GB of host RAM and ~10 min of host
   CPU for it, so it runs only with ECHO_FULL_CFG3=1 (the committed log of that run is
-  profiles/r02_fullsize_cfg3.txt).
+  profiles/r02_fullsize_parity.txt).
 """
 import os
 import time
