@@ -114,7 +114,7 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- CPU baseline
-def cpu_baseline(steps: int = 1, n: int = 64):
+def cpu_baseline(steps: int = 1, n: int = 64, n1: int = 128):
     """The oracle as it stands, on the host cores: `steps` SSP-RK3 steps (+CFL) of the
     config-3 recipe on an n^3 periodic grid (a bounded sample of the 512^3 workload)."""
     import oracle
@@ -129,9 +129,32 @@ def cpu_baseline(steps: int = 1, n: int = 64):
         U, P, _ = oracle.step(oc, dt, U, P)
     t = time.perf_counter() - t0
     zu = p.ncells * steps / t
-    return {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{steps} CFL+SSP-RK3 step(s) of the config-3 recipe (32 modes, k<=8, amp 0.1) on a {n}^3 "
-                      f"periodic grid, {t:.2f} s wall, OpenMP {cores} threads"}
+    out = {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{steps} CFL+SSP-RK3 step(s) of the config-3 recipe (32 modes, k<=8, amp 0.1) on a {n}^3 "
+                     f"periodic grid, {t:.2f} s wall, OpenMP {cores} threads",
+           "cpu_model": cpu_model()}
+    if n1 > 0:  # SURVEY §8(d) timing protocol: also the single-thread rate on 128^3
+        p1 = I.problem(3, n=(n1, n1, n1))
+        o1 = oracle.Cfg(**p1.grid_kwargs(), nthreads=1)
+        U, P = oracle.set_prims(o1, I.initial_prims(p1))
+        t0 = time.perf_counter()
+        dt = oracle.max_dt(o1, U, P, p1.cfl)
+        U, P, _ = oracle.step(o1, dt, U, P)
+        t1 = time.perf_counter() - t0
+        out["single_thread"] = {"value": p1.ncells / t1, "unit": UNIT, "cores": 1,
+                                "sample": f"1 CFL+SSP-RK3 step of the config-3 recipe on {n1}^3, {t1:.1f} s wall"}
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        r = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10)
+        for line in r.stdout.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------- distributed glue
@@ -200,8 +223,10 @@ def run_reference(args, world, rank):
     out = {"impl": "reference", "metric": METRIC, "value": zu, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
            "warmup": W, "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": workload_config(args, I.problem(args.config), world=1),
-           "cpu_baseline": {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "config": dict(workload_config(args, p, world=1),
+                          sample_of=f"BASELINE.json configs[{args.config}] at {'x'.join(map(str, I.problem(args.config).n))}"),
+           "cpu_baseline": {"value": zu, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                            "cpu_model": cpu_model()},
            "e2e": {"value": zu, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -214,7 +239,8 @@ def workload_config(args, p, world):
     return {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
                         f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[args.rec]}+HLL+DER6+{DIVB_NAMES[args.divb]}, SSP-RK3",
             "grid": list(p.n), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-            "l2": "inputs (~34 GB of state) >> 126 MB L2: no flush needed",
+            "l2": (f"inputs (~{p.ncells * 256 / 1e9:.0f} GB of state) >> 126 MB L2: no flush needed" if p.ncells * 256 > 2e9
+                   else "state smaller than L2 (reference sample on the host)"),
             "step": "CFL reduction -> dt, then one SSP-RK3 step (3 stages x [3 sweeps + update])"}
 
 
@@ -340,7 +366,7 @@ def run_ours(args, world, rank, local):
         g.set_face_field(B3)
     # warm-up in the timed loop's own mode (the device loop captures its graph here)
     if args.loop == "device":
-        g.advance(W, p.cfl, log=False)
+        g.advance(W, p.cfl, log=True)
     else:
         for _ in range(W):
             g.step(g.max_dt(p.cfl))
@@ -381,25 +407,34 @@ def run_ours(args, world, rank, local):
     prof = echo.profile_read(g.ctx)
     echo.profile(g.ctx, False)
     step_ms = sum(ms for ms, n in prof.values()) / 2.0
-    top = max(prof.items(), key=lambda kv: kv[1][0])
     shares = {k: round(ms / 2.0 / step_ms, 4) for k, (ms, n) in prof.items() if n}
 
     peaks = load_peaks()
-    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep")}
-    sw_ms = sum(v[0] for v in sweeps.values())
-    sw_n = sum(v[1] for v in sweeps.values())
-    sweep_avg_s = sw_ms / sw_n / 1e3
-    achieved = FLOPS_PER_CELL_SWEEP * N / sweep_avg_s
+    # the dominant sweep kernel (by device time in the event-profiled pass); its launch time IN THE
+    # TIMED REGION = its share of the profiled step x the timed ms/step / its launches per step
+    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep") and v[1]}
+    dom = max(sweeps.items(), key=lambda kv: kv[1][0])[0]
+    dom_ms, dom_n = sweeps[dom]
+    dom_share = dom_ms / 2.0 / step_ms
+    t_launch = dom_share * (t / K) / (dom_n / 2.0)
+    flops_launch = FLOPS_PER_CELL_SWEEP * N
+    achieved = flops_launch / t_launch
+    achieved_pp = flops_launch / (dom_ms / dom_n / 1e3)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("bytes_per_launch")
-    roofline = {"kernel": "sweep_x/y/z (K2, FP64-ALU bound)", "bound": "alu", "achieved": achieved / 1e12,
+            tj = json.load(f)
+        axis = {"sweep_x": 0, "sweep_y": 1, "sweep_z": 2}.get(dom)
+        traffic = tj["per_axis"][axis] if axis is not None and "per_axis" in tj else tj.get("bytes_per_launch")
+    roofline = {"kernel": f"{dom} (K2 axis sweep, FP64-ALU bound)", "bound": "alu", "achieved": achieved / 1e12,
                 "peak": peaks["fp64_flops"] / 1e12, "unit": "TFLOP/s", "frac": achieved / peaks["fp64_flops"],
                 "traffic": traffic, "peak_source": peaks["src_fp64"],
-                "per_launch_flops": FLOPS_PER_CELL_SWEEP * N, "avg_launch_ms": sweep_avg_s * 1e3,
-                "dominant_kernel_by_time": top[0], "kernel_share_of_step": shares}
+                "per_launch_flops": flops_launch, "launch_ms_timed": t_launch * 1e3,
+                "how": "achieved = 901 algorithmic flops/cell x cells / launch time; launch time = the kernel's "
+                       "share of the event-profiled step x the timed region's ms/step / its launches per step",
+                "frac_profile_pass": achieved_pp / peaks["fp64_flops"],
+                "kernel_share_of_step": shares}
     hbm_rate = peaks["hbm_gbs"] * 1e9 / BYTES_PER_ZONE_STEP
     hbm = {"bytes_per_zone_step": BYTES_PER_ZONE_STEP, "achieved_gbs": value / world * BYTES_PER_ZONE_STEP / 1e9,
            "peak_gbs": peaks["hbm_gbs"], "frac": value / world / hbm_rate, "peak_source": peaks["src_hbm"]}
@@ -441,7 +476,7 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(steps=args.cpu_steps, n=args.cpu_n)
+            cpu = cpu_baseline(steps=args.cpu_steps, n=args.cpu_n, n1=args.cpu_n1)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
 
@@ -488,6 +523,7 @@ def main(argv=None):
     ap.add_argument("--ref-n", type=int, default=64)
     ap.add_argument("--cpu-n", type=int, default=96)
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-n1", type=int, default=128, help="single-thread oracle sample grid (0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args(argv)
     world, rank, local = dist_setup()

@@ -14,8 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libecho_b200.so")
-SOURCES = ["march.cu", "update.cu", "uct.cu", "api.cu", "metric_tables.cpp"]
-HEADERS = ["echo_dev.cuh", "echo_kernels.h", "metric_tables.h", "cell_physics.cuh"]
+SOURCES = ["march.cu", "fused.cu", "update.cu", "uct.cu", "api.cu", "metric_tables.cpp"]
+HEADERS = ["echo_dev.cuh", "echo_kernels.h", "metric_tables.h", "cell_physics.cuh", "march_impl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",

@@ -23,11 +23,11 @@ namespace {
 
 enum KernelClass {
   kSweepX = 0, kSweepY, kSweepZ, kUpdateStage, kUpdateRhs, kC2P, kMaxSpeed, kPrim2Cons, kGetPrims, kLayout,
-  kCflDt, kUctEmf, kUctInduct, kUctCell, kNanScan, kNumClasses
+  kCflDt, kUctEmf, kUctInduct, kUctCell, kNanScan, kUpdateSweepX, kNumClasses
 };
 const char* kNames[kNumClasses] = {"sweep_x",   "sweep_y",   "sweep_z",   "update_stage", "update_rhs",
                                    "con2prim",  "max_speed", "prim2cons", "get_prims",    "layout",
-                                   "cfl_dt",    "uct_emf",   "uct_induct", "uct_cell", "nan_scan"};
+                                   "cfl_dt",    "uct_emf",   "uct_induct", "uct_cell", "nan_scan", "update_sweep_x"};
 
 std::string g_create_error;
 
@@ -57,6 +57,13 @@ struct echo_ctx {
   double* Us = nullptr;   // U^s
   double* P = nullptr;    // rho, u~, p, B
   double* R = nullptr;    // rhs + EMF accumulator
+  // fused update + x sweep (fused.cu): the update of a stage writes the x sweep of the state it
+  // produces into the OTHER accumulator (its own curl still reads this stage's EMF)
+  double* R2 = nullptr;   // second accumulator (fuse only)
+  int rsel = 0;           // accumulator of the current stage input: 0 R, 1 R2
+  bool xahead = false;    // racc() already holds the x sweep of the current stage input
+  bool fuse = false;      // fused update + x sweep (Minkowski, no slabs, no UCT; opt-in ECHO_FUSED_UPDATE=1)
+  cudaGraphExec_t step_exec_p[2] = {nullptr, nullptr};  // echo_advance step graphs by entry rsel (fuse)
   // UCT (divb = 2, uct.cu): staggered field (slots 0..2 b^n, 3..5 b^s), face data per axis, edge EMFs
   double* Bst = nullptr;
   double* FS[3] = {nullptr, nullptr, nullptr};
@@ -122,6 +129,7 @@ static cudaError_t launch(echo_ctx* c, int cls, F&& f) {
   return e;
 }
 
+static double* racc(echo_ctx* c) { return c->rsel ? c->R2 : c->R; }
 static const double* ucur(echo_ctx* c) { return c->next_stage == 1 ? c->Un : c->Us; }
 static double* ucur_mut(echo_ctx* c) { return c->next_stage == 1 ? c->Un : c->Us; }
 
@@ -139,13 +147,14 @@ static double* bcur(echo_ctx* c) { return c->Bst + (c->next_stage == 1 ? 0 : 3) 
 // sweeps x, y, z of the current stage input P (B included) into R; UCT: then the edge EMFs
 static int run_sweeps(echo_ctx* c) {
   const bool uct = is_uct(c);
-  for (int ax = 0; ax < 3; ax++) {
+  for (int ax = c->xahead ? 1 : 0; ax < 3; ax++) {  // (the fused update already swept x)
     cudaError_t e = launch(c, kSweepX + ax, [&] {
-      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), c->R, c->st,
+      return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), racc(c), c->st,
                           uct ? bcur(c) : nullptr, uct ? c->FS[ax] : nullptr);
     });
     if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
   }
+  c->xahead = false;
   if (uct) {
     const double* fs[3] = {c->FS[0], c->FS[1], c->FS[2]};
     cudaError_t e = launch(c, kUctEmf, [&] { return launch_uct_emf(c->g, fs, bcur(c), c->Ed, c->st); });
@@ -207,7 +216,7 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
     });
     if (e == cudaSuccess)
       e = launch(c, kUctCell, [&] {
-        return launch_uct_cell(c->ks, c->g, c->e, c->mt, s, dt, dtp, c->R, c->Un, Uin, Uout, c->P, c->Bst, c->dcnt,
+        return launch_uct_cell(c->ks, c->g, c->e, c->mt, s, dt, dtp, racc(c), c->Un, Uin, Uout, c->P, c->Bst, c->dcnt,
                                cfl, c->st);
       });
     if (e != cudaSuccess) return cuda_fail(c, e, "uct update launch");
@@ -222,10 +231,21 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
     return ECHO_OK;
   }
   const GhostLinks gl = ghost_links(c, s);
-  cudaError_t e = launch(c, kUpdateStage, [&] {
-    return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, c->R, c->Un, Uin, Uout, c->P, nullptr,
-                         c->dcnt, cfl, c->st, &gl, dtp);
-  });
+  cudaError_t e;
+  if (c->fuse) {  // the update of stage s + the x sweep of the state it produces (fused.cu)
+    double* Rnew = c->rsel ? c->R : c->R2;
+    e = launch(c, kUpdateSweepX, [&] {
+      return launch_update_march(c->ks, c->g, c->e, c->mt, s, dt, dtp, racc(c), c->Un, Uin, Uout, c->P, c->dcnt, cfl,
+                                 Rnew, c->st);
+    });
+    c->rsel ^= 1;
+    c->xahead = true;
+  } else {
+    e = launch(c, kUpdateStage, [&] {
+      return launch_update(kModeStage, c->ks, c->g, c->e, c->mt, s, dt, racc(c), c->Un, Uin, Uout, c->P, nullptr,
+                           c->dcnt, cfl, c->st, &gl, dtp);
+    });
+  }
   if (e != cudaSuccess) return cuda_fail(c, e, "update launch");
   if (c->debug & ECHO_DEBUG_NANSCAN) {
     e = launch(c, kNanScan, [&] { return launch_nanscan(c->g, Uout, c->P, c->ks ? 8 : 5, c->dnan, dtp ? c->dadv : nullptr, c->st); });
@@ -370,6 +390,15 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     echo_destroy(c);
     return fail(nullptr, ECHO_E_OOM, "echo_create: device allocation failed");
   }
+  {  // fused update + x sweep (opt-in, ECHO_FUSED_UPDATE=1: measured slower): a second
+     // accumulator (without memory for it the kernels stay separate)
+    const char* fu = std::getenv("ECHO_FUSED_UPDATE");
+    c->fuse = !ks && !g.zhalo && g.divb != 2 && fu && fu[0] == '1';
+    if (c->fuse && cudaMalloc(&c->R2, sizeof(double) * rec) != cudaSuccess) {
+      cudaGetLastError();
+      c->fuse = false;
+    }
+  }
   if (g.divb == 2) {
     double** uct_arrays[5] = {&c->Bst, &c->FS[0], &c->FS[1], &c->FS[2], &c->Ed};
     for (double** a : uct_arrays)
@@ -443,6 +472,9 @@ void echo_destroy(echo_ctx* c) {
   cudaFree(c->dcnt);
   cudaFree(c->dbad);
   cudaFree(c->dnan);
+  cudaFree(c->R2);
+  for (auto& x : c->step_exec_p)
+    if (x) cudaGraphExecDestroy(x);
   cudaFree(c->tables);
   cudaFree(c->dadv);
   cudaFree(c->Bst);
@@ -503,6 +535,7 @@ int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
   c->have_faces = false;
   c->cfl_valid = false;
   c->next_stage = 1;
+  c->xahead = false;
   c->swept = 0;
   return ECHO_OK;
 }
@@ -576,6 +609,7 @@ int echo_set_face_field(echo_ctx* c, const double* b3, int on_device) {
   c->have_faces = true;
   c->cfl_valid = false;
   c->next_stage = 1;
+  c->xahead = false;
   c->swept = 0;
   return ECHO_OK;
 }
@@ -600,6 +634,7 @@ int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
   }
   CK(launch(c, kLayout, [&] { return launch_layout(c->g, src, c->Un, 8, false, c->st); }), "echo_set_cons");
   c->next_stage = 1;
+  c->xahead = false;
   c->swept = 0;  // a half-done stage (echo_stage_sweeps) of the old state is void
   return echo_con2prim(c, nullptr);
 }
@@ -618,7 +653,7 @@ int echo_rhs(echo_ctx* c, double* l8, int on_device) {
   int rc = run_sweeps(c);
   if (rc) return rc;
   cudaError_t e = launch(c, kUpdateRhs, [&] {
-    return launch_update(kModeRhs, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, nullptr, c->P, dst, c->dcnt,
+    return launch_update(kModeRhs, c->ks, c->g, c->e, c->mt, 0, 0.0, racc(c), U, U, nullptr, c->P, dst, c->dcnt,
                          nullptr, c->st);
   });
   if (e != cudaSuccess) return cuda_fail(c, e, "update(rhs) launch");
@@ -644,6 +679,7 @@ int echo_con2prim(echo_ctx* c, echo_stats_t* delta) {
     before[1] = c->hpin[1];
   }
   double* U = ucur_mut(c);
+  c->xahead = false;  // the state changes
   CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_con2prim");
   cudaError_t e = launch(c, kC2P, [&] {
     return launch_update(kModeC2P, c->ks, c->g, c->e, c->mt, 0, 0.0, c->R, U, U, U, c->P, nullptr, c->dcnt,
@@ -726,17 +762,30 @@ static int issue_step_dev(echo_ctx* c, double cfl) {
   return ECHO_OK;
 }
 
-// capture issue_step_dev into c->step_exec (on a private stream: the caller's may be the
-// legacy default stream, which cannot be captured); host bookkeeping is restored after
-static int capture_step(echo_ctx* c, double cfl) {
-  if (c->step_exec) {
-    cudaGraphExecDestroy(c->step_exec);
-    c->step_exec = nullptr;
+static void drop_graphs(echo_ctx* c) {
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  c->step_exec = nullptr;
+  for (auto& x : c->step_exec_p) {
+    if (x) cudaGraphExecDestroy(x);
+    x = nullptr;
+  }
+}
+
+// capture issue_step_dev into *target (on a private stream: the caller's may be the legacy
+// default stream, which cannot be captured); host bookkeeping is restored after.  With the
+// fused update the accumulator parity alternates step by step (3 updates per step), so there
+// are two step graphs, one per entry parity (c->rsel at capture).
+static int capture_step(echo_ctx* c, double cfl, cudaGraphExec_t* target) {
+  if (*target) {
+    cudaGraphExecDestroy(*target);
+    *target = nullptr;
   }
   if (!c->cap_st) CK(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking), "echo_advance");
   const cudaStream_t user = c->st;
   const long long launches0 = c->launches;
   const unsigned long long stages0 = c->stages;
+  const int rsel0 = c->rsel;
+  const bool xahead0 = c->xahead;
   c->st = c->cap_st;
   CK(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal), "echo_advance capture");
   int rc = issue_step_dev(c, cfl);
@@ -746,12 +795,14 @@ static int capture_step(echo_ctx* c, double cfl) {
   c->step_kernels = c->launches - launches0;
   c->launches = launches0;
   c->stages = stages0;
+  c->rsel = rsel0;
+  c->xahead = xahead0;
   if (rc) {
     if (graph) cudaGraphDestroy(graph);
     return rc;
   }
   if (e != cudaSuccess) return cuda_fail(c, e, "echo_advance capture");
-  e = cudaGraphInstantiate(&c->step_exec, graph, 0);
+  e = cudaGraphInstantiate(target, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return cuda_fail(c, e, "echo_advance instantiate");
   c->step_cfl = cfl;
@@ -781,10 +832,7 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
     if (cudaMalloc(&c->dadv, sizeof(double) * (4 + ncap)) != cudaSuccess)
       return fail(c, ECHO_E_OOM, "echo_advance: dt log allocation failed");
     c->dlog_cap = ncap;
-    if (c->step_exec) {
-      cudaGraphExecDestroy(c->step_exec);
-      c->step_exec = nullptr;
-    }
+    drop_graphs(c);
   }
   if (!c->cfl_valid) {  // the first dt needs the reduction of the current state
     CK(cudaMemsetAsync(c->dcnt + 2, 0, sizeof(unsigned long long), c->st), "echo_advance");
@@ -800,13 +848,23 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
       if (rc) return rc;
     }
   } else {
-    if (!c->step_exec || c->step_cfl != cfl) {
-      int rc = capture_step(c, cfl);
-      if (rc) return rc;
+    if (c->fuse && !c->xahead) {  // the step graph starts from a swept x (its last update sweeps the next)
+      cudaError_t e = launch(c, kSweepX, [&] {
+        return launch_march(0, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), racc(c), c->st);
+      });
+      if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
+      c->xahead = true;
     }
+    if (c->step_cfl != cfl) drop_graphs(c);
     for (int n = 0; n < nsteps; n++) {
-      CK(cudaGraphLaunch(c->step_exec, c->st), "echo_advance graph launch");
+      cudaGraphExec_t& ex = c->fuse ? c->step_exec_p[c->rsel] : c->step_exec;
+      if (!ex) {
+        int rc = capture_step(c, cfl, &ex);
+        if (rc) return rc;
+      }
+      CK(cudaGraphLaunch(ex, c->st), "echo_advance graph launch");
       c->launches += c->step_kernels;
+      if (c->fuse) c->rsel ^= 1;  // three updates per step, each flips the accumulator
     }
   }
   // one readback for the whole loop: [dt, halt, steps done] and the dt log
@@ -818,6 +876,7 @@ int echo_advance(echo_ctx* c, int nsteps, double cfl, double* dt_log, int* steps
   c->steps += done;
   c->stages = stages0 + 3ull * done;
   if (steps_done) *steps_done = done;
+  if (adv[1] != 0.0) c->xahead = false;  // a halted loop skipped its later updates (and their x sweeps)
   if (adv[1] == 2.0) {  // the debug scan halted the loop
     c->cfl_valid = false;
     return nan_report(c, "echo_advance (debug scan)");
@@ -838,10 +897,7 @@ int echo_set_debug(echo_ctx* c, int flags) {
   const long long init = LLONG_MAX;
   CK(cudaMemcpyAsync(c->dnan, &init, sizeof init, cudaMemcpyHostToDevice, c->st), "echo_set_debug");
   CK(cudaStreamSynchronize(c->st), "echo_set_debug");
-  if (flags != c->debug && c->step_exec) {  // the captured step holds (or lacks) the scans
-    cudaGraphExecDestroy(c->step_exec);
-    c->step_exec = nullptr;
-  }
+  if (flags != c->debug) drop_graphs(c);  // the captured step holds (or lacks) the scans
   c->debug = flags;
   return ECHO_OK;
 }

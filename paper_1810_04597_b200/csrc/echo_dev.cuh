@@ -20,9 +20,9 @@ constexpr int kZH = 6; // stored z ghost planes per side in slab mode (kG + 1: t
 // compiler rebuilds each one with a pair of UMOVs at every use).
 //   [0..2] DER6 symmetric-sum weights 1067/960, -29/480, 3/640; [3..4] DER4 13/12, -1/24
 //   [5] WENO5 eps scaled by 3 (weno5_both), [6] 1/6 (FV candidates), [7] 4/3 (MP5 u_lc),
-//   [8] WENO-Z eps scaled by 3
-static __constant__ double kCst[9] = {1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0, 13.0 / 12.0, -1.0 / 24.0,
-                                      3.0e-6, 1.0 / 6.0, 4.0 / 3.0, 3.0e-40};
+//   [8] WENO-Z eps scaled by 3, [9] [10] point-form WENO5 eps scaled by 3/4 and -1.5 x that
+static __constant__ double kCst[11] = {1067.0 / 960.0, -29.0 / 480.0, 3.0 / 640.0, 13.0 / 12.0, -1.0 / 24.0,
+                                       3.0e-6, 1.0 / 6.0, 4.0 / 3.0, 3.0e-40, 0.75e-6, -1.125e-6};
 
 struct GridP {
   int n[3];
@@ -185,6 +185,7 @@ struct State {
   double Bl[3];      // B_i
   double B2, vB, b2;
   double rhoh, ptot;
+  double ZB;         // Z + B^2 (= tau + D + p_tot)
   double D, S[3], tau;
 };
 
@@ -212,12 +213,12 @@ ECHO_D void make_state(const M& m, const EosP& e, const double* pr, State& s) {
   s.b2 = s.B2 * s.W2i + s.vB * s.vB;
   s.rhoh = pr[0] + e.gfac * pr[4];
   s.ptot = pr[4] + 0.5 * s.b2;
-  double Z = s.rhoh * W2;
+  s.ZB = fma(s.rhoh, W2, s.B2);  // Z + B^2, Z = rho h W^2
   s.D = pr[0] * W;
 #pragma unroll
-  for (int i = 0; i < 3; i++) s.S[i] = (Z + s.B2) * s.vl[i] - s.vB * s.Bl[i];
+  for (int i = 0; i < 3; i++) s.S[i] = fma(s.ZB, s.vl[i], -s.vB * s.Bl[i]);
   // U = Z - p + (E^2 + B^2)/2 = Z + B^2 - p_tot  (E^2 = B^2 - b^2)
-  s.tau = Z + s.B2 - s.ptot - s.D;
+  s.tau = (s.ZB - s.ptot) - s.D;
 }
 
 // fast-speed bound along axis j (A4).  With N = Gamma p + b^2 and Dn = rho h + b^2,
@@ -233,20 +234,23 @@ ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, 
   const double vj = s.v[j];
   const double DmN = Dn - N;
   const double den = fma(-s.v2, N, Dn);
-  const double Q = N * (1.0 - s.v2) * fma(m.gi_diag(j), den, -vj * vj * DmN);
+  // 1 - v^2 = 1 / W^2 (exact in real arithmetic)
+  const double Q = (N * s.W2i) * fma(m.gi_diag(j), den, -vj * vj * DmN);
   const double sq = fsqrt(Q);
-  const double iden = m.alpha() * frcp(den);
-  const double c = vj * DmN;
-  lp = (c + sq) * iden - m.beta(j);
-  lm = (c - sq) * iden - m.beta(j);
+  const double iden = M::kFlat ? frcp(den) : m.alpha() * frcp(den);
+  const double c0 = M::kFlat ? vj * (DmN * iden) : fma(vj * DmN, iden, -m.beta(j));
+  lp = fma(sq, iden, c0);
+  lm = fma(-sq, iden, c0);
 }
 
-// densitised HLL flux (7 comps) between two reconstructed states at one face (A4)
+// densitised HLL flux (7 comps) between two reconstructed states at one face (A4), times
+// `scale` (the sweeps pass 1/Delta_a, so the flux difference of the DER values needs no
+// multiply: DER is linear)
 // fs (UCT, A38, A43): if not NULL, V^1..3 = alpha v^i - beta^i of the left and of the right
 // state, a+ = S_R, a- = -S_L
 template <class M>
 ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* pr, int AX, double* F,
-                     double* fs = nullptr) {
+                     double* fs = nullptr, double scale = 1.0) {
   State sl, sr;
   make_state(m, e, pl, sl);
   make_state(m, e, pr, sr);
@@ -269,13 +273,13 @@ ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* 
   }
   const double den = sR - sL;
   if (den > 0.0) {
-    const double inv = m.sqrtg() * frcp(den);
+    const double inv = (M::kFlat ? scale : m.sqrtg() * scale) * frcp(den);
     const double a = sR * inv, b = sL * inv, c = sL * sR * inv;
 #pragma unroll
     for (int q = 0; q < 7; q++) F[q] = fma(c, uR[q] - uL[q], fma(a, fL[q], -b * fR[q]));
   } else {
 #pragma unroll
-    for (int q = 0; q < 7; q++) F[q] = 0.5 * (fL[q] + fR[q]) * m.sqrtg();
+    for (int q = 0; q < 7; q++) F[q] = (fL[q] + fR[q]) * (0.5 * m.sqrtg() * scale);
   }
 }
 
@@ -289,9 +293,8 @@ ECHO_D void cons_flux(const M& m, const State& s, int j, double* u, double* f) {
   const double bj = m.beta(j);
   const double Vj = a * s.v[j] - bj;
   const double bbar = s.B[j] * s.W2i + s.vB * s.v[j];
-  // Z + B^2 = tau + D + p_tot
-  const double ZB = s.tau + s.D + s.ptot;
-  const double Sj = ZB * s.v[j] - s.vB * s.B[j];
+  // S^j = (Z + B^2) v^j - (v.B) B^j (flat: S^j = S_j)
+  const double Sj = M::kFlat ? s.S[j] : fma(s.ZB, s.v[j], -s.vB * s.B[j]);
   u[0] = s.D;
   f[0] = Vj * s.D;
 #pragma unroll
@@ -335,9 +338,22 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
   //   3 beta_2 = 10 dp^2 - 11 dp dpp + 4 dpp^2
   // (positive definite, so no cancellation beyond a few ulp); eps -> 3 eps.
   const double m2 = dm * dm, p2 = dp * dp;
-  double s0 = fma(10.0, m2, fma(dmm, fma(4.0, dmm, -11.0 * dm), eps3));
-  double s1 = fma(4.0, m2, fma(4.0, p2, fma(-5.0 * dm, dp, eps3)));
-  double s2 = fma(10.0, p2, fma(dpp, fma(4.0, dpp, -11.0 * dp), eps3));
+  double s0, s1, s2;
+  if constexpr (REC == 0) {
+    // point form: the three scaled by 1/4 (the weights depend on ratios only), eps -> 3 eps / 4,
+    // written so that every coefficient-1 term rides in an FMA (10 operations instead of 14):
+    //   s0 = dmm (dmm - 2.75 dm) + 2.5 dm^2 + e,  s1 = dm (dm - 1.25 dp) + dp^2 + e,
+    //   s2 = dpp (dpp - 2.75 dp) + 2.5 dp^2 + e = dpp (...) + 2.5 (dp^2 + e) - 1.5 e
+    const double e4 = kCst[9];
+    const double pe = fma(dp, dp, e4);
+    s0 = fma(dmm, fma(-2.75, dm, dmm), fma(2.5, m2, e4));
+    s1 = fma(dm, fma(-1.25, dp, dm), pe);
+    s2 = fma(dpp, fma(-2.75, dp, dpp), fma(2.5, pe, kCst[10]));
+  } else {
+    s0 = fma(10.0, m2, fma(dmm, fma(4.0, dmm, -11.0 * dm), eps3));
+    s1 = fma(4.0, m2, fma(4.0, p2, fma(-5.0 * dm, dp, eps3)));
+    s2 = fma(10.0, p2, fma(dpp, fma(4.0, dpp, -11.0 * dp), eps3));
+  }
   if constexpr (REC == 3) {
     // WENO-Z: alpha_k = d_k (1 + tau5 / s_k), tau5 = |s_0 - s_2| (the common factor 3 of s_k and
     // tau5 cancels); times s_0 s_1 s_2: A_k = (s_k + tau5) prod_{l != k} s_l.  The mirror face

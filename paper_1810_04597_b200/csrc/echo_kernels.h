@@ -47,6 +47,14 @@ cudaError_t launch_update(int mode, bool ks, const GridP& g, const EosP& e, cons
                           unsigned long long* counters, unsigned long long* cfl_out, cudaStream_t st,
                           const GhostLinks* links = nullptr, const double* dtp = nullptr);
 
+// K3 of stage s (as launch_update kModeStage, reading the accumulator Rold) fused with the x
+// sweep of the new state into the accumulator Rnew (fused.cu; not in slab or UCT mode:
+// cudaErrorInvalidValue).  Bit-for-bit the same results as the two separate kernels.
+cudaError_t launch_update_march(bool ks, const GridP& g, const EosP& e, const MetTables& mt, int s, double dt,
+                                const double* dtp, const double* Rold, const double* Un, const double* Us, double* Uout,
+                                double* P, unsigned long long* counters, unsigned long long* cfl_out, double* Rnew,
+                                cudaStream_t st);
+
 // device-driven time loop: dtp = adv = [dt, halt, steps done] (doubles); launch_update with
 // dtp set reads dt from adv[0] and does nothing once adv[1] != 0.  k_cfl_dt sets
 // adv[0] = cfl / m from the CFL reduction bits (halt on m <= 0 or non-finite) and appends
