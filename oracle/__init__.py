@@ -144,6 +144,7 @@ def lib():
             "orc_mc2_left": (C.c_double, [_D]),
             "orc_ppm_left": (C.c_double, [_D]),
             "orc_der": (C.c_double, [_D, C.c_int]),
+            "orc_charrec_face_pt": (C.c_int, [P, _D, C.c_int, _D, _D]),
             "orc_c2p_pt": (C.c_int, [P, _D, _D, _D, _D, C.POINTER(C.c_int)]),
             "orc_set_prims": (C.c_int, [P, _D, _D, _D, _LL]),
             "orc_get_prims": (C.c_int, [P, _D, _D, _D]),
@@ -247,6 +248,14 @@ def mc2_left(u) -> float:
 
 def ppm_left(u) -> float:
     return float(lib().orc_ppm_left(_p(_v(u, 5))))
+
+
+def charrec_face(cfg: Cfg, st, a: int):
+    """rec = 6 (A44) at one face: st[6][8] prims of cells i-2..i+3 -> (qL, qR) hydro slots 0..4."""
+    st = np.ascontiguousarray(np.asarray(st, dtype=np.float64).reshape(6, 8))
+    qL, qR = np.zeros(8), np.zeros(8)
+    lib().orc_charrec_face_pt(C.byref(cfg.c()), _p(st), int(a), _p(qL), _p(qR))
+    return qL[:5].copy(), qR[:5].copy()
 
 
 def der(F, order: int = 6) -> float:

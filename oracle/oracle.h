@@ -57,7 +57,10 @@ typedef struct {
                         2 MP5 (Suresh & Huynh 1997, point values, A33),
                         3 WENO-Z (Borges et al. 2008, point values, A34),
                         4 MC2 (monotonized-central limited linear, A35),
-                        5 PPM (Colella & Woodward 1984 on point values, A36) */
+                        5 PPM (Colella & Woodward 1984 on point values, A36),
+                        6 characteristic-wise WENO5 of the hydro primitives (eigenvectors of
+                          the flat-space relativistic-Euler Jacobian at the face, A44; B^i
+                          component-wise; Minkowski only, not with divb = 2) */
   int der;           /* 6 DER6, 4 DER4, 2 plain difference (A5) */
   int divb;          /* 0 field-CD (A6), 1 none: plain flux difference for B,
                         2 UCT: staggered field + upwind constrained transport (A37-A41;
@@ -98,6 +101,10 @@ double orc_wenoz_left(const double u[5]);
 double orc_mc2_left(const double u[5]);
 /* PPM left state at i+1/2 (u_R of cell i) from u[0..4] (A36) */
 double orc_ppm_left(const double u[5]);
+/* rec = 6 (A44) at one face: st[8*m + v] = prims (rho, u~^i, p, B^i) of cells i-2+m, m = 0..5;
+ * writes the hydro slots 0..4 of the left / right states qL, qR at face i+1/2 along axis a
+ * (slots 5..7 zero).  Returns 0. */
+int orc_charrec_face_pt(const orc_cfg* c, const double st[48], int a, double qL[8], double qR[8]);
 /* DER correction at the centre face from F[0..4] = F_{i-3/2..i+5/2}; der = 6/4/2 */
 double orc_der(const double F[5], int der);
 /* con2prim at one cell: non-densitised cons u, guess prims (for Z0), result prims.

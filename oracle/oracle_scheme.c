@@ -239,6 +239,150 @@ static void der_face(const orc_cfg* c, const double F5[5][8], const int rough5[5
   }
 }
 
+/* ------------------------------------------------------------------ */
+/* rec = 6: characteristic-wise WENO5 of the hydro primitives (A44)     */
+/* ------------------------------------------------------------------ */
+/* Plain Gauss-Jordan inverse with partial pivoting of an n x n matrix (n <= 5). */
+static void invert5(int n, const double A[5][5], double X[5][5]) {
+  double M[5][10];
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < 2 * n; j++) M[i][j] = j < n ? A[i][j] : (j - n == i ? 1.0 : 0.0);
+  for (int col = 0; col < n; col++) {
+    int piv = col;
+    for (int r = col + 1; r < n; r++)
+      if (fabs(M[r][col]) > fabs(M[piv][col])) piv = r;
+    if (piv != col)
+      for (int j = 0; j < 2 * n; j++) {
+        double t = M[col][j];
+        M[col][j] = M[piv][j];
+        M[piv][j] = t;
+      }
+    double d = M[col][col];
+    for (int j = 0; j < 2 * n; j++) M[col][j] /= d;
+    for (int r = 0; r < n; r++) {
+      if (r == col) continue;
+      double f = M[r][col];
+      for (int j = 0; j < 2 * n; j++) M[r][j] -= f * M[col][j];
+    }
+  }
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < n; j++) X[i][j] = M[i][n + j];
+}
+
+/* Reading A44, step by step.  q = (rho, u~^n, u~^t1, u~^t2, p) with n = a, t1 = a+1, t2 = a+2
+ * (cyclic), the hydro primitives of A3 in the sweep's own frame.  Flat metric only.
+ *  1. face state qbar = (q_i + q_{i+1}) / 2 (cells st[2], st[3]);
+ *  2. its right eigenvectors, the flat-space relativistic-Euler Jacobian A = (dU/dq)^-1 dF^n/dq
+ *     with B = 0: in w = (rho, v^n, v^t1, v^t2, p) they are (SURVEY §8(c) A4 gives the speeds)
+ *       r_-  = (1, k_-(1 - v^n l_-), -k_- l_- v^t1, -k_- l_- v^t2, G p / rho),  l_- = lambda_-
+ *       r_0  = (1, 0, 0, 0, 0)       (contact: lambda = v^n)
+ *       r_t1 = (0, 0, 1, 0, 0), r_t2 = (0, 0, 0, 1, 0)   (shear: lambda = v^n)
+ *       r_+  as r_- with lambda_+,   k_+- = (G p / rho) / (rho h W^2 (lambda_+- - v^n));
+ *     mapped to q by dq = blockdiag(1, W (I + W^2 v v^T), 1) dw;
+ *  3. L = R^-1 (Gauss-Jordan);
+ *  4. characteristic variables c_k(m) = L_k . q_m of cells m = i-2 .. i+3;
+ *  5. WENO5 point form (A2) of each: c_k^L from m = 0..4, c_k^R the mirror from m = 5..1;
+ *  6. q^L = R c^L, q^R = R c^R.
+ * Writes the 5 hydro slots of qL, qR (the order rho, u~^1, u~^2, u~^3, p of the state). */
+static void char_rec_face(const orc_cfg* c, const double st[6][8], int a, double qL[8], double qR[8]) {
+  const double G_ = c->gamma;
+  const int comp[3] = {a, (a + 1) % 3, (a + 2) % 3};
+  double qs[6][5];
+  for (int m = 0; m < 6; m++) {
+    qs[m][0] = st[m][0];
+    for (int d = 0; d < 3; d++) qs[m][1 + d] = st[m][1 + comp[d]];
+    qs[m][4] = st[m][4];
+  }
+  /* 1. */
+  double qb[5];
+  for (int v = 0; v < 5; v++) qb[v] = 0.5 * (qs[2][v] + qs[3][v]);
+  const double rho = qb[0], p = qb[4];
+  const double uu = qb[1] * qb[1] + qb[2] * qb[2] + qb[3] * qb[3];
+  const double W = sqrt(1.0 + uu);
+  double v[3];
+  for (int d = 0; d < 3; d++) v[d] = qb[1 + d] / W;
+  const double v2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+  const double h = 1.0 + G_ / (G_ - 1.0) * p / rho;
+  const double cs2 = G_ * p / (rho * h);
+  const double gp = G_ * p / rho;
+  /* 2. */
+  const double disc = cs2 * (1.0 - v2) * (1.0 - v2 * cs2 - v[0] * v[0] * (1.0 - cs2));
+  const double lam[2] = {(v[0] * (1.0 - cs2) - sqrt(disc)) / (1.0 - v2 * cs2),
+                         (v[0] * (1.0 - cs2) + sqrt(disc)) / (1.0 - v2 * cs2)};
+  double Rw[5][5] = {{0}};
+  for (int s = 0; s < 2; s++) {
+    const int col = s == 0 ? 0 : 4;
+    const double k = gp / (rho * h * W * W * (lam[s] - v[0]));
+    Rw[0][col] = 1.0;
+    Rw[1][col] = k * (1.0 - v[0] * lam[s]);
+    Rw[2][col] = -k * lam[s] * v[1];
+    Rw[3][col] = -k * lam[s] * v[2];
+    Rw[4][col] = gp;
+  }
+  Rw[0][1] = 1.0;
+  Rw[2][2] = 1.0;
+  Rw[3][3] = 1.0;
+  double Mv[3][3];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) Mv[i][j] = W * ((i == j ? 1.0 : 0.0) + W * W * v[i] * v[j]);
+  double R[5][5];
+  for (int col = 0; col < 5; col++) {
+    R[0][col] = Rw[0][col];
+    R[4][col] = Rw[4][col];
+    for (int i = 0; i < 3; i++) {
+      double sum = 0.0;
+      for (int j = 0; j < 3; j++) sum += Mv[i][j] * Rw[1 + j][col];
+      R[1 + i][col] = sum;
+    }
+  }
+  /* 3. */
+  double L[5][5];
+  invert5(5, R, L);
+  /* 4.-5. */
+  double cL[5], cR[5];
+  for (int k = 0; k < 5; k++) {
+    double ch[6];
+    for (int m = 0; m < 6; m++) {
+      double sum = 0.0;
+      for (int vv = 0; vv < 5; vv++) sum += L[k][vv] * qs[m][vv];
+      ch[m] = sum;
+    }
+    double l[5], r[5];
+    for (int m = 0; m < 5; m++) l[m] = ch[m];
+    for (int m = 0; m < 5; m++) r[m] = ch[5 - m];
+    cL[k] = orc_weno5_left(l, 0);
+    cR[k] = orc_weno5_left(r, 0);
+  }
+  /* 6. */
+  double fl[5], fr[5];
+  for (int vv = 0; vv < 5; vv++) {
+    double sl = 0.0, sr = 0.0;
+    for (int k = 0; k < 5; k++) {
+      sl += R[vv][k] * cL[k];
+      sr += R[vv][k] * cR[k];
+    }
+    fl[vv] = sl;
+    fr[vv] = sr;
+  }
+  qL[0] = fl[0];
+  qR[0] = fr[0];
+  qL[4] = fl[4];
+  qR[4] = fr[4];
+  for (int d = 0; d < 3; d++) {
+    qL[1 + comp[d]] = fl[1 + d];
+    qR[1 + comp[d]] = fr[1 + d];
+  }
+}
+
+int orc_charrec_face_pt(const orc_cfg* c, const double st[48], int a, double qL[8], double qR[8]) {
+  double s6[6][8];
+  for (int m = 0; m < 6; m++)
+    for (int v = 0; v < 8; v++) s6[m][v] = st[8 * m + v];
+  for (int v = 0; v < 8; v++) qL[v] = qR[v] = 0.0;
+  char_rec_face(c, s6, a, qL, qR);
+  return 0;
+}
+
 /* Face flux at face i+1/2 from the stencil st[m][v] = prims of cells i-2+m,
  * m = 0..5, v = 0..7; xf = face coordinates; a = axis.  Shared by both paths.
  * UCT (divb = 2, A37): bnorm -> the staggered sqrt(gamma) B^a of this face, whose
@@ -250,13 +394,14 @@ static void der_face(const orc_cfg* c, const double F5[5][8], const int rough5[5
 static int face_flux(const orc_cfg* c, const double st[6][8], const double xf[3], int a, double F[8],
                      const double* bnorm, double fs[8]) {
   double qL[8], qR[8];
-  for (int v = 0; v < 8; v++) {
+  for (int v = (c->rec == 6 ? 5 : 0); v < 8; v++) {  /* rec 6: B^i component-wise WENO5 (A44) */
     double l[5], r[5];
     for (int m = 0; m < 5; m++) l[m] = st[m][v];     /* cells i-2 .. i+2 */
     for (int m = 0; m < 5; m++) r[m] = st[5 - m][v]; /* cells i+3 .. i-1 (mirror) */
-    qL[v] = orc_rec_left(l, c->rec);
-    qR[v] = orc_rec_left(r, c->rec);
+    qL[v] = orc_rec_left(l, c->rec == 6 ? 0 : c->rec);
+    qR[v] = orc_rec_left(r, c->rec == 6 ? 0 : c->rec);
   }
+  if (c->rec == 6) char_rec_face(c, st, a, qL, qR); /* the hydro states (A44) */
   /* A25 positivity fallback: a non-positive reconstructed rho or p takes the
    * value of the cell the state was reconstructed in */
   if (!(qL[0] > 0.0)) qL[0] = st[2][0];
@@ -392,6 +537,7 @@ static void uct_emf_induction(const orc_cfg* c, const double* FS, const double* 
 
 /* L(U) on every owned cell; UCT (b3 != NULL): slots 5..7 receive L(b^a) at the faces */
 static int rhs_full(const orc_cfg* c, const double* U8, const double* P5, const double* b3, double* L8) {
+  if (c->rec == 6 && (c->metric != ORC_MINKOWSKI || c->divb == 2)) return -1; /* A44: flat, no UCT */
   const long long n0 = c->n[0], n1 = c->n[1], n2 = c->n[2], N = ncells(c);
   int nt = nthreads_of(c);
   double* FS = NULL; /* UCT face data [axis][8][N] of the faces i_a + 1/2 owned by the cells */
@@ -617,6 +763,7 @@ static void rhs_cell(const orc_cfg* c, const double* U8, const double* P5, const
 int orc_rhs_cells(const orc_cfg* c, const double* U8, const double* P5, long long ncell, const long long* idx,
                   double* out) {
   if (c->divb == 2) return -1; /* UCT: full-grid path only */
+  if (c->rec == 6 && c->metric != ORC_MINKOWSKI) return -1; /* A44: flat metric only */
   int nt = nthreads_of(c);
 #pragma omp parallel for num_threads(nt) schedule(dynamic)
   for (long long m = 0; m < ncell; m++) rhs_cell(c, U8, P5, &idx[3 * m], &out[8 * m]);
@@ -689,6 +836,7 @@ int orc_stage(const orc_cfg* c, int s, double dt, const double* Un, const double
 int orc_stage_cells(const orc_cfg* c, int s, double dt, const double* Un, const double* Us, const double* Ps,
                     long long ncell, const long long* idx, double* Uout, double* Pout, orc_counts* cnt) {
   if (c->divb == 2) return -1; /* UCT: full-grid path only */
+  if (c->rec == 6 && c->metric != ORC_MINKOWSKI) return -1; /* A44: flat metric only */
   long long nfl = 0, nfa = 0;
   int nt = nthreads_of(c);
 #pragma omp parallel for num_threads(nt) schedule(dynamic) reduction(+ : nfl, nfa)

@@ -285,6 +285,50 @@ def derf(F, order):
     return F[2]
 
 
+# --------------------------------------------- characteristic-wise WENO5 (A44)
+def char_rec(G: Grid, st, ax):
+    """Hydro face states (rho, u~^1..3, p) at face i+1/2 from prims st[0..5] of cells i-2..i+3:
+    the right eigenvectors of the flat relativistic-Euler Jacobian at the mean of cells i, i+1,
+    written in w = (rho, v^n, v^t1, v^t2, p) and pushed to q = (rho, u~^n, u~^t1, u~^t2, p) by
+    du~ = W (I + W^2 v v^T) dv; L from mpmath's matrix inverse; WENO5 point form per field."""
+    n, t1, t2 = ax, (ax + 1) % 3, (ax + 2) % 3
+    order = [0, 1 + n, 1 + t1, 1 + t2, 4]            # frame slot -> state slot
+    qs = [[cell[k] for k in order] for cell in st]
+    qb = [(qs[2][k] + qs[3][k]) / 2 for k in range(5)]
+    ut = qb[1:4]
+    W = mp.sqrt(1 + sum(x * x for x in ut))
+    v = [x / W for x in ut]
+    vv = sum(x * x for x in v)
+    rho, p, gam = qb[0], qb[4], G.gamma
+    h = 1 + gam * p / ((gam - 1) * rho)
+    c2 = gam * p / (rho * h)
+    root = mp.sqrt(c2 * (1 - vv) * (1 - vv * c2 - v[0] ** 2 * (1 - c2)))
+    Rw = mp.matrix(5, 5)
+    for col, sgn in ((0, -1), (4, 1)):
+        lam = (v[0] * (1 - c2) + sgn * root) / (1 - vv * c2)
+        kap = (gam * p / rho) / (rho * h * W ** 2 * (lam - v[0]))
+        Rw[0, col], Rw[1, col] = 1, kap * (1 - v[0] * lam)
+        Rw[2, col], Rw[3, col], Rw[4, col] = -kap * lam * v[1], -kap * lam * v[2], gam * p / rho
+    Rw[0, 1] = Rw[2, 2] = Rw[3, 3] = 1
+    T = mp.eye(5)
+    for i in range(3):
+        for j in range(3):
+            T[1 + i, 1 + j] = W * ((1 if i == j else 0) + W ** 2 * v[i] * v[j])
+    R = T * Rw
+    L = mp.inverse(R)
+    cL, cR = [], []
+    for k in range(5):
+        ch = [sum(L[k, j] * qs[m][j] for j in range(5)) for m in range(6)]
+        cL.append(weno(ch[0:5], 0))
+        cR.append(weno(ch[5:0:-1], 0))
+    fl = [sum(R[j, k] * cL[k] for k in range(5)) for j in range(5)]
+    fr = [sum(R[j, k] * cR[k] for k in range(5)) for j in range(5)]
+    outL, outR = [mp.mpf(0)] * 5, [mp.mpf(0)] * 5
+    for f, slot in enumerate(order):
+        outL[slot], outR[slot] = fl[f], fr[f]
+    return outL, outR
+
+
 # ------------------------------------------------------------- scheme
 class Scheme:
     """L(U) on every owned cell of a tiny grid, from fp64 state arrays (converted exactly to mp)."""
@@ -318,8 +362,12 @@ class Scheme:
             cc = list(cell)
             cc[ax] = cell[ax] - 2 + mm
             st.append(self.prim(*cc))
-        qL = [rec_left([st[mm][v] for mm in range(5)], G.rec) for v in range(8)]
-        qR = [rec_left([st[5 - mm][v] for mm in range(5)], G.rec) for v in range(8)]
+        rec = 0 if G.rec == 6 else G.rec
+        qL = [rec_left([st[mm][v] for mm in range(5)], rec) for v in range(8)]
+        qR = [rec_left([st[5 - mm][v] for mm in range(5)], rec) for v in range(8)]
+        if G.rec == 6:  # A44: the hydro states from the characteristic fields
+            hL, hR = char_rec(G, st, ax)
+            qL[:5], qR[:5] = hL, hR
         if not qL[0] > 0:
             qL[0] = st[2][0]
         if not qL[4] > 0:

@@ -35,7 +35,8 @@ def test_bruteforce_periodic_turbulence(orc):
     _compare(orc, c, G, P8)
 
 
-@pytest.mark.parametrize("divb,der,rec", [(1, 4, 0), (0, 6, 1), (0, 6, 2), (1, 6, 2), (0, 6, 3), (0, 2, 4), (0, 4, 5)])
+@pytest.mark.parametrize("divb,der,rec", [(1, 4, 0), (0, 6, 1), (0, 6, 2), (1, 6, 2), (0, 6, 3), (0, 2, 4), (0, 4, 5),
+                                          (0, 6, 6), (1, 6, 6)])
 def test_bruteforce_switches(orc, divb, der, rec):
     p = I.problem(0, n=(4, 4, 4), seed=12)
     p.params.update(amp=0.2, vmax=0.5)
@@ -45,7 +46,7 @@ def test_bruteforce_switches(orc, divb, der, rec):
     _compare(orc, c, G, P8)
 
 
-@pytest.mark.parametrize("rec", [0, 2, 3, 4, 5])
+@pytest.mark.parametrize("rec", [0, 2, 3, 4, 5, 6])
 def test_bruteforce_outflow_blast(orc, rec):
     # outflow in x and y, periodic z; a pressure jump exercises the positivity fallback
     # (and, rec=2, the MP5 limiter)
