@@ -34,7 +34,7 @@ BYTES_PER_ZONE_STEP = 752.0      # compulsory traffic per zone-update, DESIGN.md
 FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9  # SMs x FP64 lanes x 2 flop/FMA x max clock
 # algorithmic FP64 flops per cell of one sweep launch (Minkowski, DER6, WENO5 point form), DESIGN.md §7
 FLOPS_PER_CELL_SWEEP = 901.0
-REC_NAMES = {0: "WENO5", 1: "WENO5-FV", 2: "MP5", 3: "WENO-Z", 4: "MC2", 5: "PPM"}
+REC_NAMES = {0: "WENO5", 1: "WENO5-FV", 2: "MP5", 3: "WENO-Z", 4: "MC2", 5: "PPM", 6: "characteristic-wise WENO5"}
 
 
 def load_peaks():
@@ -513,8 +513,9 @@ def main(argv=None):
     ap.add_argument("--slabs", type=int, default=2, help="--decomp on one GPU: slabs held by this process")
     ap.add_argument("--fused", action="store_true",
                     help="--decomp on one GPU: the update kernels store the neighbours' ghost planes (echo_halo_link)")
-    ap.add_argument("--rec", type=int, default=0, choices=[0, 1, 2, 3, 4, 5],
-                    help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5, 3 WENO-Z, 4 MC2, 5 PPM")
+    ap.add_argument("--rec", type=int, default=0, choices=[0, 1, 2, 3, 4, 5, 6],
+                    help="reconstruction: 0 WENO5 (default, the benchmarked scheme), 1 WENO5-FV, 2 MP5, 3 WENO-Z, 4 MC2, "
+                         "5 PPM, 6 characteristic-wise WENO5 (Minkowski)")
     ap.add_argument("--loop", choices=["device", "host"], default="device",
                     help="device: echo_advance (dt on the device, CUDA-graph step); host: echo_max_dt + echo_step per step")
     ap.add_argument("--divb", type=int, default=0, choices=[0, 1, 2],

@@ -76,7 +76,13 @@ typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_met
  *      2 = MP5 (Suresh & Huynh 1997 on point values, reading A33),
  *      3 = WENO-Z (Borges et al. 2008 weights on the point form, reading A34),
  *      4 = MC2, the monotonized-central limited linear reconstruction (reading A35),
- *      5 = PPM (Colella & Woodward 1984 constraints on point values, reading A36).
+ *      5 = PPM (Colella & Woodward 1984 constraints on point values, reading A36),
+ *      6 = characteristic-wise WENO5 of the hydro primitives (reading A44: per face, the
+ *          stencil's (rho, u~, p) projected on the left eigenvectors of the flat-space
+ *          relativistic-Euler Jacobian at the mean of the two adjacent cells, WENO5 point form
+ *          per characteristic field, projected back; B^i component-wise WENO5; SURVEY §8(f) f3
+ *          "characteristic-wise reconstruction").  Minkowski only and not with divb = 2
+ *          (ECHO_E_ARG at echo_create).
  * der: 6 = DER6 (A5, default), 4 = DER4, 2 = plain flux difference.
  * divb: 0 = field-CD constrained transport (A6, default), 1 = none, 2 = UCT: staggered
  *   field + upwind constrained transport (readings A37-A41; echo_set_face_field below).
@@ -181,6 +187,15 @@ int echo_stage(echo_ctx* ctx, int s, double dt);
  * fused ghost stores of echo_halo_link).  In order, without other stage calls between. */
 int echo_stage_sweeps(echo_ctx* ctx, int s);
 int echo_stage_update(echo_ctx* ctx, int s, double dt);
+/* The sweeps of a slab stage in two parts, so that the halo exchange overlaps computation:
+ * echo_stage_sweeps_interior(s) runs the x and y sweeps over the owned planes, which read no
+ * ghost plane (call it right after echo_halo_export, while the messages are in flight);
+ * echo_stage_sweeps_boundary(s) runs the x and y sweeps of the first ghost plane on each side
+ * and the z sweep (call it after echo_halo_import / echo_halo_fill).  Together they equal
+ * echo_stage_sweeps(s) bit for bit; echo_stage_update(s, dt) follows.  Slab contexts only,
+ * not UCT (ECHO_E_ORDER). */
+int echo_stage_sweeps_interior(echo_ctx* ctx, int s);
+int echo_stage_sweeps_boundary(echo_ctx* ctx, int s);
 
 /* One full SSP-RK3 step (stages 1, 2, 3) with dt > 0.  Asynchronous. */
 int echo_step(echo_ctx* ctx, double dt);
@@ -205,10 +220,11 @@ int echo_advance(echo_ctx* ctx, int nsteps, double cfl, double* dt_log, int* ste
 int echo_stats(echo_ctx* ctx, echo_stats_t* out);
 
 /* ---- z-slab domain decomposition (ECHO_BC_HALO) ----
- * A halo message holds the P and U^s records of the ECHO_HALO_PLANES owned planes
- * next to one side: echo_halo_doubles(ctx) doubles (0 without halo boundaries),
- * an internal record layout that only echo_halo_import of a context with the same
- * n[0], n[1] reads.  side 0 = lower z, 1 = upper z.
+ * A halo message holds what the neighbour's sweeps read of the ECHO_HALO_PLANES owned
+ * planes next to one side — rho, u~^i, p and B^i of every cell (Minkowski: B from the
+ * stage-input U) — echo_halo_doubles(ctx) doubles (0 without halo boundaries), an
+ * internal layout that only echo_halo_import of a context with the same n[0], n[1] and
+ * metric reads.  side 0 = lower z, 1 = upper z.
  *   echo_halo_export(ctx, 0, buf, dev): planes 0..5 (for the lower neighbour's side 1)
  *   echo_halo_import(ctx, 0, buf, dev): ghost planes -6..-1 from the lower neighbour
  *   echo_halo_fill(ctx, side): a physical outflow side: ghost planes = the edge plane

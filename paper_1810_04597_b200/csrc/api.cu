@@ -52,6 +52,7 @@ struct echo_ctx {
     int nz = 0;
   } rlink[2];
   int swept = 0;                           // stage whose sweeps ran (echo_stage_sweeps), 0 = none
+  int swept_int = 0;                       // stage whose interior sweeps ran (echo_stage_sweeps_interior)
   size_t plane = 0;       // doubles per z plane of a record array (pitch n2)
   double* Un = nullptr;   // U^n
   double* Us = nullptr;   // U^s
@@ -144,15 +145,35 @@ static bool is_uct(const echo_ctx* c) { return c->g.divb == 2; }
 // the stage-input staggered field (UCT)
 static double* bcur(echo_ctx* c) { return c->Bst + (c->next_stage == 1 ? 0 : 3) * c->g.vs; }
 
-// sweeps x, y, z of the current stage input P (B included) into R; UCT: then the edge EMFs
-static int run_sweeps(echo_ctx* c) {
+// sweeps x, y, z of the current stage input P (B included) into R; UCT: then the edge EMFs.
+// part (slab mode, the halo exchange overlapped): 1 = x/y over the owned planes only (they read
+// no ghost plane), 2 = x/y over the first ghost plane of each side, then z; 0 = everything.
+static int run_sweeps(echo_ctx* c, int part = 0) {
   const bool uct = is_uct(c);
-  for (int ax = c->xahead ? 1 : 0; ax < 3; ax++) {  // (the fused update already swept x)
+  auto sweep = [&](int ax, PlaneRange zr) {
     cudaError_t e = launch(c, kSweepX + ax, [&] {
       return launch_march(ax, c->ks, c->g, c->e, c->mt, c->P, c->ks ? c->P : ucur(c), racc(c), c->st,
-                          uct ? bcur(c) : nullptr, uct ? c->FS[ax] : nullptr);
+                          uct ? bcur(c) : nullptr, uct ? c->FS[ax] : nullptr, zr);
     });
-    if (e != cudaSuccess) return cuda_fail(c, e, "sweep launch");
+    return e == cudaSuccess ? ECHO_OK : cuda_fail(c, e, "sweep launch");
+  };
+  if (part == 1 || part == 2) {
+    for (int ax = 0; ax < 2; ax++) {
+      if (part == 1) {
+        int rc = sweep(ax, PlaneRange{0, c->g.n[2]});
+        if (rc) return rc;
+      } else {
+        for (int zb : {-1, c->g.n[2]}) {
+          int rc = sweep(ax, PlaneRange{zb, 1});
+          if (rc) return rc;
+        }
+      }
+    }
+    return part == 2 ? sweep(2, PlaneRange{}) : ECHO_OK;
+  }
+  for (int ax = c->xahead ? 1 : 0; ax < 3; ax++) {  // (the fused update already swept x)
+    int rc = sweep(ax, PlaneRange{});
+    if (rc) return rc;
   }
   c->xahead = false;
   if (uct) {
@@ -228,6 +249,7 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
     c->stages++;
     c->next_stage = (s == 3) ? 1 : s + 1;
     c->swept = 0;
+  c->swept_int = 0;
     return ECHO_OK;
   }
   const GhostLinks gl = ghost_links(c, s);
@@ -255,6 +277,7 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
   c->stages++;
   c->next_stage = (s == 3) ? 1 : s + 1;
   c->swept = 0;
+  c->swept_int = 0;
   return ECHO_OK;
 }
 
@@ -309,7 +332,9 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     if (zh && grid->n[2] < ECHO_HALO_PLANES)
       return fail(nullptr, ECHO_E_ARG, "echo_create: a slab with halo boundaries needs n[2] >= ECHO_HALO_PLANES");
   }
-  if (grid->rec < 0 || grid->rec > 5) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..5");
+  if (grid->rec < 0 || grid->rec > 6) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..6");
+  if (grid->rec == 6 && (metric->kind != ECHO_METRIC_MINKOWSKI || grid->divb == 2))
+    return fail(nullptr, ECHO_E_ARG, "echo_create: rec = 6 (characteristic-wise, A44) needs the Minkowski metric and divb != 2");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
   if (grid->divb < 0 || grid->divb > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0, 1 or 2");
   if (grid->divb == 2) {  // UCT (A37, A42, A43): periodic or outflow axes (no slabs), any metric
@@ -537,6 +562,7 @@ int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
   c->next_stage = 1;
   c->xahead = false;
   c->swept = 0;
+  c->swept_int = 0;
   return ECHO_OK;
 }
 
@@ -611,6 +637,7 @@ int echo_set_face_field(echo_ctx* c, const double* b3, int on_device) {
   c->next_stage = 1;
   c->xahead = false;
   c->swept = 0;
+  c->swept_int = 0;
   return ECHO_OK;
 }
 
@@ -636,6 +663,7 @@ int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
   c->next_stage = 1;
   c->xahead = false;
   c->swept = 0;  // a half-done stage (echo_stage_sweeps) of the old state is void
+  c->swept_int = 0;
   return echo_con2prim(c, nullptr);
 }
 
@@ -705,7 +733,7 @@ int echo_stage(echo_ctx* c, int s, double dt) {
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage: no state (call echo_set_prims first)");
   if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_stage: divb = 2 needs echo_set_face_field first");
   if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage: s must be 1, 2 or 3");
-  if (s != c->next_stage || c->swept) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
+  if (s != c->next_stage || c->swept || c->swept_int) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage: dt > 0 violated");
   return run_stage(c, s, dt);
 }
@@ -929,9 +957,34 @@ int echo_stage_sweeps(echo_ctx* c, int s) {
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: no state");
   if (is_uct(c) && !c->have_faces) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: divb = 2 needs echo_set_face_field first");
   if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage_sweeps: s must be 1, 2 or 3");
-  if (s != c->next_stage || c->swept) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: stages must run in order");
+  if (s != c->next_stage || c->swept || c->swept_int) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps: stages must run in order");
   int rc = run_sweeps(c);
   if (rc) return rc;
+  c->swept = s;
+  return ECHO_OK;
+}
+
+int echo_stage_sweeps_interior(echo_ctx* c, int s) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_stage_sweeps_interior: no state");
+  if (!c->g.zhalo || is_uct(c))
+    return fail(c, ECHO_E_ORDER, "echo_stage_sweeps_interior: only for slab contexts (halo boundaries), not UCT");
+  if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage_sweeps_interior: s must be 1, 2 or 3");
+  if (s != c->next_stage || c->swept || c->swept_int)
+    return fail(c, ECHO_E_ORDER, "echo_stage_sweeps_interior: stages must run in order");
+  int rc = run_sweeps(c, 1);
+  if (rc) return rc;
+  c->swept_int = s;
+  return ECHO_OK;
+}
+
+int echo_stage_sweeps_boundary(echo_ctx* c, int s) {
+  if (!c) return ECHO_E_ARG;
+  if (c->swept_int != s || c->swept)
+    return fail(c, ECHO_E_ORDER, "echo_stage_sweeps_boundary: echo_stage_sweeps_interior(s) must come first");
+  int rc = run_sweeps(c, 2);
+  if (rc) return rc;
+  c->swept_int = 0;
   c->swept = s;
   return ECHO_OK;
 }
@@ -1025,34 +1078,58 @@ int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
 
 long long echo_halo_doubles(const echo_ctx* c) {
   if (!c || !c->g.zhalo) return 0;
-  return 2LL * ECHO_HALO_PLANES * (long long)c->plane;
+  return 8LL * c->g.vs * ECHO_HALO_PLANES * (long long)c->g.n[1];  // halo_copy: 8 slots x vs per row
 }
 
 // message = [P planes][U^s planes] of the ECHO_HALO_PLANES owned planes next to `side`
+// A halo message holds, for each of the ECHO_HALO_PLANES x n2 rows next to a side, what the
+// neighbour's sweeps read of a ghost cell: the primitives rho, u~, p (P slots 0..4) and B
+// (Minkowski: U slots 5..7 of the stage-input U; Kerr-Schild: P slots 5..7) — 8 vs doubles per
+// row, rows packed (P part first, then the U part).  Z0 (P slot 5, Minkowski) and the hydro U of
+// ghost cells are never read there.
+static int halo_copy(echo_ctx* c, int side, double* buf, bool out, int on_device, const char* where) {
+  const long long rows = (long long)ECHO_HALO_PLANES * c->g.n[1];
+  const long long k0 = out ? (side == 0 ? 0 : c->g.n[2] - ECHO_HALO_PLANES) : (side == 0 ? -ECHO_HALO_PLANES : c->g.n[2]);
+  const size_t pitchB = sizeof(double) * c->g.pitch;
+  const long long vs = c->g.vs;
+  cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : (out ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice);
+  struct Part {
+    double* arr;
+    long long slot0, nslot;
+  };
+  Part parts[2];
+  int np = 0;
+  if (c->ks) {
+    parts[np++] = {c->P, 0, 8};
+  } else {
+    parts[np++] = {c->P, 0, 5};
+    parts[np++] = {ucur_mut(c), 5, 3};
+  }
+  long long off = 0;
+  for (int q = 0; q < np; q++) {
+    const Part& pt = parts[q];
+    double* dev = pt.arr + k0 * (long long)c->plane + pt.slot0 * vs;
+    const size_t w = sizeof(double) * pt.nslot * vs;
+    cudaError_t e = out ? cudaMemcpy2DAsync(buf + off, w, dev, pitchB, w, rows, kind, c->st)
+                        : cudaMemcpy2DAsync(dev, pitchB, buf + off, w, w, rows, kind, c->st);
+    if (e != cudaSuccess) return cuda_fail(c, e, where);
+    off += pt.nslot * vs * rows;
+  }
+  if (!on_device) CK(cudaStreamSynchronize(c->st), where);
+  return ECHO_OK;
+}
+
 int echo_halo_export(echo_ctx* c, int side, double* buf, int on_device) {
   if (!c || !buf || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_export: bad argument") : ECHO_E_ARG;
   if (!c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_halo_export: the context has no halo boundary");
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_halo_export: no state");
-  const size_t blk = (size_t)ECHO_HALO_PLANES * c->plane;
-  const size_t k0 = side == 0 ? 0 : (size_t)(c->g.n[2] - ECHO_HALO_PLANES);
-  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  CK(cudaMemcpyAsync(buf, c->P + k0 * c->plane, sizeof(double) * blk, kind, c->st), "echo_halo_export");
-  CK(cudaMemcpyAsync(buf + blk, ucur(c) + k0 * c->plane, sizeof(double) * blk, kind, c->st), "echo_halo_export");
-  if (!on_device) CK(cudaStreamSynchronize(c->st), "echo_halo_export");
-  return ECHO_OK;
+  return halo_copy(c, side, buf, true, on_device, "echo_halo_export");
 }
 
 int echo_halo_import(echo_ctx* c, int side, const double* buf, int on_device) {
   if (!c || !buf || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_import: bad argument") : ECHO_E_ARG;
   if (!c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_halo_import: the context has no halo boundary");
-  const size_t blk = (size_t)ECHO_HALO_PLANES * c->plane;
-  const long long k0 = side == 0 ? -ECHO_HALO_PLANES : c->g.n[2];
-  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  CK(cudaMemcpyAsync(c->P + k0 * (long long)c->plane, buf, sizeof(double) * blk, kind, c->st), "echo_halo_import");
-  CK(cudaMemcpyAsync(ucur_mut(c) + k0 * (long long)c->plane, buf + blk, sizeof(double) * blk, kind, c->st),
-     "echo_halo_import");
-  if (!on_device) CK(cudaStreamSynchronize(c->st), "echo_halo_import");
-  return ECHO_OK;
+  return halo_copy(c, side, const_cast<double*>(buf), false, on_device, "echo_halo_import");
 }
 
 // a physical outflow side of a slab: every ghost plane = the owned edge plane (A13)

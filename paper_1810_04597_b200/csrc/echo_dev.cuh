@@ -480,6 +480,114 @@ ECHO_D void ppm_both(double um2, double um1, double u0, double up1, double up2, 
   qR = ppm_right_of(ppm_face(up2, up1, u0, um1), u0, ppm_face(up1, u0, um1, um2));
 }
 
+// ----------------------------------------- characteristic-wise WENO5 (rec = 6, A44)
+// One face of WENO5 point form (A2): the left-biased value at i+1/2 from u_{i-2..i+2} (the right
+// state at i+1/2 is this of the mirrored stencil u_{i+3..i-1}).  The same normalisation as
+// weno5_both (beta / 4, eps -> 3 eps / 4).
+ECHO_D double weno5_one(double um2, double um1, double u0, double up1, double up2) {
+  const double dmm = um1 - um2, dm = u0 - um1, dp = up1 - u0, dpp = up2 - up1;
+  const double e4 = kCst[9];
+  const double pe = fma(dp, dp, e4);
+  double s0 = fma(dmm, fma(-2.75, dm, dmm), fma(2.5, dm * dm, e4));
+  double s1 = fma(dm, fma(-1.25, dp, dm), pe);
+  double s2 = fma(dpp, fma(-2.75, dp, dpp), fma(2.5, pe, kCst[10]));
+  s0 *= s0;
+  s1 *= s1;
+  s2 *= s2;
+  const double p01 = s0 * s1, p02 = s0 * s2, p12 = s1 * s2;
+  const double C0 = fma(0.875, dm, -0.375 * dmm), C1 = fma(1.25, dm, 3.75 * dp), C2 = fma(3.125, dp, -0.625 * dpp);
+  const double SL = fma(5.0, p01, fma(10.0, p02, p12));
+  const double NL = fma(p01, C2, fma(p02, C1, p12 * C0));
+  return fma(NL, frcp(SL), u0);
+}
+
+// Reading A44 at one face i+1/2 along the sweep axis: q[m] = (rho, u~^n, u~^t1, u~^t2, p) of cells
+// i-2+m, m = 0..5, in the sweep's frame.  Projection with the closed-form LEFT eigenvectors of the
+// flat relativistic-Euler Jacobian at the mean of cells i and i+1 (the oracle inverts the right
+// ones numerically; exact in real arithmetic):
+//   w = (rho, v^n, v^t1, v^t2, p):  l_- = (0, -1, 0, 0, a_+/g) / Da,  l_0 = (1, 0, 0, 0, -1/g),
+//   l_t1 = (0, -v^t1 T, 1, 0, -v^t1 X),  l_t2 likewise,  l_+ = (0, 1, 0, 0, -a_-/g) / Da,
+//   a_+- = k_+-(1 - v^n lambda_+-), t_+- = -k_+- lambda_+-, k_+- = g / (rho h W^2 (lambda_+- - v^n)),
+//   g = Gamma p / rho, Da = a_+ - a_-, T = (t_+ - t_-) / Da, X = (t_- a_+ - t_+ a_-) / (g Da);
+//   in q (du~ = W (I + W^2 v v^T) dv) a row (l_rho, l_v, l_p) becomes (l_rho, (l_v - (l_v.v) v)/W, l_p).
+// WENO5 per characteristic field, then back with the right eigenvectors:
+//   rho = c_- + c_0 + c_+,  p = g (c_- + c_+),  u~ = W (z + W^2 v (v.z)),
+//   z = (c_- a_- + c_+ a_+, v^t1 (c_- t_- + c_+ t_+) + c_t1, v^t2 (c_- t_- + c_+ t_+) + c_t2).
+// fL / fR: the left / right hydro states at the face, frame order.
+ECHO_D void char_face(const EosP& e, const double (&q)[6][5], double* fL, double* fR) {
+  double qb[5];
+#pragma unroll
+  for (int k = 0; k < 5; k++) qb[k] = 0.5 * (q[2][k] + q[3][k]);
+  const double u2 = fma(qb[1], qb[1], fma(qb[2], qb[2], qb[3] * qb[3]));
+  const double W2 = 1.0 + u2;
+  const double iW = frsqrt(W2);
+  const double W = W2 * iW;
+  const double v[3] = {qb[1] * iW, qb[2] * iW, qb[3] * iW};
+  const double v2 = u2 * (iW * iW);
+  const double rho = qb[0], p = qb[4];
+  const double rhoh = fma(e.gfac, p, rho);
+  const double irho = frcp(rho * rhoh);                  // 1/rho and 1/(rho h) from one reciprocal
+  const double g = e.gamma * p * (rhoh * irho);          // Gamma p / rho
+  const double cs2 = e.gamma * p * (rho * irho);         // Gamma p / (rho h)
+  const double den = fma(-v2, cs2, 1.0);
+  const double disc = cs2 * (1.0 - v2) * fma(-v[0] * v[0], 1.0 - cs2, den);
+  const double sq = fsqrt(disc);
+  const double iden = frcp(den);
+  const double b = v[0] * (1.0 - cs2) * iden;
+  const double lp = fma(sq, iden, b), lm = fma(-sq, iden, b);
+  // k_+- = g / (rho h W^2 (lambda_+- - v^n)) through one reciprocal of the product
+  const double dp_ = lp - v[0], dm_ = lm - v[0];
+  const double ir = frcp(rhoh * W2 * dp_ * dm_);
+  const double kp = g * dm_ * ir, km = g * dp_ * ir;
+  const double ap = kp * fma(-v[0], lp, 1.0), am = km * fma(-v[0], lm, 1.0);
+  const double tp = -kp * lp, tm = -km * lm;
+  const double iDa = frcp(ap - am);
+  const double ig = frcp(g);
+  const double T = (tp - tm) * iDa, X = (tm * ap - tp * am) * (ig * iDa);
+  // left eigenvectors in q: e_ = (e_n - v^n v) / (W Da) for l_+ (l_- = -e_), l_t1, l_t2
+  const double iWD = iW * iDa;
+  const double en[3] = {(1.0 - v[0] * v[0]) * iWD, -v[0] * v[1] * iWD, -v[0] * v[2] * iWD};
+  double lt[2][3];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const double vt = v[1 + k];
+    const double lv[3] = {-vt * T, k == 0 ? 1.0 : 0.0, k == 0 ? 0.0 : 1.0};
+    const double dot = vt * fma(-T, v[0], 1.0);         // l_v . v
+#pragma unroll
+    for (int d = 0; d < 3; d++) lt[k][d] = fma(-dot, v[d], lv[d]) * iW;
+  }
+  const double pm = ap * ig * iDa, pp = -am * ig * iDa;  // p coefficients of l_- and l_+
+  double cl[5], cr[5];  // characteristic face values: -, 0, t1, t2, +
+#pragma unroll
+  for (int k = 0; k < 5; k++) {
+    double ch[6];
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+      const double eu = fma(en[0], q[m][1], fma(en[1], q[m][2], en[2] * q[m][3]));
+      if (k == 0) ch[m] = fma(pm, q[m][4], -eu);
+      else if (k == 4) ch[m] = fma(pp, q[m][4], eu);
+      else if (k == 1) ch[m] = fma(-ig, q[m][4], q[m][0]);
+      else {
+        const double* l = lt[k - 2];
+        ch[m] = fma(-v[k - 1] * X, q[m][4], fma(l[0], q[m][1], fma(l[1], q[m][2], l[2] * q[m][3])));
+      }
+    }
+    cl[k] = weno5_one(ch[0], ch[1], ch[2], ch[3], ch[4]);
+    cr[k] = weno5_one(ch[5], ch[4], ch[3], ch[2], ch[1]);
+  }
+  auto back = [&](const double* c, double* f) {
+    f[0] = c[0] + c[1] + c[4];
+    f[4] = g * (c[0] + c[4]);
+    const double tt = fma(c[0], tm, c[4] * tp);
+    const double z[3] = {fma(c[0], am, c[4] * ap), fma(v[1], tt, c[2]), fma(v[2], tt, c[3])};
+    const double vz = W2 * fma(v[0], z[0], fma(v[1], z[1], v[2] * z[2]));
+#pragma unroll
+    for (int d = 0; d < 3; d++) f[1 + d] = W * fma(vz, v[d], z[d]);
+  };
+  back(cl, fL);
+  back(cr, fR);
+}
+
 // reconstruction switch: REC 0/1 WENO5 (point / finite-volume form), 2 MP5, 3 WENO-Z, 4 MC2, 5 PPM
 template <int REC>
 ECHO_D void rec_both(double um2, double um1, double u0, double up1, double up2, double& qL, double& qR) {

@@ -18,9 +18,14 @@ namespace echo {
 // the stage-input U in Minkowski, where B^i = U_B)
 // UCT (divb = 2): Bface = the stage-input staggered field (slot a = b^a), FSo = this axis's
 // face-data array (uct.cu); NULL otherwise
+// zr (x/y sweeps only; zn = 0: every plane of the sweep, incl. the slab's first ghost planes):
+// sweep the planes zb .. zb + zn - 1 only (slab mode: the interior sweeps overlap the halo exchange)
+struct PlaneRange {
+  int zb = 0, zn = 0;
+};
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
                          const double* UB, double* R, cudaStream_t st, const double* Bface = nullptr,
-                         double* FSo = nullptr);
+                         double* FSo = nullptr, PlaneRange zr = PlaneRange{});
 
 // slab mode, fused ghost exchange: K3 also stores the new P and U of the owned planes
 // next to a linked side straight into the neighbour slab's ghost planes (peer memory:

@@ -141,6 +141,7 @@ static cudaError_t um_rec(const GridP& g, const EosP& e, const MetTables& mt, in
                           const double* Rold, const double* Un, const double* Us, double* Uout, double* P,
                           unsigned long long* cnt, unsigned long long* cfl, double* Rnew, cudaStream_t st) {
   switch (g.rec) {
+    case 6: return cudaErrorInvalidValue;  // (the fused kernel keeps the x sweep's register budget)
     case 1: return um_dm<KS, DER, 1>(g, e, mt, s, dt, dtp, Rold, Un, Us, Uout, P, cnt, cfl, Rnew, st);
     case 2: return um_dm<KS, DER, 2>(g, e, mt, s, dt, dtp, Rold, Un, Us, Uout, P, cnt, cfl, Rnew, st);
     case 3: return um_dm<KS, DER, 3>(g, e, mt, s, dt, dtp, Rold, Un, Us, Uout, P, cnt, cfl, Rnew, st);

@@ -6,7 +6,8 @@ namespace march {
 
 template <int AX, bool KS, int DER, int REC, int DM>
 static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB,
-                              double* R, const double* Bface, double* FSo, cudaStream_t st) {
+                              double* R, const double* Bface, double* FSo, cudaStream_t st,
+                              const PlaneRange& zr) {
   using GE = Geo<AX>;
   auto kern = k_march<AX, KS, DER, REC, DM>;
   // per device (the attribute and the occupancy are per-device properties); the cache is
@@ -25,7 +26,7 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
     grid_cap = sms * (per > 0 ? per : 1);
     if (dev < kMaxDev) grid_caps[dev].store(grid_cap, std::memory_order_relaxed);
   }
-  const LineGeom lg = make_line_geom<AX>(g, P, R);
+  const LineGeom lg = make_line_geom<AX>(g, P, R, zr);
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
   if (ECHO_PDL && AX != 0) {  // y/z: may start over the previous sweep's tail (griddepcontrol)
     cudaLaunchConfig_t cfg{};
@@ -46,42 +47,54 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
 
 template <int AX, bool KS, int DER, int REC>
 static cudaError_t launch_dn(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
-                             const double* Bface, double* FSo, cudaStream_t st) {
-  if (g.divb == 2) return launch_one<AX, KS, DER, REC, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (g.divb == 1) return launch_one<AX, KS, DER, REC, 1>(g, e, mt, P, UB, R, nullptr, nullptr, st);
-  return launch_one<AX, KS, DER, REC, 0>(g, e, mt, P, UB, R, nullptr, nullptr, st);
+                             const double* Bface, double* FSo, cudaStream_t st,
+                              const PlaneRange& zr) {
+  if constexpr (REC == 6) {  // A44: not with UCT (echo_create refuses it)
+    if (g.divb == 2) return cudaErrorInvalidValue;
+  } else {
+    if (g.divb == 2) return launch_one<AX, KS, DER, REC, 2>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  }
+  if (g.divb == 1) return launch_one<AX, KS, DER, REC, 1>(g, e, mt, P, UB, R, nullptr, nullptr, st, zr);
+  return launch_one<AX, KS, DER, REC, 0>(g, e, mt, P, UB, R, nullptr, nullptr, st, zr);
 }
 template <int AX, bool KS, int DER>
 static cudaError_t launch_rec(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
-                              const double* Bface, double* FSo, cudaStream_t st) {
-  if (g.rec == 5) return launch_dn<AX, KS, DER, 5>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (g.rec == 4) return launch_dn<AX, KS, DER, 4>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (g.rec == 3) return launch_dn<AX, KS, DER, 3>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (g.rec == 2) return launch_dn<AX, KS, DER, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, UB, R, Bface, FSo, st);
-  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, UB, R, Bface, FSo, st);
+                              const double* Bface, double* FSo, cudaStream_t st,
+                              const PlaneRange& zr) {
+  if (g.rec == 6) {  // A44: flat metric only (echo_create refuses Kerr-Schild)
+    if constexpr (KS) return cudaErrorInvalidValue;
+    else return launch_dn<AX, KS, DER, 6>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  }
+  if (g.rec == 5) return launch_dn<AX, KS, DER, 5>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  if (g.rec == 4) return launch_dn<AX, KS, DER, 4>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  if (g.rec == 3) return launch_dn<AX, KS, DER, 3>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  if (g.rec == 2) return launch_dn<AX, KS, DER, 2>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  if (g.rec == 1) return launch_dn<AX, KS, DER, 1>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  return launch_dn<AX, KS, DER, 0>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
 }
 template <int AX, bool KS>
 static cudaError_t launch_der(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB, double* R,
-                              const double* Bface, double* FSo, cudaStream_t st) {
-  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, UB, R, Bface, FSo, st);
-  return launch_rec<AX, KS, 6>(g, e, mt, P, UB, R, Bface, FSo, st);
+                              const double* Bface, double* FSo, cudaStream_t st,
+                              const PlaneRange& zr) {
+  if (g.der == 4) return launch_rec<AX, KS, 4>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  if (g.der == 2) return launch_rec<AX, KS, 2>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  return launch_rec<AX, KS, 6>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
 }
 
 }  // namespace march
 
 cudaError_t launch_march(int axis, bool ks, const GridP& g, const EosP& e, const MetTables& mt, const double* P,
-                         const double* UB, double* R, cudaStream_t st, const double* Bface, double* FSo) {
+                         const double* UB, double* R, cudaStream_t st, const double* Bface, double* FSo,
+                         PlaneRange zr) {
   using namespace march;
   if (ks) {
-    if (axis == 0) return launch_der<0, true>(g, e, mt, P, UB, R, Bface, FSo, st);
-    if (axis == 1) return launch_der<1, true>(g, e, mt, P, UB, R, Bface, FSo, st);
-    return launch_der<2, true>(g, e, mt, P, UB, R, Bface, FSo, st);
+    if (axis == 0) return launch_der<0, true>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+    if (axis == 1) return launch_der<1, true>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+    return launch_der<2, true>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
   }
-  if (axis == 0) return launch_der<0, false>(g, e, mt, P, UB, R, Bface, FSo, st);
-  if (axis == 1) return launch_der<1, false>(g, e, mt, P, UB, R, Bface, FSo, st);
-  return launch_der<2, false>(g, e, mt, P, UB, R, Bface, FSo, st);
+  if (axis == 0) return launch_der<0, false>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  if (axis == 1) return launch_der<1, false>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  return launch_der<2, false>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
 }
 
 }  // namespace echo

@@ -343,20 +343,53 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
         int pos[5];
 #pragma unroll
         for (int m = 0; m < 5; m++) pos[m] = loff<AX, RING>(t, GE::wrap(rr - 2 + m));
+        constexpr bool CHAR = REC == 6;  // A44: the hydro states per face from the characteristic fields
 #pragma unroll
         for (int v = 0; v < 8; v++) {
           const double* r = smem + GE::OFF_P + v * GE::VP;
           double u[5];
 #pragma unroll
           for (int m = 0; m < 5; m++) u[m] = r[pos[m]];
-          rec_both<REC>(u[0], u[1], u[2], u[3], u[4], qL[v], qR[v]);
+          if (!CHAR || v >= 5) rec_both<CHAR ? 0 : REC>(u[0], u[1], u[2], u[3], u[4], qL[v], qR[v]);
           if (v == 0 || v == 4) {
-            if (!(qL[v] > 0.0)) qL[v] = u[2];  // A25 positivity fallback
-            if (!(qR[v] > 0.0)) qR[v] = u[2];
+            if constexpr (!CHAR) {
+              if (!(qL[v] > 0.0)) qL[v] = u[2];  // A25 positivity fallback
+              if (!(qR[v] > 0.0)) qR[v] = u[2];
+            }
             // face xr joins cells xr and xr+1 (der_jump = +inf when the switch is off: never fires)
             const double lo = u[2] < u[3] ? u[2] : u[3];
             rgh |= fabs(u[3] - u[2]) > g.der_jump * lo;
           }
+        }
+        if constexpr (CHAR) {
+          // face xf = xr - 1 (between cells xr-1 and xr): stencil cells xr-3 .. xr+2 in the sweep frame;
+          // its left state goes to qL (used by this lane in B, no shuffle), its right state to qR
+          double q6[6][5];
+          constexpr int cmp[3] = {1 + AX, 1 + (AX + 1) % 3, 1 + (AX + 2) % 3};
+#pragma unroll
+          for (int m = 0; m < 6; m++) {
+            const int ps = loff<AX, RING>(t, GE::wrap(rr - 3 + m));
+            q6[m][0] = smem[GE::OFF_P + 0 * GE::VP + ps];
+#pragma unroll
+            for (int d = 0; d < 3; d++) q6[m][1 + d] = smem[GE::OFF_P + cmp[d] * GE::VP + ps];
+            q6[m][4] = smem[GE::OFF_P + 4 * GE::VP + ps];
+          }
+          double fL[5], fR[5];
+          char_face(e, q6, fL, fR);
+          qL[0] = fL[0];
+          qR[0] = fR[0];
+          qL[4] = fL[4];
+          qR[4] = fR[4];
+#pragma unroll
+          for (int d = 0; d < 3; d++) {
+            qL[cmp[d]] = fL[1 + d];
+            qR[cmp[d]] = fR[1 + d];
+          }
+          // A25: a non-positive rho or p takes the value of the cell the state was reconstructed in
+          if (!(qL[0] > 0.0)) qL[0] = q6[2][0];
+          if (!(qL[4] > 0.0)) qL[4] = q6[2][4];
+          if (!(qR[0] > 0.0)) qR[0] = q6[3][0];
+          if (!(qR[4] > 0.0)) qR[4] = q6[3][4];
         }
         if constexpr (!kBallot) rough[t * RR + ((B + 3 + i) & (RR - 1))] = rgh;
         if (edge_out) {  // publish the left state of cell xr for the slot to the right
@@ -456,12 +489,15 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
       // ---- B: face xf = B+2+i between reconstructed cells xf and xf+1 (a3) ----
       if (ab) {
         double pl[8];
+        constexpr int V0 = REC == 6 ? 5 : 0;  // A44: the hydro left state of this face is the lane's own
 #pragma unroll
-        for (int v = 0; v < 8; v++) pl[v] = __shfl_up_sync(0xffffffffu, qL[v], GE::DELTA);
+        for (int v = V0; v < 8; v++) pl[v] = __shfl_up_sync(0xffffffffu, qL[v], GE::DELTA);
         if (edge_in) {
 #pragma unroll
-          for (int v = 0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + eslot_in * GE::NL + t];
+          for (int v = V0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + eslot_in * GE::NL + t];
         }
+#pragma unroll
+        for (int v = 0; v < V0; v++) pl[v] = qL[v];
         const int xf = B + 2 + i;
         if (xf >= -3) {
           double F[7];
@@ -504,7 +540,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
 }
 
 template <int AX, bool KS, int DER, int REC, int DM>
-__global__ void __launch_bounds__(Geo<AX>::THREADS, Geo<AX>::BPS)
+__global__ void __launch_bounds__(Geo<AX>::THREADS, REC == 6 ? (Geo<AX>::BPS + 1) / 2 : Geo<AX>::BPS)
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         const double* __restrict__ UB, double* R, const double* __restrict__ Bface, double* __restrict__ FSo) {
   using GE = Geo<AX>;
@@ -528,7 +564,7 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 
 // line-group geometry of a sweep launch (the slab extension included)
 template <int AX>
-inline LineGeom make_line_geom(const GridP& g, const double* P, const double* R) {
+inline LineGeom make_line_geom(const GridP& g, const double* P, const double* R, const PlaneRange& zr = PlaneRange{}) {
   using GE = Geo<AX>;
   LineGeom lg;
   lg.na = g.n[AX];
@@ -547,6 +583,10 @@ inline LineGeom make_line_geom(const GridP& g, const double* P, const double* R)
       lg.nz += 2;
       lg.zoff = -1;
     }
+  }
+  if (AX != 2 && zr.zn > 0) {  // x/y sweeps over planes zb .. zb + zn - 1 only (slab overlap, echo.h)
+    lg.zoff = zr.zb;
+    lg.nz = zr.zn;
   }
   lg.nchunks = (lg.na + GE::CH - 1) / GE::CH;  // (after the slab extension of na)
   lg.vec16 = (g.n[0] % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);

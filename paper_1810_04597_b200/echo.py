@@ -84,6 +84,8 @@ _sig = {
     "echo_halo_pull": (C.c_int, [_P, C.c_int]),
     "echo_stage_sweeps": (C.c_int, [_P, C.c_int]),
     "echo_stage_update": (C.c_int, [_P, C.c_int, C.c_double]),
+    "echo_stage_sweeps_interior": (C.c_int, [_P, C.c_int]),
+    "echo_stage_sweeps_boundary": (C.c_int, [_P, C.c_int]),
     "echo_halo_export": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_import": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_fill": (C.c_int, [_P, C.c_int]),
@@ -307,6 +309,14 @@ def stage_sweeps(ctx, s: int):
 
 def stage_update(ctx, s: int, dt: float):
     return _check(ctx, _lib.echo_stage_update(ctx, int(s), float(dt)))
+
+
+def stage_sweeps_interior(ctx, s: int):
+    return _check(ctx, _lib.echo_stage_sweeps_interior(ctx, int(s)))
+
+
+def stage_sweeps_boundary(ctx, s: int):
+    return _check(ctx, _lib.echo_stage_sweeps_boundary(ctx, int(s)))
 
 
 def halo_doubles(ctx) -> int:

@@ -160,7 +160,13 @@ class DistSlab:
         self.send = [torch.empty(nd, dtype=torch.float64, device=device) for _ in range(2)]
         self.recv = [torch.empty(nd, dtype=torch.float64, device=device) for _ in range(2)]
 
-    def exchange(self):
+    def exchange(self, overlap=None):
+        """The ghost exchange of one stage, stream-ordered: the exports are kernels on the
+        compute stream, and NCCL's stream waits for them (torch orders a collective after the
+        work already issued on the current stream), so the host never synchronises; `overlap`
+        (e.g. the stage's interior sweeps, echo_stage_sweeps_interior) is issued on the compute
+        stream while the messages are in flight; req.wait() then makes the compute stream wait
+        for NCCL before the imports.  (gloo, the CPU tests: wait() blocks the host.)"""
         import torch.distributed as dist
 
         # sends in the order (upper planes, lower planes), receives (lower ghosts, upper ghosts),
@@ -176,10 +182,11 @@ class DistSlab:
         for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
             if nb is not None and nb != self.rank:
                 ops.append(dist.P2POp(dist.irecv, self.recv[side], nb, tag=1 - side))
-        if ops:
-            self.io.sync()
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        if overlap is not None:
+            overlap()
+        for req in reqs:
+            req.wait()
         for side, nb in ((LOWER, self.lo), (UPPER, self.hi)):
             if nb is None:
                 self.io.fill(side)
@@ -187,6 +194,13 @@ class DistSlab:
                 self.io.import_(side, self.send[1 - side])
             else:
                 self.io.import_(side, self.recv[side])
+
+    def step(self, dt: float):
+        """One SSP-RK3 step with the exchange overlapped by each stage's interior sweeps."""
+        for s in (1, 2, 3):
+            self.exchange(overlap=lambda s=s: self.io.sweeps_interior(s))
+            self.io.sweeps_boundary(s)
+            self.io.update(s, dt)
 
     def link_fused(self):
         """Exchange the slabs' IPC handles and link both z sides (a self-neighbour, i.e. a
@@ -273,6 +287,12 @@ class CtxIO:
 
     def sweeps(self, s):
         self.E.stage_sweeps(self.g.ctx, s)
+
+    def sweeps_interior(self, s):
+        self.E.stage_sweeps_interior(self.g.ctx, s)
+
+    def sweeps_boundary(self, s):
+        self.E.stage_sweeps_boundary(self.g.ctx, s)
 
     def update(self, s, dt):
         self.E.stage_update(self.g.ctx, s, dt)

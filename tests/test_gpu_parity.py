@@ -125,10 +125,14 @@ def test_multistep_parity(E, orc, cfg, n, steps):
 @pytest.mark.parametrize("cfg,n,steps,rec", [(0, (32, 32, 32), 10, 2), (2, (40, 40, 40), 10, 2),
                                               (4, (64, 32, 16), 5, 2), (0, (32, 32, 32), 10, 3),
                                               (2, (40, 40, 40), 10, 3), (2, (40, 40, 40), 10, 4),
-                                              (0, (32, 32, 32), 10, 5), (2, (40, 40, 40), 10, 5)])
+                                              (0, (32, 32, 32), 10, 5), (2, (40, 40, 40), 10, 5),
+                                              (0, (32, 32, 32), 10, 6), (2, (40, 40, 40), 10, 6),
+                                              (1, (36, 20, 28), 10, 6), (3, (70, 13, 33), 5, 6)])
 def test_multistep_parity_mp5(E, orc, cfg, n, steps, rec):
-    """MP5 (rec=2, A33) and WENO-Z (rec=3, A34) reconstruction: multi-step
-    parity, incl. the blast (limiter active at the shock) and the Kerr-Schild torus."""
+    """MP5 (rec=2, A33), WENO-Z (rec=3, A34), MC2 (4), PPM (5) and characteristic-wise WENO5
+    (rec=6, A44) reconstruction: multi-step parity, incl. the blast (limiter
+    active at the shock) and the Kerr-Schild torus (not for rec 6: flat only); the rec-6
+    cases include a ragged multi-tile grid (70 x 13 x 33)."""
     p = small_problem(cfg, n)
     p.rec = rec
     P8 = I.initial_prims(p)
@@ -174,7 +178,8 @@ def test_con2prim_parity(E, orc):
 def test_switches_parity(E, orc):
     # rec=FV, der=4, divb=none on a multi-tile grid
     p = small_problem(0, (70, 9, 10))
-    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}, {"rec": 3}, {"rec": 4, "der": 2}, {"rec": 5, "der": 4}):
+    for kw in ({"rec": 1}, {"der": 4}, {"divb": 1}, {"der": 2}, {"rec": 2}, {"rec": 2, "divb": 1}, {"rec": 3}, {"rec": 4, "der": 2}, {"rec": 5, "der": 4},
+               {"rec": 6}, {"rec": 6, "divb": 1, "der": 4}):
         for k, v in kw.items():
             setattr(p, k, v)
         P8 = I.initial_prims(p)
@@ -352,3 +357,38 @@ def test_full_size_conservation_and_divb(E):
     st = g.stats()
     assert st["floor_events"] == 0 and st["c2p_failures"] == 0
     g.close()
+
+
+@pytest.mark.parametrize("n,bc", [((4, 4, 4), ((0, 0), (0, 0), (0, 0))), ((5, 3, 7), ((1, 1), (1, 1), (1, 1))),
+                                  ((33, 2, 9), ((0, 0), (1, 1), (0, 0)))])
+def test_characteristic_degenerate_grids_parity(E, orc, n, bc):
+    """rec = 6 (A44) on grids shorter than the halo / a chunk, outflow on short axes: rhs and 3 steps."""
+    p = I.problem(0, n=n)
+    p.bc, p.rec = bc, 6
+    P8 = I.initial_prims(p)
+    oc = ocfg(orc, p)
+    U, P = orc.set_prims(oc, P8)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    dt = orc.max_dt(oc, U, P, p.cfl)
+    assert_rhs_groups(g.rhs(), orc.rhs(oc, U, P), U, dt, CONS_GROUPS, TOL_STAGE, what=f"rec6 rhs {n}",
+                      fscale=flux_scale(orc, oc, U, P))
+    for _ in range(3):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        U, P, _ = orc.step(oc, dt, U, P)
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    assert_groups(gn, U, CONS_GROUPS, TOL_10, what=f"rec6 3 steps U {n}")
+    assert_groups(gp, P, PRIM5_GROUPS, TOL_10, what=f"rec6 3 steps P {n}")
+
+
+def test_characteristic_scope_refused(E):
+    """A44 is flat-metric and field-CD / none only: Kerr-Schild or UCT with rec = 6 fail at create."""
+    for cfg, kw in ((4, {}), (0, {"divb": 2})):
+        p = I.problem(cfg, n=(8, 8, 8))
+        p.rec = 6
+        for k, v in kw.items():
+            setattr(p, k, v)
+        with pytest.raises(E.EchoError) as ei:
+            E.Echo(p)
+        assert ei.value.code == E.E_ARG and "rec = 6" in str(ei.value)

@@ -43,7 +43,7 @@ def test_library_loads_without_gpu(lib_path):
     for s in declared_symbols():
         assert hasattr(lib, s)
     lib.echo_kernel_classes.restype = ctypes.c_int
-    assert lib.echo_kernel_classes() == 15
+    assert lib.echo_kernel_classes() == 16
     lib.echo_kernel_name.restype = ctypes.c_char_p
     assert lib.echo_kernel_name(0) == b"sweep_x"
 

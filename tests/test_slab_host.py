@@ -116,3 +116,76 @@ def test_dist_ghost_exchange_gloo(world, nzg, periodic):
                     want = min(max(k_global, 0), nzg - 1)
                 assert a[k_local, 0] == want, (r, side, h, a[k_local])
                 assert np.array_equal(a[k_local], want + 0.5 * np.arange(3))
+
+
+class LogIO(HostIO):
+    """HostIO that records the call order of DistSlab.step."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.log = []
+
+    def export(self, side, buf):
+        self.log.append(("export", side))
+        super().export(side, buf)
+
+    def import_(self, side, buf):
+        self.log.append(("import", side))
+        super().import_(side, buf)
+
+    def fill(self, side):
+        self.log.append(("fill", side))
+        super().fill(side)
+
+    def sweeps_interior(self, s):
+        self.log.append(("interior", s))
+
+    def sweeps_boundary(self, s):
+        self.log.append(("boundary", s))
+
+    def update(self, s, dt):
+        self.log.append(("update", s))
+
+
+def _step_worker(rank, world, port, nzg, periodic, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    S = _slab_module()
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    z0, nz = S.decompose_z(nzg, world)[rank]
+    io = LogIO(z0, nz, nzg)
+    slab = S.DistSlab(io, rank, world, periodic, "cpu")
+    slab.step(0.01)
+    out[rank] = (io.log, io.a.copy(), z0, nz)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,periodic", [(2, True), (3, False)])
+def test_dist_step_overlaps_exchange_with_interior_sweeps(world, periodic):
+    """DistSlab.step, per stage: both exports, the interior sweeps (issued while the messages are
+    in flight), then the imports / outflow fills, the boundary sweeps and the update, in this
+    order; the ghost planes hold the neighbours' planes (echo.h, echo_stage_sweeps_interior)."""
+    nzg = 30
+    out = mp.Manager().dict()
+    mp.spawn(_step_worker, args=(world, _port(), nzg, periodic, out), nprocs=world, join=True)
+    for r in range(world):
+        log, a, z0, nz = out[r]
+        for s in (1, 2, 3):
+            i_int = log.index(("interior", s))
+            i_bnd = log.index(("boundary", s))
+            i_upd = log.index(("update", s))
+            exports = [k for k, e in enumerate(log) if e[0] == "export" and k < i_int and
+                       (s == 1 or k > log.index(("update", s - 1)))]
+            ins = [k for k, e in enumerate(log) if e[0] in ("import", "fill") and i_int < k < i_bnd]
+            assert len(ins) == 2 and i_int < i_bnd < i_upd, log
+            nb = S_neighbours(r, world, periodic)
+            assert len(exports) == sum(x is not None for x in nb), log
+        for h in range(1, H + 1):
+            k_global = z0 - h
+            want = k_global % nzg if periodic else min(max(k_global, 0), nzg - 1)
+            assert a[H - h, 0] == want
+
+
+def S_neighbours(r, world, periodic):
+    return _slab_module().neighbours(r, world, periodic)

@@ -13,3 +13,11 @@ template __global__ void k_march<2, false, 6, 0, 0>(const GridP, const EosP, con
                                                     const double*, const double*, double*, const double*, double*);
 }  // namespace march
 }  // namespace echo
+namespace echo {
+namespace march {
+template __global__ void k_march<0, false, 6, 6, 0>(const GridP, const EosP, const MetTables, const LineGeom,
+                                                    const double*, const double*, double*, const double*, double*);
+template __global__ void k_march<1, false, 6, 6, 0>(const GridP, const EosP, const MetTables, const LineGeom,
+                                                    const double*, const double*, double*, const double*, double*);
+}  // namespace march
+}  // namespace echo
