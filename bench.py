@@ -7,9 +7,10 @@ A step = one CFL reduction (echo_max_dt) + one full SSP-RK3 step (echo_step) of
 BASELINE.json config 3 (512^3 periodic multi-mode turbulence, Gamma = 4/3,
 fp64), the configuration the metric is quoted on.  Inputs are resident in HBM
 when the timed region starts; they are ~34 GB >> 126 MB L2, so no flush is
-needed.  Prints ONE JSON line (rank 0).  Under torchrun (N > 1) every rank runs
-an independent replica ("replicas only" — the north star runs on
-one GPU with no sharding), timing is the max over ranks.
+needed.  Prints ONE JSON line (rank 0).  Under torchrun (N > 1) the grid is split
+into z slabs, one per GPU, with the NCCL ghost exchange overlapped by each stage's
+interior sweeps (strong scaling, DESIGN.md §9; --replicas: independent replicas);
+timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -246,10 +247,12 @@ def workload_config(args, p, world):
 
 # ------------------------------------------------- ours, z-slab decomposition
 def run_decomp(args, world, rank, local):
-    """--decomp: the config's grid split into z slabs, strong
-    scaling: N ranks x 1 slab (ghost exchange by NCCL point-to-point over NVLink), or
-    on one GPU --slabs S slabs in one process (device copies; the decomposition's own
-    cost: the extra ghost-plane sweeps and the exchange)."""
+    """The config's grid split into z slabs (the paper's own Cartesian
+    domain decomposition), STRONG scaling: the default for N > 1 ranks (one
+    slab per GPU, ghost exchange by NCCL point-to-point over NVLink, stream-ordered and
+    overlapped by each stage's interior sweeps; --fused: the update kernels store the
+    neighbours' ghost planes over CUDA IPC); on one GPU (--decomp) --slabs S slabs in one
+    process (device copies: the decomposition's own cost)."""
     import torch
 
     if world > 1:
@@ -270,33 +273,36 @@ def run_decomp(args, world, rank, local):
     N = p.ncells
     stream = torch.cuda.current_stream(dev)
     P8 = I.initial_prims(p, device=dev)
+    ctxs = []
     if world == 1:
         S = slab.LocalSlabs(p, args.slabs, device=dev, fused=args.fused)
         S.set_prims(P8)
-        launches0 = sum(echo.launch_count(g.ctx) for g, _, _ in S.parts)
+        ctxs = [g for g, _, _ in S.parts]
 
         def one_step():
             S.step(S.max_dt(p.cfl))
-        nslab = args.slabs
+        nslab, path = args.slabs, ("ghost planes stored by the update kernels" if args.fused else "device-copy exchange")
+        z0, nz = 0, p.n[2]
     else:
         sp, (z0, nz) = slab.slab_problem(p, rank, world)
         g = echo.Echo(sp)
         echo.set_stream(g.ctx, stream.cuda_stream)
         g.set_prims(P8[:, z0:z0 + nz].contiguous())
+        ctxs = [g]
         D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev)
         if args.fused:  # neighbours' arrays mapped by CUDA IPC; the updates store the ghost planes
             D.link_fused()
-        launches0 = echo.launch_count(g.ctx)
 
         def one_step():
             dt = D.min_dt(g.max_dt(p.cfl))
             if args.fused:
                 D.step_fused(dt)
-                return
-            for s in (1, 2, 3):
-                D.exchange()
-                g.stage(s, dt)
+            else:
+                D.step(dt)
         nslab = world
+        path = ("ghost planes stored by the update kernels over CUDA IPC / NVLink (host barriers per half stage)"
+                if args.fused else "NCCL point-to-point ghost exchange, stream-ordered, overlapped by the interior x/y sweeps")
+    P8_slab = P8[:, z0:z0 + nz].contiguous() if world > 1 else None
     del P8
     for _ in range(W):
         one_step()
@@ -306,6 +312,7 @@ def run_decomp(args, world, rank, local):
     time.sleep(0.3)
     barrier(world)
     torch.cuda.synchronize()
+    launches0 = sum(echo.launch_count(c.ctx) for c in ctxs)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -316,18 +323,73 @@ def run_decomp(args, world, rank, local):
     barrier(world)
     clocks = clk.stop()
     t = reduce_max(e0.elapsed_time(e1) / 1e3, world, dev)
-    launches = (sum(echo.launch_count(g.ctx) for g, _, _ in S.parts) if world == 1 else echo.launch_count(g.ctx)) - launches0
+    launches = sum(echo.launch_count(c.ctx) for c in ctxs) - launches0
+    value = N * K / t
+
+    # per-kernel device times (rank 0's slab; CUDA events on the context stream)
+    g0 = ctxs[0]
+    echo.profile(g0.ctx, True)
+    for _ in range(2):
+        one_step()
+    prof = echo.profile_read(g0.ctx)
+    echo.profile(g0.ctx, False)
+    step_ms = sum(ms for ms, n in prof.values()) / 2.0
+    shares = {k: round(ms / 2.0 / step_ms, 4) for k, (ms, n) in prof.items() if n}
+    peaks = load_peaks()
+    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep") and v[1]}
+    dom = max(sweeps.items(), key=lambda kv: kv[1][0])[0]
+    dom_ms, dom_n = sweeps[dom]
+    cells_slab = g0.N
+    t_launch = (dom_ms / 2.0 / step_ms) * (t / K) / (dom_n / 2.0) * (len(ctxs) if world == 1 else 1)
+    achieved = FLOPS_PER_CELL_SWEEP * cells_slab / t_launch
+    roofline = {"kernel": f"{dom} (K2 axis sweep, FP64-ALU bound; rank 0's slab)", "bound": "alu",
+                "achieved": achieved / 1e12, "peak": peaks["fp64_flops"] / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / peaks["fp64_flops"], "traffic": None, "peak_source": peaks["src_fp64"],
+                "per_launch_flops": FLOPS_PER_CELL_SWEEP * cells_slab, "launch_ms_timed": t_launch * 1e3,
+                "how": "901 algorithmic flops/cell x the slab's cells / (share of the profiled step x timed ms/step / "
+                       "launches per step)", "kernel_share_of_step": shares}
+
+    # end to end: each rank's slab from pinned host memory, K steps, back to pinned host memory
+    e2e = None
+    if world > 1:
+        host_in = torch.empty(P8_slab.shape, dtype=torch.float64, pin_memory=True)
+        host_in.copy_(P8_slab)
+        host_out = torch.empty(P8_slab.shape, dtype=torch.float64, pin_memory=True)
+        del P8_slab
+        barrier(world)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        echo.set_prims(g.ctx, host_in.numpy())
+        if args.fused:
+            D.link_fused()
+        for _ in range(K):
+            one_step()
+        echo.get_prims(g.ctx, host_out.numpy())
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te2e = reduce_max(f0.elapsed_time(f1) / 1e3, world, dev)
+        e2e = {"value": N * K / te2e, "unit": UNIT, "h2d_bytes_per_step": int(8 * N * 8 / K),
+               "d2h_bytes_per_step": int(8 * N * 8 / K),
+               "what": "every rank: echo_set_prims(pinned host slab) + K decomposed steps + echo_get_prims(pinned host)"}
     if rank == 0:
-        out = {"metric": METRIC, "value": N * K / t, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
                "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "f64", "data": "synthetic",
                "config": {"workload": f"BASELINE.json configs[{args.config}]: {p.name}, {p.n[0]}x{p.n[1]}x{p.n[2]}, "
-                                      f"{REC_NAMES[p.rec]}+HLL+DER6+field-CD, SSP-RK3",
-                          "grid": list(p.n), "parallelism": f"{nslab} z-slabs" + (f" on {world} GPUs (" + ("ghost planes stored by the update kernels over CUDA IPC / NVLink" if args.fused else "NCCL P2P ghost exchange") + ")"
-                                                                                 if world > 1 else (" on 1 GPU (ghost planes stored by the update kernels)" if args.fused else " on 1 GPU (device-copy exchange)")),
-                          "step": "min-reduced CFL dt + 3 x (ghost exchange + echo_stage)"},
+                                      f"CFL {p.cfl}, Gamma 4/3, {REC_NAMES[p.rec]}+HLL+DER6+{DIVB_NAMES[p.divb]}, SSP-RK3",
+                          "grid": list(p.n), "nranks": world, "slabs": nslab,
+                          "parallelism": f"{nslab} z-slabs on {world} GPU(s): {path}",
+                          "l2": "inputs >> 126 MB L2 per GPU: no flush needed",
+                          "step": "min-reduced CFL dt + 3 x (ghost exchange + stage)"},
+               "hbm_roofline": None, "roofline": roofline, "cpu_baseline": None, "e2e": e2e,
                "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(out), flush=True)
+    for c in ctxs if world > 1 else []:
+        c.close()
+    if world == 1:
+        S.close()
     if world > 1:
         import torch.distributed as dist
 
@@ -509,7 +571,9 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--decomp", action="store_true",
-                    help="z-slab domain decomposition (strong scaling; default N>1 mode is independent replicas)")
+                    help="z-slab domain decomposition on one GPU (--slabs S); N > 1 ranks decompose by default")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent 512^3 replicas per GPU (weak scaling) instead of the z-slab decomposition")
     ap.add_argument("--slabs", type=int, default=2, help="--decomp on one GPU: slabs held by this process")
     ap.add_argument("--fused", action="store_true",
                     help="--decomp on one GPU: the update kernels store the neighbours' ghost planes (echo_halo_link)")
@@ -530,7 +594,7 @@ def main(argv=None):
     world, rank, local = dist_setup()
     if args.impl == "reference":
         return run_reference(args, world, rank)
-    if args.decomp:
+    if args.decomp or (world > 1 and not args.replicas):
         return run_decomp(args, world, rank, local)
     return run_ours(args, world, rank, local)
 

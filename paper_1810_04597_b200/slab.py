@@ -99,6 +99,8 @@ class LocalSlabs:
 
     def exchange(self):
         E, n = self.E, len(self.parts)
+        if self.buf.numel() == 0:  # one slab of a non-periodic z axis: no halo side at all
+            return
         for r, (g, _, _) in enumerate(self.parts):
             lo, hi = neighbours(r, n, self.periodic)
             for side, nb in ((LOWER, lo), (UPPER, hi)):
@@ -111,13 +113,22 @@ class LocalSlabs:
     def max_dt(self, cfl: float) -> float:
         return min(g.max_dt(cfl) for g, _, _ in self.parts)
 
-    def step(self, dt: float):
+    def step(self, dt: float, split: bool = False):
+        """split=True (copy exchange): each slab's interior sweeps first, then the exchange, the
+        boundary sweeps and the updates -- DistSlab.step's order, on one GPU."""
         E = self.E
         for s in (1, 2, 3):
             if self.fused:
                 for g, _, _ in self.parts:
                     E.stage_sweeps(g.ctx, s)
                 for g, _, _ in self.parts:
+                    E.stage_update(g.ctx, s, dt)
+            elif split and self.buf.numel() > 0:
+                for g, _, _ in self.parts:
+                    E.stage_sweeps_interior(g.ctx, s)
+                self.exchange()
+                for g, _, _ in self.parts:
+                    E.stage_sweeps_boundary(g.ctx, s)
                     E.stage_update(g.ctx, s, dt)
             else:
                 self.exchange()
@@ -169,6 +180,10 @@ class DistSlab:
         for NCCL before the imports.  (gloo, the CPU tests: wait() blocks the host.)"""
         import torch.distributed as dist
 
+        if self.send[0].numel() == 0:  # a single rank on a non-periodic z axis: no halo side
+            if overlap is not None:
+                overlap()
+            return
         # sends in the order (upper planes, lower planes), receives (lower ghosts, upper ghosts),
         # tagged with the side of the sender's planes: with two ranks both neighbours are the
         # same peer, and NCCL ignores tags and matches point-to-point messages in issue order
@@ -198,8 +213,11 @@ class DistSlab:
     def step(self, dt: float):
         """One SSP-RK3 step with the exchange overlapped by each stage's interior sweeps."""
         for s in (1, 2, 3):
-            self.exchange(overlap=lambda s=s: self.io.sweeps_interior(s))
-            self.io.sweeps_boundary(s)
+            if self.send[0].numel() == 0:  # no halo side (one rank, non-periodic z): a plain stage
+                self.io.sweeps(s)
+            else:
+                self.exchange(overlap=lambda s=s: self.io.sweeps_interior(s))
+                self.io.sweeps_boundary(s)
             self.io.update(s, dt)
 
     def link_fused(self):

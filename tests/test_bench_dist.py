@@ -1,6 +1,7 @@
-"""bench.py's multi-process plumbing (N > 1 runs independent replicas):
-barrier + max-over-ranks timing, exercised with world_size 2 on the gloo backend
-(CPU).  No GPU needed."""
+"""bench.py's multi-process plumbing (N > 1 decomposes the grid into z slabs by default,
+--replicas runs independent replicas): barrier + max-over-ranks timing,
+exercised with world_size 2 on the gloo backend (CPU), the dispatch, and the reference
+arm.  No GPU needed."""
 import json
 import os
 import socket
@@ -64,3 +65,24 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
                         "--ref-n", "8"], cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+@pytest.mark.parametrize("world,extra,want", [("1", [], "ours"), ("2", [], "decomp"), ("2", ["--replicas"], "ours"),
+                                              ("1", ["--decomp"], "decomp")])
+def test_dispatch_decomposes_by_default_for_several_ranks(monkeypatch, world, extra, want):
+    sys.path.insert(0, ROOT)
+    import bench
+
+    seen = []
+    monkeypatch.setenv("WORLD_SIZE", world)
+    monkeypatch.setattr(bench, "run_decomp", lambda *a: seen.append("decomp"))
+    monkeypatch.setattr(bench, "run_ours", lambda *a: seen.append("ours"))
+    bench.main(["--steps", "1", *extra])
+    assert seen == [want]
+
+
+def test_reference_arm_names_the_grid_it_times():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                        "--ref-n", "12"], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["config"]["grid"] == [12, 12, 12] and "512x512x512" in d["config"]["sample_of"]

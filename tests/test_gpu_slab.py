@@ -27,31 +27,34 @@ def E():
     return echo
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [False, True, "split"])
 @pytest.mark.parametrize("cfg,n,nslabs,steps", [
     (0, (32, 24, 32), 2, 3),     # periodic turbulence: a ring of 2 (both neighbours the same slab)
     (0, (20, 16, 40), 3, 3),     # periodic, 3 unequal slabs (14/13/13 planes)
     (0, (16, 16, 16), 1, 2),     # one periodic slab: its own neighbour on both sides
+    (2, (16, 16, 20), 1, 2),     # one outflow slab: no halo side at all (nothing to exchange)
     (2, (24, 20, 36), 3, 3),     # outflow blast: physical ends filled locally, shocks crossing slab edges
     (4, (48, 24, 24), 2, 2),     # Kerr-Schild torus, slabs in phi
 ])
 def test_slabs_match_single_domain_bitwise(E, orc, cfg, n, nslabs, steps, fused):
     """fused=False: export/copy/import before every stage; fused=True: the updates store
-    their edge planes into the neighbours' ghost planes (echo_halo_link)."""
+    their edge planes into the neighbours' ghost planes (echo_halo_link); "split": the copy
+    exchange between each stage's interior sweeps and its boundary sweeps (DistSlab.step's
+    overlap, echo_stage_sweeps_interior / _boundary)."""
     from paper_1810_04597_b200.slab import LocalSlabs
 
     p = I.problem(cfg, n=n)
     P8 = I.initial_prims(p)
     one = E.Echo(p)
     one.set_prims(P8)
-    sl = LocalSlabs(p, nslabs, fused=fused)
+    sl = LocalSlabs(p, nslabs, fused=fused is True)
     sl.set_prims(P8)
     for _ in range(steps):
         dt1 = one.max_dt(p.cfl)
         dts = sl.max_dt(p.cfl)
         assert dts == dt1  # max over cells is order independent
         one.step(dt1)
-        sl.step(dts)
+        sl.step(dts, split=fused == "split")
     un1, _, p1 = one.get_state()
     uns = sl.gather(lambda g: g.get_state()[0])
     ps = sl.gather(lambda g: g.get_state()[2])
@@ -80,6 +83,12 @@ def test_slab_api_errors(E):
         g.advance(1, 0.4)  # so does the device-driven loop
     with pytest.raises(E.EchoError):
         E.halo_fill(g.ctx, 0)  # a halo side is imported, not filled
+    with pytest.raises(E.EchoError) as ei:
+        E.stage_sweeps_boundary(g.ctx, 1)  # the interior half comes first
+    assert ei.value.code == E.E_ORDER
+    E.stage_sweeps_interior(g.ctx, 1)
+    with pytest.raises(E.EchoError):
+        g.stage(1, 1e-3)  # a half-swept stage is finished by its boundary half only
     with pytest.raises(E.EchoError):
         E.create(n=(8, 8, 4), lo=(0, 0, 0), hi=(1, 1, 1), bc=((0, 0), (0, 0), (2, 2)))  # thinner than the halo
     with pytest.raises(E.EchoError):
