@@ -269,6 +269,13 @@ int echo_halo_fill(echo_ctx* ctx, int side);
  * that after the offending stage) and reports it at its end.  flags = 0 turns it off.  The
  * environment variable ECHO_DEBUG_NANSCAN=1 at echo_create sets the flag. */
 enum { ECHO_DEBUG_NANSCAN = 1 };
+/* Out-of-bounds write detection (compute-sanitizer is closed on this build's GPU pool): with the
+ * environment variable ECHO_GUARD_BANDS=1 at echo_create (contexts without halo boundaries),
+ * every state array (U^n, U^s, P, the accumulator(s); UCT: the staggered field, face data and
+ * edge EMFs) gets 32 KB guard bands before and after, filled with 0xA5 bytes.
+ * echo_check_guards verifies every band (synchronises): ECHO_OK, or ECHO_E_CUDA naming the array
+ * and how far outside it the nearest overwritten double lies.  ECHO_E_ORDER without guards. */
+int echo_check_guards(echo_ctx* ctx);
 int echo_set_debug(echo_ctx* ctx, int flags);
 int echo_check_finite(echo_ctx* ctx);
 

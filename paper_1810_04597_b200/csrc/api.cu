@@ -61,6 +61,10 @@ struct echo_ctx {
   // fused update + x sweep (fused.cu): the update of a stage writes the x sweep of the state it
   // produces into the OTHER accumulator (its own curl still reads this stage's EMF)
   double* R2 = nullptr;   // second accumulator (fuse only)
+  // guard bands (ECHO_GUARD_BANDS=1, contexts without halo boundaries): `guard` doubles of 0xA5
+  // bytes before and after every state array, checked by echo_check_guards
+  size_t guard = 0;
+  std::vector<std::pair<double*, size_t>> guarded;  // (allocation base, doubles between the bands)
   int rsel = 0;           // accumulator of the current stage input: 0 R, 1 R2
   bool xahead = false;    // racc() already holds the x sweep of the current stage input
   bool fuse = false;      // fused update + x sweep (Minkowski, no slabs, no UCT; opt-in ECHO_FUSED_UPDATE=1)
@@ -401,10 +405,28 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   c->plane = (size_t)g.pitch * g.n[1];
   const size_t ghost = g.zhalo ? (size_t)kZH * c->plane : 0;
   const size_t rec = c->plane * g.n[2] + 2 * ghost;  // doubles per record array
+  {
+    const char* gb = std::getenv("ECHO_GUARD_BANDS");
+    c->guard = (gb && gb[0] == '1' && !g.zhalo) ? 4096 : 0;  // 32 KB per side
+  }
+  // a state array of n doubles between two guard bands; *base = the allocation (for cudaFree / IPC)
+  auto galloc = [&](size_t n, double** base) -> double* {
+    *base = nullptr;
+    if (cudaMalloc(base, sizeof(double) * (n + 2 * c->guard)) != cudaSuccess) {
+      *base = nullptr;
+      return nullptr;
+    }
+    if (c->guard) {
+      cudaMemset(*base, 0xA5, sizeof(double) * c->guard);
+      cudaMemset(*base + c->guard + n, 0xA5, sizeof(double) * c->guard);
+      c->guarded.push_back({*base, n});
+    }
+    return *base + c->guard;
+  };
   auto alloc = [&](int slot, double** p) {
-    cudaError_t e = cudaMalloc(&c->alloc_base[slot], sizeof(double) * rec);
-    *p = c->alloc_base[slot] ? c->alloc_base[slot] + ghost : nullptr;
-    return e;
+    double* q = galloc(rec, &c->alloc_base[slot]);
+    *p = q ? q + ghost : nullptr;
+    return q ? cudaSuccess : cudaErrorMemoryAllocation;
   };
   if (alloc(0, &c->Un) != cudaSuccess || alloc(1, &c->Us) != cudaSuccess || alloc(2, &c->P) != cudaSuccess ||
       alloc(3, &c->R) != cudaSuccess ||
@@ -419,7 +441,8 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
      // accumulator (without memory for it the kernels stay separate)
     const char* fu = std::getenv("ECHO_FUSED_UPDATE");
     c->fuse = !ks && !g.zhalo && g.divb != 2 && fu && fu[0] == '1';
-    if (c->fuse && cudaMalloc(&c->R2, sizeof(double) * rec) != cudaSuccess) {
+    double* base = nullptr;
+    if (c->fuse && !(c->R2 = galloc(rec, &base))) {
       cudaGetLastError();
       c->fuse = false;
     }
@@ -427,7 +450,7 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   if (g.divb == 2) {
     double** uct_arrays[5] = {&c->Bst, &c->FS[0], &c->FS[1], &c->FS[2], &c->Ed};
     for (double** a : uct_arrays)
-      if (cudaMalloc(a, sizeof(double) * rec) != cudaSuccess) {
+      if (double* base = nullptr; !(*a = galloc(rec, &base))) {
         cudaGetLastError();
         echo_destroy(c);
         return fail(nullptr, ECHO_E_OOM, "echo_create: UCT field allocation failed");
@@ -436,7 +459,8 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
       }
   }
   cudaMemset(c->dcnt, 0, 4 * sizeof(unsigned long long));
-  for (double* b : c->alloc_base) cudaMemset(b, 0, sizeof(double) * rec);
+  for (double* b : c->alloc_base)
+    if (b) cudaMemset(b + c->guard, 0, sizeof(double) * rec);
   if (ks) {
     KsTables t;
     build_ks_tables(metric->M, metric->a, g.n, g.lo, g.dx, &t);
@@ -497,14 +521,14 @@ void echo_destroy(echo_ctx* c) {
   cudaFree(c->dcnt);
   cudaFree(c->dbad);
   cudaFree(c->dnan);
-  cudaFree(c->R2);
+  cudaFree(c->R2 ? c->R2 - c->guard : nullptr);
   for (auto& x : c->step_exec_p)
     if (x) cudaGraphExecDestroy(x);
   cudaFree(c->tables);
   cudaFree(c->dadv);
-  cudaFree(c->Bst);
-  for (double* f : c->FS) cudaFree(f);
-  cudaFree(c->Ed);
+  cudaFree(c->Bst ? c->Bst - c->guard : nullptr);
+  for (double* f : c->FS) cudaFree(f ? f - c->guard : nullptr);
+  cudaFree(c->Ed ? c->Ed - c->guard : nullptr);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->hpin) cudaFreeHost(c->hpin);
@@ -938,6 +962,28 @@ int echo_check_finite(echo_ctx* c) {
   cudaError_t e = launch(c, kNanScan, [&] { return launch_nanscan(c->g, ucur(c), c->P, c->ks ? 8 : 5, c->dnan, nullptr, c->st); });
   if (e != cudaSuccess) return cuda_fail(c, e, "nan scan launch");
   return nan_report(c, "echo_check_finite");
+}
+
+int echo_check_guards(echo_ctx* c) {
+  if (!c) return ECHO_E_ARG;
+  if (!c->guard) return fail(c, ECHO_E_ORDER, "echo_check_guards: no guard bands (ECHO_GUARD_BANDS=1 at echo_create)");
+  CK(cudaStreamSynchronize(c->st), "echo_check_guards");
+  std::vector<unsigned long long> h(c->guard);
+  const unsigned long long pat = 0xA5A5A5A5A5A5A5A5ull;
+  for (size_t a = 0; a < c->guarded.size(); a++) {
+    for (int side = 0; side < 2; side++) {
+      const double* src = c->guarded[a].first + (side ? c->guard + c->guarded[a].second : 0);
+      CK(cudaMemcpy(h.data(), src, sizeof(double) * c->guard, cudaMemcpyDeviceToHost), "echo_check_guards");
+      for (size_t k = 0; k < c->guard; k++)
+        if (h[side ? k : c->guard - 1 - k] != pat) {  // nearest to the array first
+          char buf[200];
+          std::snprintf(buf, sizeof buf, "echo_check_guards: state array %zu written out of bounds, %s its end by %zu doubles",
+                        a, side ? "after" : "before", k + 1);
+          return fail(c, ECHO_E_CUDA, buf);
+        }
+    }
+  }
+  return ECHO_OK;
 }
 
 int echo_stats(echo_ctx* c, echo_stats_t* out) {

@@ -35,9 +35,14 @@ ECHO_D long long rec_shift(const GridP& g, const int x[3], int a, int d) {
 // hi the mirror from f[5..1] (rec_both of the cells at 0 and +1; the unused halves are dead code)
 template <int REC>
 ECHO_D void rec_pair(const double f[6], double& lo, double& hi) {
-  double dead0, dead1;
-  rec_both<REC>(f[0], f[1], f[2], f[3], f[4], lo, dead0);
-  rec_both<REC>(f[1], f[2], f[3], f[4], f[5], dead1, hi);
+  if constexpr (REC == 0) {  // WENO5 point form: one face each (no shared second normalisation)
+    lo = weno5_one(f[0], f[1], f[2], f[3], f[4]);
+    hi = weno5_one(f[5], f[4], f[3], f[2], f[1]);
+  } else {
+    double dead0, dead1;
+    rec_both<REC>(f[0], f[1], f[2], f[3], f[4], lo, dead0);
+    rec_both<REC>(f[1], f[2], f[3], f[4], f[5], dead1, hi);
+  }
 }
 
 // A38 quadrant velocities (V^p, V^q) = the mean of the two double reconstructions, A39

@@ -91,6 +91,7 @@ _sig = {
     "echo_halo_fill": (C.c_int, [_P, C.c_int]),
     "echo_set_debug": (C.c_int, [_P, C.c_int]),
     "echo_check_finite": (C.c_int, [_P]),
+    "echo_check_guards": (C.c_int, [_P]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -276,6 +277,10 @@ def check_finite(ctx):
     return _check(ctx, _lib.echo_check_finite(ctx))
 
 
+def check_guards(ctx):
+    return _check(ctx, _lib.echo_check_guards(ctx))
+
+
 def launch_count(ctx) -> int:
     return int(_lib.echo_launch_count(ctx))
 
@@ -422,3 +427,6 @@ class Echo:
 
     def check_finite(self):
         return check_finite(self.ctx)
+
+    def check_guards(self):
+        return check_guards(self.ctx)
