@@ -43,6 +43,12 @@ namespace march {
 #ifndef ECHO_PDL
 #define ECHO_PDL 0  // programmatic dependent launch of the y and z sweeps (-DECHO_PDL=1; no gain measured)
 #endif
+#ifndef ECHO_ACC_REGS
+#define ECHO_ACC_REGS 1  // y/z: the old accumulator values by plain loads into registers (not cp.async to smem)
+#endif
+#ifndef ECHO_EDGE_SELECT
+#define ECHO_EDGE_SELECT 0  // y/z: the edge-buffer values loaded by every lane and selected (branch free)
+#endif
 #ifndef ECHO_BALLOT_FLAGS
 #define ECHO_BALLOT_FLAGS 1  // A31 flags as warp ballots + a per-line bit history (warp-local kernels)
 #endif
@@ -309,12 +315,19 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
       cp_async_wait0();
       if constexpr (GE::WARP_LOCAL) __syncwarp();
       else __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
+      double acc[7];  // ECHO_ACC_REGS: the old rhs/EMF values of the output cell, in registers
       if (AX != 0 && d2) {  // old rhs/EMF values of the output cells (accumulated in D)
         if (!dep_waited) {  // the previous sweep's R (uniform: every thread reaches it at the same chunk)
           asm volatile("griddepcontrol.wait;" ::: "memory");
           dep_waited = true;
         }
-        if (!(vec && (t & 1))) {
+        if constexpr (ECHO_ACC_REGS) {  // plain loads issued now, consumed in D2 (latency behind A, D1)
+          const int a = min(X0 + i, lg.na - 1) + lg.coff;
+          const double* src = R + lb + a * as;
+#pragma unroll
+          for (int q = 0; q < 7; q++)
+            acc[q] = (!accumulates<AX, DN>(q) || (UCT && q >= 5)) ? 0.0 : src[out_slot<AX, DN>(q) * vs];
+        } else if (!(vec && (t & 1))) {
           const int a = min(X0 + i, lg.na - 1) + lg.coff;
           const double* src = R + lb + a * as;
           const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
@@ -461,7 +474,15 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
         double Hm[7];
 #pragma unroll
         for (int q = 0; q < 7; q++) Hm[q] = __shfl_up_sync(0xffffffffu, H[q], GE::DELTA);
-        if (edge_in) {
+        // edge lanes take the value from the edge buffer: every lane loads (branch free, so the
+        // shared loads can be scheduled early), the edge lanes select it
+        if constexpr (ECHO_EDGE_SELECT && !GE::LM) {
+#pragma unroll
+          for (int q = 0; q < 7; q++) {
+            const double eh = smem[GE::OFF_HE + par * 7 * GE::VE + q * GE::VE + eslot_in * GE::NL + t];
+            Hm[q] = edge_in ? eh : Hm[q];
+          }
+        } else if (edge_in) {
 #pragma unroll
           for (int q = 0; q < 7; q++) Hm[q] = smem[GE::OFF_HE + par * 7 * GE::VE + q * GE::VE + eslot_in * GE::NL + t];
         }
@@ -481,7 +502,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
               d = (q == 5) ? -hs : hs;
             }
             dst[out_slot<AX, DN>(q) * vs] =
-                accumulates<AX, DN>(q) ? (smem[GE::OFF_A + q * GE::VA + loff<AX, CH>(t, i)] + d) : d;
+                accumulates<AX, DN>(q) ? ((ECHO_ACC_REGS ? acc[q] : smem[GE::OFF_A + q * GE::VA + loff<AX, CH>(t, i)]) + d) : d;
           }
         }
       }
@@ -492,7 +513,13 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
         constexpr int V0 = REC == 6 ? 5 : 0;  // A44: the hydro left state of this face is the lane's own
 #pragma unroll
         for (int v = V0; v < 8; v++) pl[v] = __shfl_up_sync(0xffffffffu, qL[v], GE::DELTA);
-        if (edge_in) {
+        if constexpr (ECHO_EDGE_SELECT && !GE::LM) {
+#pragma unroll
+          for (int v = V0; v < 8; v++) {  // (branch free, as for H above)
+            const double ee = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + eslot_in * GE::NL + t];
+            pl[v] = edge_in ? ee : pl[v];
+          }
+        } else if (edge_in) {
 #pragma unroll
           for (int v = V0; v < 8; v++) pl[v] = smem[GE::OFF_E + par * 8 * GE::VE + v * GE::VE + eslot_in * GE::NL + t];
         }

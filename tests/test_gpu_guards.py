@@ -41,7 +41,7 @@ CASES = [
     (0, (33, 9, 10), {}),                    # one cell past a chunk along x, short y/z lines
     (0, (1, 16, 1), {}),                     # single-cell x and z axes
     (2, (5, 3, 7), {}),                      # outflow everywhere, below one chunk
-    (4, (36, 18, 8), {}),                    # Kerr-Schild (metric tables, sources)
+    (4, (36, 35, 8), {}),                    # Kerr-Schild (metric tables, sources)
     (0, (20, 12, 9), {"rec": 6}),            # characteristic-wise reconstruction
     (0, (20, 12, 9), {"rec": 5, "der": 4}),  # PPM, DER4
     (2, (17, 11, 13), {"divb": 2}),          # UCT: face data, edge EMFs, induction, centring
@@ -68,7 +68,10 @@ def test_no_out_of_bounds_writes(E, cfg, n, kw):
     g.step(g.max_dt(p.cfl))
     g.advance(2, p.cfl)
     g.check_guards()
-    E.set_cons(g.ctx, np.ascontiguousarray(g.get_cons()))
+    if p.divb != 2:  # (UCT keeps its field staggered: no cons setter)
+        E.set_cons(g.ctx, np.ascontiguousarray(g.get_cons()))
+    else:
+        g.set_face_field(g.get_face_field())
     g.get_prims()
     g.get_state()
     g.check_guards()

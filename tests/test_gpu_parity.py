@@ -194,7 +194,9 @@ def test_switches_parity(E, orc):
 
 
 # ------------------------------------------------ full-size sampled parity
-FULL = [(1, None), (2, None), (4, None), (3, None)]
+# (config, reconstruction): the default WENO5 on every config, plus the characteristic-wise
+# (rec 6, A44) and MP5 (rec 2) sweeps at 512^3 and the characteristic-wise at the blast
+FULL = [(1, None), (2, None), (4, None), (3, None), (3, 6), (2, 6), (3, 2)]
 
 
 def _full_state(E, p, device_ic):
@@ -210,14 +212,16 @@ def _full_state(E, p, device_ic):
     return g
 
 
-@pytest.mark.parametrize("cfg,_", FULL)
-def test_full_size_sampled_stage_parity(E, orc, cfg, _):
+@pytest.mark.parametrize("cfg,rec", FULL)
+def test_full_size_sampled_stage_parity(E, orc, cfg, rec):
     """At BASELINE.json's full sizes, in the bench launch configuration: each RK
     stage's output at 2000 sampled cells (incl. the 8 corners) against the
     oracle's per-cell path on the GPU's own input state."""
     import torch
 
     p = I.problem(cfg)
+    if rec is not None:
+        p.rec = rec
     g = _full_state(E, p, device_ic=(cfg == 3))
     oc = ocfg(orc, p)
     cells = I.sample_cells(p.n, 2000, seed=100 + cfg)
