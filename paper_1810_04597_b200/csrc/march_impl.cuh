@@ -126,7 +126,8 @@ struct Geo {
   static constexpr int OFF_P = 0;
   static constexpr int OFF_F = OFF_P + 8 * VP;
   static constexpr int OFF_A = OFF_F + 7 * VF;
-  static constexpr int OFF_E = OFF_A + ((AX == 0) ? 0 : 7 * VA);   // left states qL at warp edges [2][8]
+  // the y/z accumulation buffer (none with ECHO_ACC_REGS: the old values are held in registers)
+  static constexpr int OFF_E = OFF_A + ((AX == 0 || ECHO_ACC_REGS) ? 0 : 7 * VA);  // left states qL at warp edges [2][8]
   static constexpr int OFF_HE = OFF_E + 2 * 8 * VE;                 // DER fluxes H at warp edges [2][7]
   static constexpr int TOTAL = OFF_HE + 2 * 7 * VE;
   static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RR;  // + A31 flag ring (bytes)

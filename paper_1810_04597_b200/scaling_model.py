@@ -10,9 +10,14 @@ Per rank of an N-slab run of an n1 x n2 x n3 grid (nz = n3 / N planes):
   g        ghost-plane work per slab: the x/y sweeps also run on one ghost plane per
            side and the z sweep's lines are 2 cells longer (calibrated, below)
   L        kernel launches per step and slab (12 + the exchange launches)
-  T_xchg   ghost exchange per step: 3 stages x 2 sides x 6 planes x 2 records x the
-           plane bytes, over NVLink (copy exchange) or folded into the update's stores
-           (fused exchange: only the part that does not overlap the update, f_exposed)
+  T_xchg   ghost exchange per step: 3 stages x 2 sides x 6 planes of halo messages, over
+           NVLink.  Round 1's messages were whole P and U records (2 x 64 B per cell); round
+           2's hold what the sweeps read (8 doubles per cell, `exchange_bytes(layout="r02")`).
+           "copy": the exchange in series with the stage; "overlap" (round 2's default,
+           DistSlab.step): the NCCL messages in flight while the stage's interior x/y sweeps
+           run (a fraction f_xy of the stage's compute), only the excess exposed; "fused":
+           folded into the update's stores (only the part that does not overlap the update,
+           f_exposed)
 
 Calibration (`calibrate`) fits t_plane, g and the exchange cost per byte to the measured
 1-GPU runs (profiles/r01_bench_default.json and r01_bench_decomp_*.json, where the
@@ -43,9 +48,13 @@ def plane_bytes(n1: int, n2: int) -> int:
     return (8 * vs + 8) * n2 * 8
 
 
-def exchange_bytes(n1: int, n2: int) -> int:
-    """Bytes a slab sends per step: 3 stages x 2 sides x 6 planes x (P, U) records."""
-    return 3 * 2 * HALO * 2 * plane_bytes(n1, n2)
+def exchange_bytes(n1: int, n2: int, layout: str = "r01") -> int:
+    """Bytes a slab sends per step: 3 stages x 2 sides x 6 planes.  layout "r01": the P and U
+    records (round 1); "r02": per row 8 x vs doubles (rho, u~, p from P, B from U)."""
+    if layout == "r01":
+        return 3 * 2 * HALO * 2 * plane_bytes(n1, n2)
+    vs = n1 + (n1 & 1)
+    return 3 * 2 * HALO * n2 * 8 * vs * 8
 
 
 @dataclass
@@ -56,16 +65,24 @@ class Model:
     copy_bw: float = 3.0e12     # B/s of the 1-GPU device-copy exchange (read + write in HBM)
     fused_exposed: float = 0.5  # fraction of the fused ghost stores not hidden by the update
     nvlink_bw: float = 0.7e12   # B/s per direction and GPU pair, effective (900 GB/s nominal)
+    f_xy: float = 0.51          # x + y sweeps' share of a stage (profiles/r02_launch_shares.txt)
+    plane_cells: int = 512 * 512  # cells of the calibration plane: t_plane scales with n1 n2
 
     def step_time(self, n: tuple, nslabs: int, mode: str = "copy", link: str = "nvlink") -> dict:
         """Per-step time of one slab (= the job, all slabs in parallel on separate GPUs)."""
         n1, n2, n3 = n
         nz = n3 / nslabs
-        compute = self.t_plane * (nz + (self.g if nslabs > 1 else 0.0))
-        xb = exchange_bytes(n1, n2) if nslabs > 1 else 0
+        tp = self.t_plane * (n1 * n2) / self.plane_cells
+        compute = tp * (nz + (self.g if nslabs > 1 else 0.0))
+        layout = "r02" if mode == "overlap" else "r01"
+        xb = exchange_bytes(n1, n2, layout) if nslabs > 1 else 0
         bw = self.nvlink_bw if link == "nvlink" else self.copy_bw
         if mode == "copy":
             xchg = xb / bw + 12 * self.t_launch
+        elif mode == "overlap":  # per stage: the messages against the interior x/y sweeps
+            per_stage = xb / 3 / bw
+            hidden = self.f_xy * (tp * nz) / 3
+            xchg = 3 * max(0.0, per_stage - hidden) + (12 * self.t_launch if nslabs > 1 else 0.0)
         elif mode == "fused":
             xchg = self.fused_exposed * xb / bw
         else:
