@@ -567,8 +567,18 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
   }
 }
 
+// CTAs per SM of a sweep: half for rec = 6 (its per-face eigen-projection needs ~2x the registers);
+// the Kerr-Schild x sweep (face metric records) spilled 164 B at the x sweep's 80 registers: 4 CTAs (128)
+#ifndef ECHO_KSX_BPS
+#define ECHO_KSX_BPS 4
+#endif
+template <int AX, bool KS, int REC>
+constexpr int sweep_bps() {
+  return REC == 6 ? (Geo<AX>::BPS + 1) / 2 : ((KS && AX == 0) ? ECHO_KSX_BPS : Geo<AX>::BPS);
+}
+
 template <int AX, bool KS, int DER, int REC, int DM>
-__global__ void __launch_bounds__(Geo<AX>::THREADS, REC == 6 ? (Geo<AX>::BPS + 1) / 2 : Geo<AX>::BPS)
+__global__ void __launch_bounds__(Geo<AX>::THREADS, (sweep_bps<AX, KS, REC>()))
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         const double* __restrict__ UB, double* R, const double* __restrict__ Bface, double* __restrict__ FSo) {
   using GE = Geo<AX>;

@@ -436,7 +436,7 @@ ECHO_D void uct_reduce(double rate, int nfl, int nfa, unsigned long long* counte
 }
 
 template <bool KS>
-__global__ void __launch_bounds__(kCellThreads, 3)
+__global__ void __launch_bounds__(kCellThreads, KS ? 2 : 3)  // KS: spill-free at 128 registers
 k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, const double* dtp,
            const double* __restrict__ R, const double* Un, const double* Us, double* Uout, double* P,
            const double* __restrict__ Bst, unsigned long long* counters, unsigned long long* cfl_out) {
@@ -460,7 +460,7 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
 // the same marching along z (one thread per (i, j) column and kZSeg planes): the centring's
 // b^z samples along z come from a 6-entry register window
 template <bool KS>
-__global__ void __launch_bounds__(128, 6)
+__global__ void __launch_bounds__(128, KS ? 4 : 6)  // KS: spill-free at 128 registers
 k_uct_cell_zm(const GridP g, const EosP e, const MetTables mt, int s, double dt, const double* dtp,
               const double* __restrict__ R, const double* Un, const double* Us, double* Uout, double* P,
               const double* __restrict__ Bst, unsigned long long* counters, unsigned long long* cfl_out) {

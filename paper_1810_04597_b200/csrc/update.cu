@@ -33,8 +33,13 @@ ECHO_D void block_max_atomic(double v, unsigned long long* out) {
   }
 }
 
+// Kerr-Schild: the metric records and the sources need more registers than 85 (at 3 CTAs/SM
+// the curved-metric stage kernel spilled 180 B per thread): 2 CTAs/SM there (ECHO_KS_UPDATE_BPS)
+#ifndef ECHO_KS_UPDATE_BPS
+#define ECHO_KS_UPDATE_BPS 2
+#endif
 template <bool KS, int MODE, bool DIVB_NONE>
-__global__ void __launch_bounds__(kCellThreads, 3)
+__global__ void __launch_bounds__(kCellThreads, KS ? ECHO_KS_UPDATE_BPS : 3)
 k_update(const GridP g, const EosP e, const MetTables mt, const int s, const double dt, const double* __restrict__ R,
          const double* Un, const double* Us, double* Uout, double* P, double* __restrict__ Lout,
          unsigned long long* counters, unsigned long long* cfl_out, const GhostLinks gl, const double* dtp) {
