@@ -572,13 +572,18 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
 #ifndef ECHO_KSX_BPS
 #define ECHO_KSX_BPS 4
 #endif
-template <int AX, bool KS, int REC>
+// (and the UCT x sweep, which also writes the face data, spilled 56 B at 80: 5 CTAs)
+#ifndef ECHO_UCTX_BPS
+#define ECHO_UCTX_BPS 5
+#endif
+template <int AX, bool KS, int REC, int DM>
 constexpr int sweep_bps() {
-  return REC == 6 ? (Geo<AX>::BPS + 1) / 2 : ((KS && AX == 0) ? ECHO_KSX_BPS : Geo<AX>::BPS);
+  return REC == 6 ? (Geo<AX>::BPS + 1) / 2
+                  : ((KS && AX == 0) ? ECHO_KSX_BPS : ((DM == 2 && AX == 0) ? ECHO_UCTX_BPS : Geo<AX>::BPS));
 }
 
 template <int AX, bool KS, int DER, int REC, int DM>
-__global__ void __launch_bounds__(Geo<AX>::THREADS, (sweep_bps<AX, KS, REC>()))
+__global__ void __launch_bounds__(Geo<AX>::THREADS, (sweep_bps<AX, KS, REC, DM>()))
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         const double* __restrict__ UB, double* R, const double* __restrict__ Bface, double* __restrict__ FSo) {
   using GE = Geo<AX>;

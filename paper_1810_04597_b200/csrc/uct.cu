@@ -142,7 +142,7 @@ k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restric
 // y or x) are loaded per step.  Same arithmetic as uct_emf_one.
 constexpr int kZSeg = 16;  // planes per thread
 #ifndef ECHO_EMF_ZM_BPS
-#define ECHO_EMF_ZM_BPS 3
+#define ECHO_EMF_ZM_BPS 3  // (168 registers, 52-104 B of spills; 2 CTAs/SM: variant "emf2" below)
 #endif
 template <int REC, int CC>
 __global__ void __launch_bounds__(128, ECHO_EMF_ZM_BPS)
