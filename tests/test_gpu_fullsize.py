@@ -10,6 +10,7 @@ checked against the oracle's at every step.
 
 * config 1 (128^3 CP Alfven wave), config 2 (256^3 blast, A31 active at the shock),
   config 4 (256 x 128 x 256 Kerr-Schild torus, floors firing in the atmosphere): 10 steps.
+* UCT (divb = 2) on configs 1 and 4: 10 steps, the staggered field included.
 * config 3 (512^3): 5 steps.  The oracle needs ~45 GB of host RAM and ~10 min of host
   CPU for it, so it runs only with ECHO_FULL_CFG3=1 (the committed log of that run is
   profiles/r02_fullsize_parity.txt).
@@ -93,3 +94,43 @@ def test_full_size_10_step_parity(E, orc, cfg):
                     reason="512^3 oracle: ~45 GB host RAM, ~10 min; set ECHO_FULL_CFG3=1 (log in profiles/)")
 def test_full_size_cfg3_5_step_parity(E, orc):
     _run(E, orc, 3, 5)
+
+
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_full_size_10_step_parity_uct(E, orc, cfg):
+    """UCT (divb = 2, readings A37-A43) at the same full sizes: configs 1 (128^3) and 4
+    (256 x 128 x 256, Kerr-Schild), 10 steps, every cell, the staggered field included."""
+    p = I.problem(cfg)
+    p.divb = 2
+    oc = orc.Cfg(**p.grid_kwargs())
+    t0 = time.time()
+    P8, b3 = I.initial_prims(p), I.face_field(p)
+    U, P, ob = orc.set_prims_uct(oc, P8, b3)
+    g = E.Echo(p)
+    g.set_prims(P8)
+    g.set_face_field(b3)
+    del P8, b3
+    ocnt = [0, 0]
+    for _ in range(10):
+        dt = orc.max_dt(oc, U, P, p.cfl)
+        assert g.max_dt(p.cfl) == pytest.approx(dt, rel=1e-13)
+        U, P, ob, cnt = orc.step_uct(oc, dt, U, P, ob)
+        ocnt[0] += cnt[0]
+        ocnt[1] += cnt[1]
+        g.step(dt)
+    gn, _, gp = g.get_state()
+    eu, ep = group_errors(gn, U, CONS_GROUPS), group_errors(gp, P, PRIM5_GROUPS)
+    eb = group_errors(g.get_face_field(), ob, {"b": [0, 1, 2]})
+    st = g.stats()
+    g.close()
+    line = (f"uct cfg{cfg} {p.n} 10 steps ({time.time() - t0:.0f} s): U {eu} P {ep} b {eb} "
+            f"counters gpu ({st['floor_events']}, {st['c2p_failures']}) oracle {tuple(ocnt)}")
+    print(line)
+    log = os.environ.get("ECHO_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write("fullsize " + line + "\n")
+    for name, errs in (("U", eu), ("P", ep), ("b", eb)):
+        bad = {k: v for k, v in errs.items() if not v <= TOL_10}
+        assert not bad, f"uct cfg{cfg} 10 steps {name}: {errs}"
+    assert (st["floor_events"], st["c2p_failures"]) == tuple(ocnt)

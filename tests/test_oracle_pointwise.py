@@ -1,7 +1,9 @@
 """Pins of the oracle's point-wise pieces against values and identities the
 mathematics fixes.
 CPU only."""
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -198,8 +200,8 @@ def test_der_values(orc):
     for o in (2, 4, 6):
         assert orc.der([2.5] * 5, o) == 2.5
     # App. A: F = cell average of sin over [x-h/2, x+h/2]; max |DER(F) - sin|
-    want = {2: [6.41e-3, 1.61e-3, 4.02e-4, 1.00e-4], 4: [1.11e-4, 6.95e-6, 4.35e-7, 2.72e-8],
-            6: [2.51e-6, 3.98e-8, 6.24e-10, 9.76e-12]}
+    gd = _golden("appendix_a_der_errors.json")
+    want = {int(k): v for k, v in gd["errors"].items()}
     for o, ref in want.items():
         for N, r in zip((16, 32, 64, 128), ref):
             h = 2 * math.pi / N
@@ -210,15 +212,17 @@ def test_der_values(orc):
 
 
 # ------------------------------------------------------------ prim2cons
-APP_A_P2C = [
-    # (rho, v, p, B) -> (D, S, U)  SURVEY App. A (sympy, Gamma = 4/3)
-    ((1, (0, 0, 0), 1, (0, 0, 0)), (1.0, (0, 0, 0), 4.0)),
-    ((1, (0, 0, 0), 1, (0.5, 0, 0)), (1.0, (0, 0, 0), 4.125)),
-    ((1, (0.1, 0, 0), 1, (0.5, 0, 0)), (1.00503781525921, (0.505050505050505, 0, 0), 4.17550505050505)),
-    ((0.01, (0, 0, 0), 0.001, (0.1, 0, 0)), (0.01, (0, 0, 0), 0.018)),
-    ((0.01, (0.6, 0.3, 0), 1, (0.1, 0, 0)), (0.0134839972492648, (4.374545454545455, 2.190272727272728, 0),
-                                             6.29635909090909)),
-]
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+# (rho, v, p, B) -> (D, S, U): tests/golden/appendix_a_prim2cons.json (sympy, Gamma = 4/3)
+APP_A_P2C = [((c["rho"], tuple(c["v"]), c["p"], tuple(c["B"])), (c["D"], tuple(c["S"]), c["U"]))
+             for c in _golden("appendix_a_prim2cons.json")["cases"]]
 
 
 @pytest.mark.parametrize("case", APP_A_P2C)
@@ -244,13 +248,9 @@ def test_prim2cons_rest_frame(orc):
 
 
 # ----------------------------------------------------------------- speeds
-APP_A_SPEEDS = [
-    ((1, (0, 0, 0), 1, (0, 0, 0)), (-0.516397779494322, 0.516397779494322)),
-    ((1, (0, 0, 0), 1, (0.5, 0, 0)), (-0.549169647365276, 0.549169647365276)),
-    ((1, (0.1, 0, 0), 1, (0.5, 0, 0)), (-0.475270035124538, 0.615375113933645)),
-    ((0.01, (0, 0, 0), 0.001, (0.1, 0, 0)), (-0.687184270936277, 0.687184270936277)),
-    ((0.01, (0.6, 0.3, 0), 1, (0.1, 0, 0)), (0.0763249619071452, 0.864230029959631)),
-]
+# tests/golden/appendix_a_speeds.json
+APP_A_SPEEDS = [((c["rho"], tuple(c["v"]), c["p"], tuple(c["B"])), tuple(c["lambda"]))
+                for c in _golden("appendix_a_speeds.json")["cases"]]
 
 
 @pytest.mark.parametrize("case", APP_A_SPEEDS)

@@ -166,18 +166,23 @@ def test_divb_diagnostic_spec_examples(orc):
 
 # ----------------------------------------------------------------- CFL
 def test_cfl_worked_values(orc):
-    # P16, unit box, CFL 0.4
+    # P16 (tests/golden/cfl_worked.json: SURVEY §8(c) P16), unit box, CFL 0.4
+    import json
+    import os
+
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfl_worked.json")))
+    dt_rest, dt_b, dt_blast = (c["dt"] for c in gold["cases"])
     c = orc.Cfg(n=(32, 32, 32))
     U, P = state(orc, c, I.uniform_prims((32, 32, 32), 1, (0, 0, 0), 1, (0, 0, 0)))
-    assert orc.max_dt(c, U, P, 0.4) == pytest.approx(0.00806871530459879, rel=1e-13)
+    assert orc.max_dt(c, U, P, 0.4) == pytest.approx(dt_rest, rel=1e-13)
     U, P = state(orc, c, I.uniform_prims((32, 32, 32), 1, (0, 0, 0), 1, (0.5, 0, 0)))
-    assert orc.max_dt(c, U, P, 0.4) == pytest.approx(0.00758721223333605, rel=1e-13)
+    assert orc.max_dt(c, U, P, 0.4) == pytest.approx(dt_b, rel=1e-13)
     c2 = orc.Cfg(n=(32, 32, 32), hi=(2.0, 2.0, 2.0))  # doubling Delta doubles dt
-    assert orc.max_dt(c2, U, P, 0.4) == pytest.approx(2 * 0.00758721223333605, rel=1e-13)
+    assert orc.max_dt(c2, U, P, 0.4) == pytest.approx(2 * dt_b, rel=1e-13)
     # blast ambient, n = 256 (one line is enough: uniform)
     cb = orc.Cfg(n=(256, 1, 1), hi=(1.0, 1 / 256, 1 / 256))
     U, P = state(orc, cb, I.uniform_prims((256, 1, 1), 0.01, (0, 0, 0), 0.001, (0.1, 0, 0)))
-    assert orc.max_dt(cb, U, P, 0.4) == pytest.approx(0.000757923828238541, rel=1e-13)
+    assert orc.max_dt(cb, U, P, 0.4) == pytest.approx(dt_blast, rel=1e-13)
 
 
 # ------------------------------------------------------- convergence
