@@ -277,6 +277,8 @@ def run_decomp(args, world, rank, local):
     if world == 1:
         S = slab.LocalSlabs(p, args.slabs, device=dev, fused=args.fused)
         S.set_prims(P8)
+        if p.divb == 2:  # UCT slabs: the staggered field (set, exchanged, centred again)
+            S.set_face_field(I.face_field(p, device=dev))
         ctxs = [g for g, _, _ in S.parts]
 
         def one_step():
@@ -289,7 +291,9 @@ def run_decomp(args, world, rank, local):
         echo.set_stream(g.ctx, stream.cuda_stream)
         g.set_prims(P8[:, z0:z0 + nz].contiguous())
         ctxs = [g]
-        D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev)
+        D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev, uct=p.divb == 2)
+        if p.divb == 2:
+            D.set_face_field(I.face_field(p, device=dev)[:, z0:z0 + nz].contiguous())
         if args.fused:  # neighbours' arrays mapped by CUDA IPC; the updates store the ghost planes
             D.link_fused()
 
@@ -362,6 +366,8 @@ def run_decomp(args, world, rank, local):
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         echo.set_prims(g.ctx, host_in.numpy())
+        if p.divb == 2:
+            D.set_face_field(I.face_field(p)[:, z0:z0 + nz].copy())
         if args.fused:
             D.link_fused()
         for _ in range(K):

@@ -78,6 +78,7 @@ class Problem:
     der_jump: float = 0.5
     steps: int = 10
     cfl: float = 0.4
+    dz: float = 0.0  # > 0: the z cell size itself (a z slab of a larger grid, echo.h echo_grid.dz)
     seed: int = 0
     params: dict = field(default_factory=dict)
 
@@ -89,7 +90,8 @@ class Problem:
         return dict(n=tuple(self.n), lo=tuple(self.lo), hi=tuple(self.hi), bc=tuple(tuple(b) for b in self.bc),
                     metric=self.metric, M=self.M, a=self.a, gamma=self.gamma, rho_floor=self.rho_floor,
                     p_floor=self.p_floor, w_max=self.w_max, c2p_max_iter=self.c2p_max_iter,
-                    c2p_tol=self.c2p_tol, rec=self.rec, der=self.der, divb=self.divb, der_jump=self.der_jump)
+                    c2p_tol=self.c2p_tol, rec=self.rec, der=self.der, divb=self.divb, der_jump=self.der_jump,
+                    **({"dz": self.dz} if self.dz > 0 else {}))
 
     def centres(self, a: int) -> np.ndarray:
         d = (self.hi[a] - self.lo[a]) / self.n[a]

@@ -60,6 +60,10 @@ typedef enum { ECHO_BC_PERIODIC = 0, ECHO_BC_OUTFLOW = 1, ECHO_BC_HALO = 2 } ech
  * WENO5 + DER6, plus one because the sweeps also evaluate the EMF on the first
  * ghost plane (the field-CD curl of the edge plane reads it). */
 #define ECHO_HALO_PLANES 6
+/* UCT (divb = 2) slabs store 8: the induction's DER along z reads the edge EMFs of 3 ghost
+ * planes, whose z reconstructions read face data 5 planes in, whose HLL states read the
+ * primitives 7 planes in */
+#define ECHO_HALO_PLANES_UCT 8
 typedef enum { ECHO_METRIC_MINKOWSKI = 0, ECHO_METRIC_KERR_SCHILD = 1 } echo_metric_kind;
 
 /* Grid: n owned cells per axis (n >= 1; periodic n < 5 is allowed, ghosts wrap
@@ -98,6 +102,9 @@ typedef struct {
   int der;
   int divb;
   double der_jump;
+  double dz;  /* > 0: the z cell size Delta_z itself instead of (hi[2] - lo[2]) / n[2] (z slabs take the
+                 global grid's, so that every z difference of the slab is the single domain's bit for
+                 bit; it must agree with hi - lo to 1e-12 relative); 0: derived */
 } echo_grid;
 
 /* Stationary background metric (A1, A14): Minkowski, or Kerr-Schild with mass M >= 0 and spin a
@@ -144,7 +151,8 @@ int echo_set_prims(echo_ctx* ctx, const double* p8, int on_device);
 int echo_get_prims(echo_ctx* ctx, double* p8, int on_device);
 
 /* UCT (grid.divb = 2; readings A37-A43; periodic or outflow axes (A42), any
- * metric (A43); slab boundaries are refused at echo_create): the magnetic state is the staggered field
+ * metric (A43); z-slab boundaries with the copy exchange, ECHO_HALO_PLANES_UCT ghost planes whose
+ * messages also carry b; the fused links are refused): the magnetic state is the staggered field
  * b3[a][n3][n2][n1] = sqrt(gamma) B^a at the centre of the face i_a + 1/2 of cell
  * (i1, i2, i3) (point values).  After echo_set_prims (which supplies the hydro
  * primitives; its B is replaced), echo_set_face_field sets b, the cell-centred field
@@ -196,6 +204,21 @@ int echo_stage_update(echo_ctx* ctx, int s, double dt);
  * not UCT (ECHO_E_ORDER). */
 int echo_stage_sweeps_interior(echo_ctx* ctx, int s);
 int echo_stage_sweeps_boundary(echo_ctx* ctx, int s);
+/* UCT slabs (divb = 2 with halo boundaries): the cell update centres the NEW b^z of 3 faces
+ * beyond the slab, which the neighbour's induction writes, so a stage is
+ *   exchange (echo_halo_export / import / fill) -> echo_stage_sweeps(s)
+ *   -> echo_stage_update_field(s, dt)   (the induction, A41)
+ *   -> new-field exchange: echo_halo_export_field / echo_halo_import_field, or
+ *      echo_halo_fill_field on a physical outflow side (echo_halo_field_doubles(ctx) doubles:
+ *      the new b^z of the 3 owned planes next to the side)
+ *   -> echo_stage_update_cells(s, dt)   (hydro RK, U_B = I6(b), con2prim, A37)
+ * echo_stage and echo_stage_update are refused on such contexts (ECHO_E_ORDER). */
+int echo_stage_update_field(echo_ctx* ctx, int s, double dt);
+int echo_stage_update_cells(echo_ctx* ctx, int s, double dt);
+long long echo_halo_field_doubles(const echo_ctx* ctx);
+int echo_halo_export_field(echo_ctx* ctx, int side, double* buf, int on_device);
+int echo_halo_import_field(echo_ctx* ctx, int side, const double* buf, int on_device);
+int echo_halo_fill_field(echo_ctx* ctx, int side);
 
 /* One full SSP-RK3 step (stages 1, 2, 3) with dt > 0.  Asynchronous. */
 int echo_step(echo_ctx* ctx, double dt);

@@ -53,6 +53,7 @@ struct echo_ctx {
   } rlink[2];
   int swept = 0;                           // stage whose sweeps ran (echo_stage_sweeps), 0 = none
   int swept_int = 0;                       // stage whose interior sweeps ran (echo_stage_sweeps_interior)
+  int inducted = 0;                        // UCT slabs: stage whose induction ran (echo_stage_update_field)
   size_t plane = 0;       // doubles per z plane of a record array (pitch n2)
   double* Un = nullptr;   // U^n
   double* Us = nullptr;   // U^s
@@ -61,6 +62,7 @@ struct echo_ctx {
   // fused update + x sweep (fused.cu): the update of a stage writes the x sweep of the state it
   // produces into the OTHER accumulator (its own curl still reads this stage's EMF)
   double* R2 = nullptr;   // second accumulator (fuse only)
+  double* uct_base[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // allocations of Bst, FS[3], Ed
   // guard bands (ECHO_GUARD_BANDS=1, contexts without halo boundaries): `guard` doubles of 0xA5
   // bytes before and after every state array, checked by echo_check_guards
   size_t guard = 0;
@@ -229,16 +231,26 @@ static GhostLinks ghost_links(echo_ctx* c, int s) {
   return gl;
 }
 
-static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr) {
+// part (UCT slabs, whose cell update centres the new b^z of 3 ghost faces that the neighbour's
+// induction writes): 1 = the induction only, 2 = the cell update only, 0 = both
+static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr, int part = 0) {
   const double* Uin = (s == 1) ? c->Un : c->Us;
   double* Uout = (s == 3) ? c->Un : c->Us;
   // the last stage also reduces the CFL rate of the new state (a9 fused into K3)
   unsigned long long* cfl = (s == 3) ? c->dcnt + 2 : nullptr;
   if (cfl) CK(cudaMemsetAsync(cfl, 0, sizeof(unsigned long long), c->st), "stage");
   if (is_uct(c)) {  // staggered field first (A41), then the cells read its centring (A37)
-    cudaError_t e = launch(c, kUctInduct, [&] {
-      return launch_uct_induct(c->g, 0, s, dt, dtp, c->Ed, c->Bst, nullptr, c->st);
-    });
+    cudaError_t e = cudaSuccess;
+    if (part != 2)
+      e = launch(c, kUctInduct, [&] {
+        return launch_uct_induct(c->g, 0, s, dt, dtp, c->Ed, c->Bst, nullptr, c->st);
+      });
+    if (part == 1) {
+      if (e != cudaSuccess) return cuda_fail(c, e, "uct induction launch");
+      c->inducted = s;
+      return ECHO_OK;
+    }
+    c->inducted = 0;
     if (e == cudaSuccess)
       e = launch(c, kUctCell, [&] {
         return launch_uct_cell(c->ks, c->g, c->e, c->mt, s, dt, dtp, racc(c), c->Un, Uin, Uout, c->P, c->Bst, c->dcnt,
@@ -254,6 +266,7 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
     c->next_stage = (s == 3) ? 1 : s + 1;
     c->swept = 0;
   c->swept_int = 0;
+  c->inducted = 0;
     return ECHO_OK;
   }
   const GhostLinks gl = ghost_links(c, s);
@@ -282,6 +295,7 @@ static int run_update(echo_ctx* c, int s, double dt, const double* dtp = nullptr
   c->next_stage = (s == 3) ? 1 : s + 1;
   c->swept = 0;
   c->swept_int = 0;
+  c->inducted = 0;
   return ECHO_OK;
 }
 
@@ -333,19 +347,16 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   }
   {
     const bool zh = grid->bc[2][0] == ECHO_BC_HALO || grid->bc[2][1] == ECHO_BC_HALO;
-    if (zh && grid->n[2] < ECHO_HALO_PLANES)
-      return fail(nullptr, ECHO_E_ARG, "echo_create: a slab with halo boundaries needs n[2] >= ECHO_HALO_PLANES");
+    if (zh && grid->n[2] < (grid->divb == 2 ? ECHO_HALO_PLANES_UCT : ECHO_HALO_PLANES))
+      return fail(nullptr, ECHO_E_ARG,
+                  "echo_create: a slab with halo boundaries needs n[2] >= ECHO_HALO_PLANES (UCT: ECHO_HALO_PLANES_UCT)");
   }
   if (grid->rec < 0 || grid->rec > 6) return fail(nullptr, ECHO_E_ARG, "echo_create: rec must be 0..6");
   if (grid->rec == 6 && (metric->kind != ECHO_METRIC_MINKOWSKI || grid->divb == 2))
     return fail(nullptr, ECHO_E_ARG, "echo_create: rec = 6 (characteristic-wise, A44) needs the Minkowski metric and divb != 2");
   if (grid->der != 2 && grid->der != 4 && grid->der != 6) return fail(nullptr, ECHO_E_ARG, "echo_create: der must be 2, 4 or 6");
   if (grid->divb < 0 || grid->divb > 2) return fail(nullptr, ECHO_E_ARG, "echo_create: divb must be 0, 1 or 2");
-  if (grid->divb == 2) {  // UCT (A37, A42, A43): periodic or outflow axes (no slabs), any metric
-    bool ok = true;
-    for (int a = 0; a < 3; a++) ok = ok && grid->bc[a][0] != ECHO_BC_HALO && grid->bc[a][1] != ECHO_BC_HALO;
-    if (!ok) return fail(nullptr, ECHO_E_ARG, "echo_create: divb = 2 (UCT) needs periodic or outflow axes (no slabs)");
-  }
+  // UCT (A37, A42, A43): periodic, outflow or (z) slab axes, any metric; slabs with the copy exchange
   if (!(eos->gamma > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: gamma > 1 violated");
   if (!(eos->rho_floor > 0.0) || !(eos->p_floor > 0.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: floors > 0 violated");
   if (!(eos->w_max > 1.0)) return fail(nullptr, ECHO_E_ARG, "echo_create: w_max > 1 violated");
@@ -379,6 +390,14 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     g.bc[a][0] = grid->bc[a][0];
     g.bc[a][1] = grid->bc[a][1];
   }
+  if (grid->dz > 0.0) {  // a slab: the global grid's Delta_z bit for bit (echo.h)
+    if (!(std::fabs(grid->dz * grid->n[2] - (grid->hi[2] - grid->lo[2])) <= 1e-12 * std::fabs(grid->hi[2] - grid->lo[2]))) {
+      delete c;
+      return fail(nullptr, ECHO_E_ARG, "echo_create: dz * n[2] must equal hi[2] - lo[2]");
+    }
+    g.dx[2] = grid->dz;
+    g.idx[2] = 1.0 / grid->dz;
+  }
   g.rec = grid->rec;
   g.der = grid->der;
   g.divb = grid->divb;
@@ -401,9 +420,9 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
   g.pitch = 8LL * g.vs + 8;
   // slab mode (z boundaries of kind ECHO_BC_HALO): kZH stored ghost planes below and above
   // the owned ones in every record array; the array pointers point at plane 0
-  g.zhalo = (g.bc[2][0] == ECHO_BC_HALO || g.bc[2][1] == ECHO_BC_HALO) ? 1 : 0;
+  g.zhalo = (g.bc[2][0] == ECHO_BC_HALO || g.bc[2][1] == ECHO_BC_HALO) ? (g.divb == 2 ? kZHU : kZH) : 0;
   c->plane = (size_t)g.pitch * g.n[1];
-  const size_t ghost = g.zhalo ? (size_t)kZH * c->plane : 0;
+  const size_t ghost = (size_t)g.zhalo * c->plane;
   const size_t rec = c->plane * g.n[2] + 2 * ghost;  // doubles per record array
   {
     const char* gb = std::getenv("ECHO_GUARD_BANDS");
@@ -448,15 +467,18 @@ int echo_create(const echo_grid* grid, const echo_metric* metric, const echo_eos
     }
   }
   if (g.divb == 2) {
+    // (slab mode: like the record arrays, the pointers point at plane 0, ghost planes before)
     double** uct_arrays[5] = {&c->Bst, &c->FS[0], &c->FS[1], &c->FS[2], &c->Ed};
-    for (double** a : uct_arrays)
-      if (double* base = nullptr; !(*a = galloc(rec, &base))) {
+    for (int q = 0; q < 5; q++) {
+      double* a = galloc(rec, &c->uct_base[q]);
+      if (!a) {
         cudaGetLastError();
         echo_destroy(c);
         return fail(nullptr, ECHO_E_OOM, "echo_create: UCT field allocation failed");
-      } else {
-        cudaMemset(*a, 0, sizeof(double) * rec);
       }
+      cudaMemset(a, 0, sizeof(double) * rec);
+      *uct_arrays[q] = a + ghost;
+    }
   }
   cudaMemset(c->dcnt, 0, 4 * sizeof(unsigned long long));
   for (double* b : c->alloc_base)
@@ -526,9 +548,7 @@ void echo_destroy(echo_ctx* c) {
     if (x) cudaGraphExecDestroy(x);
   cudaFree(c->tables);
   cudaFree(c->dadv);
-  cudaFree(c->Bst ? c->Bst - c->guard : nullptr);
-  for (double* f : c->FS) cudaFree(f ? f - c->guard : nullptr);
-  cudaFree(c->Ed ? c->Ed - c->guard : nullptr);
+  for (double* b : c->uct_base) cudaFree(b);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->hpin) cudaFreeHost(c->hpin);
@@ -587,6 +607,7 @@ int echo_set_prims(echo_ctx* c, const double* p8, int on_device) {
   c->xahead = false;
   c->swept = 0;
   c->swept_int = 0;
+  c->inducted = 0;
   return ECHO_OK;
 }
 
@@ -662,6 +683,7 @@ int echo_set_face_field(echo_ctx* c, const double* b3, int on_device) {
   c->xahead = false;
   c->swept = 0;
   c->swept_int = 0;
+  c->inducted = 0;
   return ECHO_OK;
 }
 
@@ -759,6 +781,10 @@ int echo_stage(echo_ctx* c, int s, double dt) {
   if (s < 1 || s > 3) return fail(c, ECHO_E_ARG, "echo_stage: s must be 1, 2 or 3");
   if (s != c->next_stage || c->swept || c->swept_int) return fail(c, ECHO_E_ORDER, "echo_stage: stages must run in order 1, 2, 3");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage: dt > 0 violated");
+  if (is_uct(c) && c->g.zhalo)
+    return fail(c, ECHO_E_ORDER,
+                "echo_stage: UCT slabs: echo_stage_sweeps, echo_stage_update_field, the new-field halo exchange, "
+                "echo_stage_update_cells");
   return run_stage(c, s, dt);
 }
 
@@ -1039,7 +1065,78 @@ int echo_stage_update(echo_ctx* c, int s, double dt) {
   if (!c) return ECHO_E_ARG;
   if (c->swept != s) return fail(c, ECHO_E_ORDER, "echo_stage_update: echo_stage_sweeps(s) must come first");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage_update: dt > 0 violated");
+  if (is_uct(c) && c->g.zhalo)
+    return fail(c, ECHO_E_ORDER,
+                "echo_stage_update: UCT slabs: echo_stage_update_field, the new-field halo exchange, echo_stage_update_cells");
   return run_update(c, s, dt);
+}
+
+int echo_stage_update_field(echo_ctx* c, int s, double dt) {
+  if (!c) return ECHO_E_ARG;
+  if (!is_uct(c) || !c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_stage_update_field: UCT slab contexts only");
+  if (c->swept != s || c->inducted) return fail(c, ECHO_E_ORDER, "echo_stage_update_field: echo_stage_sweeps(s) must come first");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage_update_field: dt > 0 violated");
+  return run_update(c, s, dt, nullptr, 1);
+}
+
+int echo_stage_update_cells(echo_ctx* c, int s, double dt) {
+  if (!c) return ECHO_E_ARG;
+  if (c->inducted != s || c->swept != s)
+    return fail(c, ECHO_E_ORDER, "echo_stage_update_cells: echo_stage_update_field(s) must come first");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, ECHO_E_ARG, "echo_stage_update_cells: dt > 0 violated");
+  return run_update(c, s, dt, nullptr, 2);
+}
+
+// the new b^z of the 3 owned faces next to `side` (written by this stage's induction: slot 2 of the
+// b^n half at stage 3, of the b^s half before), for the neighbour's centring of its edge cells
+static int field_copy(echo_ctx* c, int side, double* buf, bool out, int on_device, const char* where) {
+  if (!is_uct(c) || !c->g.zhalo) return fail(c, ECHO_E_ORDER, (std::string(where) + ": UCT slab contexts only").c_str());
+  if (!c->inducted) return fail(c, ECHO_E_ORDER, (std::string(where) + ": after echo_stage_update_field").c_str());
+  const int H = 3;
+  const long long rows = (long long)H * c->g.n[1];
+  const long long k0 = out ? (side == 0 ? 0 : c->g.n[2] - H) : (side == 0 ? -H : c->g.n[2]);
+  const long long slot = (c->inducted == 3 ? 0 : 3) + 2;  // b^z of the new field
+  double* dev = c->Bst + k0 * (long long)c->plane + slot * c->g.vs;
+  const size_t w = sizeof(double) * c->g.vs, pitchB = sizeof(double) * c->g.pitch;
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : (out ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice);
+  cudaError_t e = out ? cudaMemcpy2DAsync(buf, w, dev, pitchB, w, rows, kind, c->st)
+                      : cudaMemcpy2DAsync(dev, pitchB, buf, w, w, rows, kind, c->st);
+  if (e != cudaSuccess) return cuda_fail(c, e, where);
+  if (!on_device) CK(cudaStreamSynchronize(c->st), where);
+  return ECHO_OK;
+}
+
+long long echo_halo_field_doubles(const echo_ctx* c) {
+  if (!c || !c->g.zhalo || c->g.divb != 2) return 0;
+  return 3LL * c->g.vs * c->g.n[1];
+}
+
+int echo_halo_export_field(echo_ctx* c, int side, double* buf, int on_device) {
+  if (!c || !buf || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_export_field: bad argument") : ECHO_E_ARG;
+  return field_copy(c, side, buf, true, on_device, "echo_halo_export_field");
+}
+
+int echo_halo_import_field(echo_ctx* c, int side, const double* buf, int on_device) {
+  if (!c || !buf || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_import_field: bad argument") : ECHO_E_ARG;
+  return field_copy(c, side, const_cast<double*>(buf), false, on_device, "echo_halo_import_field");
+}
+
+// a physical outflow side: the new b^z of the edge face replicated into the 3 ghost faces (A42)
+int echo_halo_fill_field(echo_ctx* c, int side) {
+  if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_fill_field: bad argument") : ECHO_E_ARG;
+  if (!is_uct(c) || !c->g.zhalo || !c->inducted)
+    return fail(c, ECHO_E_ORDER, "echo_halo_fill_field: UCT slab contexts, after echo_stage_update_field");
+  if (c->g.bc[2][side] != ECHO_BC_OUTFLOW) return fail(c, ECHO_E_ARG, "echo_halo_fill_field: only an outflow side");
+  const long long slot = (c->inducted == 3 ? 0 : 3) + 2;
+  const long long edge = side == 0 ? 0 : c->g.n[2] - 1;
+  for (int h = 1; h <= 3; h++) {
+    const long long k = side == 0 ? -h : c->g.n[2] - 1 + h;
+    CK(cudaMemcpy2DAsync(c->Bst + k * (long long)c->plane + slot * c->g.vs, sizeof(double) * c->g.pitch,
+                         c->Bst + edge * (long long)c->plane + slot * c->g.vs, sizeof(double) * c->g.pitch,
+                         sizeof(double) * c->g.vs, c->g.n[1], cudaMemcpyDeviceToDevice, c->st),
+       "echo_halo_fill_field");
+  }
+  return ECHO_OK;
 }
 
 // ------------------------------------------------------------ slab halos
@@ -1058,6 +1155,7 @@ int echo_halo_link_ipc(echo_ctx* c, int side, const void* handles, int peer_nz) 
   if (!c || (side != 0 && side != 1)) return c ? fail(c, ECHO_E_ARG, "echo_halo_link_ipc: bad argument") : ECHO_E_ARG;
   ipc_close(c->rlink[side]);
   if (!handles) return ECHO_OK;
+  if (is_uct(c)) return fail(c, ECHO_E_ARG, "echo_halo_link_ipc: UCT slabs use the copy exchange (export / import)");
   if (!c->g.zhalo || c->g.bc[2][side] != ECHO_BC_HALO || peer_nz < ECHO_HALO_PLANES)
     return fail(c, ECHO_E_ARG, "echo_halo_link_ipc: the side must be a halo boundary facing a slab of >= 6 planes");
   const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(handles);
@@ -1111,6 +1209,7 @@ int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
     c->link[side] = nullptr;
     return ECHO_OK;
   }
+  if (is_uct(c)) return fail(c, ECHO_E_ARG, "echo_halo_link: UCT slabs use the copy exchange (export / import)");
   if (!c->g.zhalo || c->g.bc[2][side] != ECHO_BC_HALO || !peer->g.zhalo || peer->g.bc[2][1 - side] != ECHO_BC_HALO)
     return fail(c, ECHO_E_ARG, "echo_halo_link: both facing sides must be halo boundaries");
   if (peer->g.n[0] != c->g.n[0] || peer->g.n[1] != c->g.n[1] || peer->g.pitch != c->g.pitch || peer->ks != c->ks)
@@ -1124,18 +1223,19 @@ int echo_halo_link(echo_ctx* c, int side, echo_ctx* peer) {
 
 long long echo_halo_doubles(const echo_ctx* c) {
   if (!c || !c->g.zhalo) return 0;
-  return 8LL * c->g.vs * ECHO_HALO_PLANES * (long long)c->g.n[1];  // halo_copy: 8 slots x vs per row
+  // halo_copy: 8 slots x vs per row (+ 3 for UCT's staggered field), zhalo planes
+  return (is_uct(c) ? 11LL : 8LL) * c->g.vs * c->g.zhalo * (long long)c->g.n[1];
 }
 
-// message = [P planes][U^s planes] of the ECHO_HALO_PLANES owned planes next to `side`
-// A halo message holds, for each of the ECHO_HALO_PLANES x n2 rows next to a side, what the
-// neighbour's sweeps read of a ghost cell: the primitives rho, u~, p (P slots 0..4) and B
-// (Minkowski: U slots 5..7 of the stage-input U; Kerr-Schild: P slots 5..7) — 8 vs doubles per
-// row, rows packed (P part first, then the U part).  Z0 (P slot 5, Minkowski) and the hydro U of
-// ghost cells are never read there.
+// A halo message holds, for each of the zhalo x n2 rows next to a side, what the neighbour reads
+// of a ghost cell: the primitives rho, u~, p (P slots 0..4) and B (Minkowski: U slots 5..7 of the
+// stage-input U; Kerr-Schild: P slots 5..7) — 8 vs doubles per row — and with UCT the stage-input
+// staggered field b^1..3 (3 vs more), rows packed part by part.  Z0 (P slot 5, Minkowski) and the
+// hydro U of ghost cells are never read there.
 static int halo_copy(echo_ctx* c, int side, double* buf, bool out, int on_device, const char* where) {
-  const long long rows = (long long)ECHO_HALO_PLANES * c->g.n[1];
-  const long long k0 = out ? (side == 0 ? 0 : c->g.n[2] - ECHO_HALO_PLANES) : (side == 0 ? -ECHO_HALO_PLANES : c->g.n[2]);
+  const int H = c->g.zhalo;
+  const long long rows = (long long)H * c->g.n[1];
+  const long long k0 = out ? (side == 0 ? 0 : c->g.n[2] - H) : (side == 0 ? -H : c->g.n[2]);
   const size_t pitchB = sizeof(double) * c->g.pitch;
   const long long vs = c->g.vs;
   cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : (out ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice);
@@ -1143,7 +1243,7 @@ static int halo_copy(echo_ctx* c, int side, double* buf, bool out, int on_device
     double* arr;
     long long slot0, nslot;
   };
-  Part parts[2];
+  Part parts[3];
   int np = 0;
   if (c->ks) {
     parts[np++] = {c->P, 0, 8};
@@ -1151,6 +1251,7 @@ static int halo_copy(echo_ctx* c, int side, double* buf, bool out, int on_device
     parts[np++] = {c->P, 0, 5};
     parts[np++] = {ucur_mut(c), 5, 3};
   }
+  if (is_uct(c)) parts[np++] = {bcur(c), 0, 3};  // the stage-input staggered field b^1..3
   long long off = 0;
   for (int q = 0; q < np; q++) {
     const Part& pt = parts[q];
@@ -1185,12 +1286,15 @@ int echo_halo_fill(echo_ctx* c, int side) {
   if (c->g.bc[2][side] != ECHO_BC_OUTFLOW)
     return fail(c, ECHO_E_ARG, "echo_halo_fill: only an outflow side is filled locally (halo sides are imported)");
   const long long edge = side == 0 ? 0 : c->g.n[2] - 1;
-  for (int h = 1; h <= ECHO_HALO_PLANES; h++) {
+  for (int h = 1; h <= c->g.zhalo; h++) {
     const long long k = side == 0 ? -h : c->g.n[2] - 1 + h;
-    for (double* a : {c->P, ucur_mut(c)})
+    // (UCT: also the staggered field, A42: a ghost face takes the nearest owned face)
+    for (double* a : {c->P, ucur_mut(c), is_uct(c) ? c->Bst : nullptr}) {
+      if (!a) continue;
       CK(cudaMemcpyAsync(a + k * (long long)c->plane, a + edge * (long long)c->plane, sizeof(double) * c->plane,
                          cudaMemcpyDeviceToDevice, c->st),
          "echo_halo_fill");
+    }
   }
   return ECHO_OK;
 }

@@ -14,6 +14,9 @@ namespace echo {
 constexpr int kG = 5;  // halo: WENO5 (3) + DER6 (2), A12
 constexpr int kZH = 6; // stored z ghost planes per side in slab mode (kG + 1: the sweeps also
                        // produce the EMF on the first ghost plane, which the field-CD curl reads)
+constexpr int kZHU = 8;  // UCT slabs: the induction's DER needs the edge EMFs 3 planes into the
+                         // halo, their z reconstructions face data 5 planes in, whose HLL states
+                         // the primitives 7 planes in (+1: the staggered b^z of the last face)
 
 // FP64 constants that are not exact in a 32-bit-high-word immediate live in the
 // constant bank, so every DFMA takes them as a c[][] operand (otherwise the
@@ -31,7 +34,8 @@ struct GridP {
   double dx[3];     // (hi - lo) / n
   double idx[3];    // 1 / dx
   int bc[3][2];     // 0 periodic, 1 outflow, 2 halo (z only: planes filled by the caller, echo_halo_*)
-  int zhalo;        // z ghost planes are stored (kZH per side) and filled by the caller before each stage
+  int zhalo;        // stored z ghost planes per side (0: none; kZH, or kZHU with UCT), filled by the caller
+                    // before each stage
   int rec, der, divb;
   double der_jump;  // A31 DER shock switch (+inf: off; the host maps <= 0 to +inf)
   long long vs;     // variable stride inside a row: n1 rounded up to even (16-byte aligned variables, TMA)
@@ -169,8 +173,9 @@ ECHO_HD long long rec_base_id(const GridP& g, long long id) {  // id = linear ce
 
 // --------------------------------------------------------------- indices
 ECHO_D int map_index(int i, int n, int bclo, int bchi) {  // ghost rule A12/A13
-  if (i < 0) return bclo == 0 ? ((i % n) + n) % n : 0;
-  if (i >= n) return bchi == 0 ? (i % n) : n - 1;
+  // (bc 2: a slab side whose ghost planes are stored: the index itself)
+  if (i < 0) return bclo == 0 ? ((i % n) + n) % n : (bclo == 2 ? i : 0);
+  if (i >= n) return bchi == 0 ? (i % n) : (bchi == 2 ? i : n - 1);
   return i;
 }
 

@@ -230,7 +230,7 @@ ECHO_D void load_cells(const GridP& g, const LineGeom& lg, long long lb, int t, 
   using GE = Geo<AX>;
   // slab z sweep: ghosts are stored planes (-kZH .. n + kZH - 1); the clamp only touches the
   // cells past the line end that the last chunk's window over-fetches (never used)
-  const int ag = lg.stored ? min(max(x + lg.coff, -kZH), g.n[AX] + kZH - 1)
+  const int ag = lg.stored ? min(max(x + lg.coff, -g.zhalo), g.n[AX] + g.zhalo - 1)
                            : map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
   const long long off = lb + ag * axis_stride<AX>(g);
   const long long vs = g.vs;
@@ -534,7 +534,8 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
             if constexpr (UCT) {
               // A37: both states take the staggered normal field of face xf + 1/2 (owned by
               // cell xf; A42 ghost rule), b = sqrt(g) B
-              const long long fo = lb + (long long)map_index(xf, lg.na, g.bc[AX][0], g.bc[AX][1]) * as;
+              // (slab z sweep: the line's cell xf is the slab's cell xf + coff, ghosts stored)
+              const long long fo = lb + (long long)(lg.stored ? xf + lg.coff : map_index(xf, lg.na, g.bc[AX][0], g.bc[AX][1])) * as;
               const double bnv = Bface[fo + AX * vs] * (KS ? frcp(mf.sqrtg()) : 1.0);
               pl[5 + AX] = bnv;
               qR[5 + AX] = bnv;
@@ -542,7 +543,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
               hll_face(mf, e, pl, qR, AX, F, fsv, kFluxScale);
               if (xf >= 0 && xf < lg.na && line_ok) {
 #pragma unroll
-                for (int m = 0; m < 8; m++) FSo[lb + (long long)xf * as + m * vs] = fsv[m];
+                for (int m = 0; m < 8; m++) FSo[lb + (long long)(xf + lg.coff) * as + m * vs] = fsv[m];
               }
             } else {
               hll_face(mf, e, pl, qR, AX, F, nullptr, kFluxScale);
@@ -618,13 +619,17 @@ inline LineGeom make_line_geom(const GridP& g, const double* P, const double* R,
   lg.coff = 0;
   lg.stored = 0;
   if (g.zhalo) {
-    if (AX == 2) {  // lines over the owned planes and the first ghost plane on each side
-      lg.na += 2;
-      lg.coff = -1;
+    // field-CD: the owned planes and the first ghost plane on each side (the x/y sweeps' EMF there
+    // feeds the curl); UCT: 5 ghost planes on each side (the face data the edge EMFs of 3 ghost
+    // planes reconstruct along z)
+    const int ext = g.divb == 2 ? 5 : 1;
+    if (AX == 2) {
+      lg.na += 2 * ext;
+      lg.coff = -ext;
       lg.stored = 1;
-    } else {        // x/y sweeps also on the first ghost planes (their EMF feeds the curl)
-      lg.nz += 2;
-      lg.zoff = -1;
+    } else {
+      lg.nz += 2 * ext;
+      lg.zoff = -ext;
     }
   }
   if (AX != 2 && zr.zn > 0) {  // x/y sweeps over planes zb .. zb + zn - 1 only (slab overlap, echo.h)

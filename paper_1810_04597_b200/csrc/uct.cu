@@ -147,7 +147,8 @@ constexpr int kZSeg = 16;  // planes per thread
 template <int REC, int CC>
 __global__ void __launch_bounds__(128, ECHO_EMF_ZM_BPS)
 k_uct_emf_zm(const GridP g, const double* __restrict__ FSx, const double* __restrict__ FSy,
-             const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed) {
+             const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed, const int kzb,
+             const int kze) {
   constexpr int p = (CC + 1) % 3, q = (CC + 2) % 3;
   constexpr bool ZQ = (q == 2);   // CC 0: z is q; CC 1: z is p
   constexpr int ip = ZQ ? p : q;  // the in-plane direction of the other pairs (y for CC 0, x for CC 1)
@@ -155,8 +156,10 @@ k_uct_emf_zm(const GridP g, const double* __restrict__ FSx, const double* __rest
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= g.n[0]) return;
-  const int k0 = blockIdx.z * kZSeg;
-  const int k1 = min(k0 + kZSeg, g.n[2]);
+  // planes kzb .. kze - 1: the owned ones, and in slab mode (stored ghost planes) 3 more below and
+  // 2 above, whose EMFs the induction's DER along z reads
+  const int k0 = kzb + blockIdx.z * kZSeg;
+  const int k1 = min(k0 + kZSeg, kze);
   const long long vs = g.vs;
   // along-z windows: 4 face-data streams (slot 3 side + comp), b (slot bz), speeds (slots 6, 7) at k, k+1
   const int comp[2] = {p, q};
@@ -538,12 +541,14 @@ k_uct_centre_p2c(const GridP g, const EosP e, const MetTables mt, double* __rest
 template <int REC>
 cudaError_t emf_rec(const GridP& g, const double* const FS[3], const double* Bin, double* Ed, cudaStream_t st) {
   if (ECHO_EMF_ZMARCH) {  // E^x, E^y marching along z; E^z one thread per edge
-    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSeg - 1) / kZSeg));
-    k_uct_emf_zm<REC, 0><<<zb, 128, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
-    k_uct_emf_zm<REC, 1><<<zb, 128, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed);
+    const int kzb = g.zhalo ? -3 : 0, kze = g.n[2] + (g.zhalo ? 2 : 0);
+    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((kze - kzb + kZSeg - 1) / kZSeg));
+    k_uct_emf_zm<REC, 0><<<zb, 128, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed, kzb, kze);
+    k_uct_emf_zm<REC, 1><<<zb, 128, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed, kzb, kze);
     const dim3 blocks((unsigned)((g.N + kCellThreads - 1) / kCellThreads), 1);
     k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed, 2);
   } else {
+    if (g.zhalo) return cudaErrorInvalidValue;  // slab mode needs the z-march (ghost-plane EMFs)
     const dim3 blocks((unsigned)((g.N + kCellThreads - 1) / kCellThreads), 3);
     k_uct_emf<REC><<<blocks, kCellThreads, 0, st>>>(g, FS[0], FS[1], FS[2], Bin, Ed, 0);
   }

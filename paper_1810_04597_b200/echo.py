@@ -34,7 +34,7 @@ METRIC_MINKOWSKI, METRIC_KERR_SCHILD = 0, 1
 
 class Grid(C.Structure):
     _fields_ = [("n", C.c_int * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("bc", (C.c_int * 2) * 3),
-                ("rec", C.c_int), ("der", C.c_int), ("divb", C.c_int), ("der_jump", C.c_double)]
+                ("rec", C.c_int), ("der", C.c_int), ("divb", C.c_int), ("der_jump", C.c_double), ("dz", C.c_double)]
 
 
 class Metric(C.Structure):
@@ -85,6 +85,12 @@ _sig = {
     "echo_stage_sweeps": (C.c_int, [_P, C.c_int]),
     "echo_stage_update": (C.c_int, [_P, C.c_int, C.c_double]),
     "echo_stage_sweeps_interior": (C.c_int, [_P, C.c_int]),
+    "echo_stage_update_field": (C.c_int, [_P, C.c_int, C.c_double]),
+    "echo_stage_update_cells": (C.c_int, [_P, C.c_int, C.c_double]),
+    "echo_halo_field_doubles": (C.c_longlong, [_P]),
+    "echo_halo_export_field": (C.c_int, [_P, C.c_int, _P, C.c_int]),
+    "echo_halo_import_field": (C.c_int, [_P, C.c_int, _P, C.c_int]),
+    "echo_halo_fill_field": (C.c_int, [_P, C.c_int]),
     "echo_stage_sweeps_boundary": (C.c_int, [_P, C.c_int]),
     "echo_halo_export": (C.c_int, [_P, C.c_int, _P, C.c_int]),
     "echo_halo_import": (C.c_int, [_P, C.c_int, _P, C.c_int]),
@@ -126,7 +132,7 @@ def _buf(a, writable=False):
     return a.data_ptr(), 1
 
 
-def _grid(n, lo, hi, bc, rec=0, der=6, divb=0, der_jump=0.5) -> Grid:
+def _grid(n, lo, hi, bc, rec=0, der=6, divb=0, der_jump=0.5, dz=0.0) -> Grid:
     g = Grid()
     for i in range(3):
         g.n[i] = int(n[i])
@@ -136,13 +142,14 @@ def _grid(n, lo, hi, bc, rec=0, der=6, divb=0, der_jump=0.5) -> Grid:
         g.bc[i][1] = int(bc[i][1])
     g.rec, g.der, g.divb = int(rec), int(der), int(divb)
     g.der_jump = float(der_jump)
+    g.dz = float(dz)
     return g
 
 
 # ------------------------------------------------------------- C names
 def create(n, lo, hi, bc, metric=METRIC_MINKOWSKI, M=1.0, a=0.0, gamma=4.0 / 3.0, rho_floor=1e-8, p_floor=1e-10,
-           w_max=50.0, c2p_max_iter=30, c2p_tol=1e-13, rec=0, der=6, divb=0, der_jump=0.5):
-    g = _grid(n, lo, hi, bc, rec, der, divb, der_jump)
+           w_max=50.0, c2p_max_iter=30, c2p_tol=1e-13, rec=0, der=6, divb=0, der_jump=0.5, dz=0.0):
+    g = _grid(n, lo, hi, bc, rec, der, divb, der_jump, dz)
     m = Metric(int(metric), float(M), float(a))
     e = Eos(float(gamma), float(rho_floor), float(p_floor), float(w_max), int(c2p_max_iter), float(c2p_tol))
     out = _P()
@@ -314,6 +321,32 @@ def stage_sweeps(ctx, s: int):
 
 def stage_update(ctx, s: int, dt: float):
     return _check(ctx, _lib.echo_stage_update(ctx, int(s), float(dt)))
+
+
+def stage_update_field(ctx, s: int, dt: float):
+    return _check(ctx, _lib.echo_stage_update_field(ctx, int(s), float(dt)))
+
+
+def stage_update_cells(ctx, s: int, dt: float):
+    return _check(ctx, _lib.echo_stage_update_cells(ctx, int(s), float(dt)))
+
+
+def halo_field_doubles(ctx) -> int:
+    return int(_lib.echo_halo_field_doubles(ctx))
+
+
+def halo_export_field(ctx, side: int, buf):
+    p, d = _buf(buf, True)
+    return _check(ctx, _lib.echo_halo_export_field(ctx, int(side), p, d))
+
+
+def halo_import_field(ctx, side: int, buf):
+    p, d = _buf(buf)
+    return _check(ctx, _lib.echo_halo_import_field(ctx, int(side), p, d))
+
+
+def halo_fill_field(ctx, side: int):
+    return _check(ctx, _lib.echo_halo_fill_field(ctx, int(side)))
 
 
 def stage_sweeps_interior(ctx, s: int):

@@ -30,7 +30,8 @@ def _port():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("cfg,n,extra", [(0, (48, 40, 36), []), (2, (40, 36, 44), []), (0, (48, 40, 36), ["--fused"])])
+@pytest.mark.parametrize("cfg,n,extra", [(0, (48, 40, 36), []), (2, (40, 36, 44), []), (0, (48, 40, 36), ["--fused"]),
+                                         (0, (40, 32, 36), ["--divb", "2"]), (4, (48, 35, 36), ["--divb", "2"])])
 def test_slabs_across_gpus_bitwise(tmp_path, cfg, n, extra):
     from paper_1810_04597_b200 import build
 
@@ -44,3 +45,4 @@ def test_slabs_across_gpus_bitwise(tmp_path, cfg, n, extra):
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(out.read_text())
     assert res["world"] == world and res["dt_equal"] and res["U_bitwise"] and res["P_bitwise"], res
+    assert res.get("b_bitwise", True), res

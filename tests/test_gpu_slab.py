@@ -94,3 +94,51 @@ def test_slab_api_errors(E):
     with pytest.raises(E.EchoError):
         E.create(n=(8, 8, 8), lo=(0, 0, 0), hi=(1, 1, 1), bc=((2, 2), (0, 0), (0, 0)))  # halo only along z
     g.close()
+
+
+@pytest.mark.parametrize("cfg,n,nslabs,steps", [
+    (0, (24, 20, 32), 2, 2),     # periodic turbulence, a ring of 2
+    (0, (20, 16, 27), 3, 2),     # 3 unequal periodic slabs (9 planes each)
+    (2, (20, 18, 36), 3, 2),     # outflow blast: physical ends filled locally (b included, A42)
+    (4, (48, 35, 24), 2, 2),     # Kerr-Schild torus, slabs in phi
+])
+def test_uct_slabs_match_single_domain_bitwise(E, orc, cfg, n, nslabs, steps):
+    """UCT (divb = 2) on z slabs with the copy exchange: ECHO_HALO_PLANES_UCT = 8 ghost planes,
+    the messages carry the staggered field too; the x/y sweeps and the z sweep cover 5 ghost
+    planes, the edge EMFs 3.  Bit for bit the single-domain UCT run, b included."""
+    from paper_1810_04597_b200.slab import LocalSlabs
+
+    p = I.problem(cfg, n=n)
+    p.divb = 2
+    P8, b3 = I.initial_prims(p), I.face_field(p)
+    one = E.Echo(p)
+    one.set_prims(P8)
+    one.set_face_field(b3)
+    sl = LocalSlabs(p, nslabs)
+    sl.set_prims(P8)
+    sl.set_face_field(b3)
+    assert np.array_equal(sl.gather(lambda g: g.get_state()[0]), one.get_state()[0])  # the centring, edges included
+    for _ in range(steps):
+        dt1 = one.max_dt(p.cfl)
+        assert sl.max_dt(p.cfl) == dt1
+        one.step(dt1)
+        sl.step(dt1)
+    assert np.array_equal(sl.gather(lambda g: g.get_state()[0]), one.get_state()[0])
+    assert np.array_equal(sl.gather(lambda g: g.get_state()[2]), one.get_state()[2])
+    assert np.array_equal(sl.gather(lambda g: g.get_face_field()), one.get_face_field())
+    st = [g.stats() for g, _, _ in sl.parts]
+    assert sum(s["floor_events"] for s in st) == one.stats()["floor_events"]
+    sl.close()
+    one.close()
+
+
+def test_uct_slab_refusals(E):
+    """UCT slabs: thinner than 8 planes, or the fused links, are refused."""
+    with pytest.raises(E.EchoError):
+        E.create(n=(8, 8, 7), lo=(0, 0, 0), hi=(1, 1, 1), bc=((0, 0), (0, 0), (2, 2)), divb=2)
+    p = I.problem(0, n=(8, 8, 16))
+    p.divb = 2
+    g = E.Echo(p, bc=((0, 0), (0, 0), (E.BC_HALO, E.BC_HALO)))
+    with pytest.raises(E.EchoError):
+        E.halo_link(g.ctx, 0, g.ctx)
+    g.close()

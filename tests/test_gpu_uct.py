@@ -147,11 +147,17 @@ def test_uct_api_rules(E):
     h.set_prims(P8)
     with pytest.raises(E.EchoError):
         h.set_face_field(I.face_field(p))
-    r = I.problem(0, n=(16, 16, 16))  # slab (halo) boundaries: UCT refused at create
+    r = I.problem(0, n=(16, 16, 7))  # UCT slabs need >= ECHO_HALO_PLANES_UCT = 8 planes
     r.divb = 2
     r.bc = ((0, 0), (0, 0), (2, 2))
     with pytest.raises(E.EchoError):
         E.Echo(r)
+    with pytest.raises(E.EchoError):  # and no echo_step on a slab (an exchange precedes every stage)
+        r.n = (16, 16, 16)
+        s = E.Echo(r)
+        s.set_prims(I.initial_prims(I.problem(0, n=(16, 16, 16))))
+        s.set_face_field(I.face_field(I.problem(0, n=(16, 16, 16))))
+        s.step(1e-3)
 
 
 def test_uct_full_size_conservation_and_divh(E):

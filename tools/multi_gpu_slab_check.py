@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--n", type=int, nargs=3, default=[48, 40, 36])
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--fused", action="store_true")
+    ap.add_argument("--divb", type=int, default=0)
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     import numpy as np
@@ -34,12 +35,16 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     p = I.problem(a.config, n=tuple(a.n))
+    p.divb = a.divb
     P8 = I.initial_prims(p)
+    B3 = I.face_field(p) if a.divb == 2 else None
     sp, (z0, nz) = slab.slab_problem(p, rank, world)
     g = echo.Echo(sp)
     echo.set_stream(g.ctx, torch.cuda.current_stream(dev).cuda_stream)
     g.set_prims(np.ascontiguousarray(P8[:, z0:z0 + nz]))
-    D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev)
+    D = slab.DistSlab(slab.CtxIO(g), rank, world, p.bc[2][0] == 0, dev, uct=a.divb == 2)
+    if B3 is not None:
+        D.set_face_field(np.ascontiguousarray(B3[:, z0:z0 + nz]))
     if a.fused:
         D.link_fused()
     dts = []
@@ -48,11 +53,14 @@ def main():
         dts.append(dt)
         (D.step_fused if a.fused else D.step)(dt)
     un, _, pp = g.get_state()
+    bb = g.get_face_field() if B3 is not None else np.zeros(1)
     parts = [None] * world
-    dist.all_gather_object(parts, (z0, nz, un, pp))
+    dist.all_gather_object(parts, (z0, nz, un, pp, bb))
     if rank == 0:
         ref = echo.Echo(p)
         ref.set_prims(P8)
+        if B3 is not None:
+            ref.set_face_field(B3)
         rdts = []
         for _ in range(a.steps):
             dt = ref.max_dt(p.cfl)
@@ -64,6 +72,9 @@ def main():
         res = {"world": world, "dt_equal": dts == rdts, "U_bitwise": bool(np.array_equal(un_all, run)),
                "P_bitwise": bool(np.array_equal(pp_all, rpp)),
                "max_abs_dU": float(np.max(np.abs(un_all - run)))}
+        if B3 is not None:
+            b_all = np.concatenate([x[4] for x in sorted(parts, key=lambda x: x[0])], axis=1)
+            res["b_bitwise"] = bool(np.array_equal(b_all, ref.get_face_field()))
         with open(a.out, "w") as f:
             json.dump(res, f)
         ref.close()
