@@ -66,7 +66,7 @@ ECHO_D double emf_combine(const double pS[2][2], const double pN[2][2], const do
   const double EEN = v[3][1] * bpN - v[3][0] * bqE;
   const double sp = app + apm, sq = aqp + aqm;
   if (sp > 0.0 && sq > 0.0) {
-    const double isp = 1.0 / sp, isq = 1.0 / sq;
+    const double isp = frcp(sp), isq = frcp(sq);  // (MUFU seed + refinement, A32)
     return (app * (aqp * EWS + aqm * EWN) + apm * (aqp * EES + aqm * EEN)) * (isp * isq) +
            app * apm * (bqE - bqW) * isp - aqp * aqm * (bpN - bpS) * isq;
   }
