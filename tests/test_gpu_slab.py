@@ -142,3 +142,24 @@ def test_uct_slab_refusals(E):
     with pytest.raises(E.EchoError):
         E.halo_link(g.ctx, 0, g.ctx)
     g.close()
+
+
+def test_destroy_unlinks_the_peers(E):
+    """A context linked to a peer (echo_halo_link) forgets the link when the peer is destroyed:
+    its updates can no longer store into freed ghost planes (echo_halo_pull then reports the
+    side as unlinked)."""
+    p = I.problem(0, n=(8, 8, 24))
+    bc = ((0, 0), (0, 0), (E.BC_HALO, E.BC_HALO))
+    a = E.Echo(p, n=(8, 8, 12), bc=bc)
+    b = E.Echo(p, n=(8, 8, 12), bc=bc)
+    E.halo_link(a.ctx, 1, b.ctx)
+    E.halo_link(b.ctx, 0, a.ctx)
+    P8 = I.initial_prims(I.problem(0, n=(8, 8, 12)))
+    a.set_prims(P8)
+    b.set_prims(P8)
+    E.halo_pull(a.ctx, 1)  # linked: fine
+    b.close()
+    with pytest.raises(E.EchoError) as ei:
+        E.halo_pull(a.ctx, 1)
+    assert "not linked" in str(ei.value)
+    a.close()
