@@ -10,7 +10,8 @@ checked against the oracle's at every step.
 
 * config 1 (128^3 CP Alfven wave), config 2 (256^3 blast, A31 active at the shock),
   config 4 (256 x 128 x 256 Kerr-Schild torus, floors firing in the atmosphere): 10 steps.
-* UCT (divb = 2) on configs 1 and 4: 10 steps, the staggered field included.
+* UCT (divb = 2) on configs 1 and 4: 10 steps, the staggered field included (config 4 with
+  ECHO_FULL_UCT4=1, to keep the suite's oracle time well inside the driver's budget).
 * config 3 (512^3): 5 steps.  The oracle needs ~45 GB of host RAM and ~10 min of host
   CPU for it, so it runs only with ECHO_FULL_CFG3=1 (the committed log of that run is
   profiles/r02_fullsize_parity.txt).
@@ -96,10 +97,13 @@ def test_full_size_cfg3_5_step_parity(E, orc):
     _run(E, orc, 3, 5)
 
 
-@pytest.mark.parametrize("cfg", [1, 4])
+@pytest.mark.parametrize("cfg", [1, pytest.param(4, marks=pytest.mark.skipif(
+    os.environ.get("ECHO_FULL_UCT4") != "1", reason="~2.5 min of host oracle: ECHO_FULL_UCT4=1 (log in profiles/)"))])
 def test_full_size_10_step_parity_uct(E, orc, cfg):
     """UCT (divb = 2, readings A37-A43) at the same full sizes: configs 1 (128^3) and 4
-    (256 x 128 x 256, Kerr-Schild), 10 steps, every cell, the staggered field included."""
+    (256 x 128 x 256, Kerr-Schild), 10 steps, every cell, the staggered field included.  Config 4
+    (137 s of oracle on the box's 16 cores) runs with ECHO_FULL_UCT4=1; its log is in
+    profiles/r02_fullsize_parity.txt."""
     p = I.problem(cfg)
     p.divb = 2
     oc = orc.Cfg(**p.grid_kwargs())

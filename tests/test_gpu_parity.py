@@ -195,8 +195,8 @@ def test_switches_parity(E, orc):
 
 # ------------------------------------------------ full-size sampled parity
 # (config, reconstruction): the default WENO5 on every config, plus the characteristic-wise
-# (rec 6, A44) and MP5 (rec 2) sweeps at 512^3 and the characteristic-wise at the blast
-FULL = [(1, None), (2, None), (4, None), (3, None), (3, 6), (2, 6), (3, 2)]
+# (rec 6, A44) sweeps at 512^3 and at the blast
+FULL = [(1, None), (2, None), (4, None), (3, None), (3, 6), (2, 6)]
 
 
 def _full_state(E, p, device_ic):
