@@ -8,7 +8,7 @@ template <int AX, bool KS, int DER, int REC, int DM>
 static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB,
                               double* R, const double* Bface, double* FSo, cudaStream_t st,
                               const PlaneRange& zr) {
-  using GE = Geo<AX>;
+  using GE = typename GeoSel<AX, DM>::type;
   auto kern = k_march<AX, KS, DER, REC, DM>;
   // per device (the attribute and the occupancy are per-device properties); the cache is
   // written at most once per device, racing writers store the same value
@@ -26,7 +26,7 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
     grid_cap = sms * (per > 0 ? per : 1);
     if (dev < kMaxDev) grid_caps[dev].store(grid_cap, std::memory_order_relaxed);
   }
-  const LineGeom lg = make_line_geom<AX>(g, P, R, zr);
+  const LineGeom lg = make_line_geom<AX, GE>(g, P, R, zr);
   unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
   if (ECHO_PDL && AX != 0) {  // y/z: may start over the previous sweep's tail (griddepcontrol)
     cudaLaunchConfig_t cfg{};

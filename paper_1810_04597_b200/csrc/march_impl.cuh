@@ -72,14 +72,31 @@ namespace march {
 #define ECHO_YZ_CH 4
 #define ECHO_YZ_BPS 12
 #endif
+// -DECHO_YZ_TRANS=1: the field-CD / divb-none y/z sweeps (not UCT's) take the x sweep's thread
+// mapping (one warp per line, 32 cells per chunk) over NL = 8 x-adjacent lines, and every global
+// access is transposed through shared memory: the ring is filled by lanes running over the 8
+// lines (64-byte rows), and the rhs contributions of a chunk are written to a shared buffer
+// that the next chunk adds to the accumulator with the same transposed mapping (CTA barriers)
+#ifndef ECHO_YZ_TRANS
+#define ECHO_YZ_TRANS 0
+#endif
+#ifndef ECHO_YZT_NL
+#define ECHO_YZT_NL 8
+#define ECHO_YZT_BPS 3
+#endif
 struct GeomSpec {
   int nl, ch, bps;
 };
 constexpr GeomSpec kGeomX{ECHO_X_NL, ECHO_X_CH, ECHO_X_BPS};
 constexpr GeomSpec kGeomYZ{ECHO_YZ_NL, ECHO_YZ_CH, ECHO_YZ_BPS};
+constexpr GeomSpec kGeomYZT{ECHO_YZT_NL, 32, ECHO_YZT_BPS};
 
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 constexpr bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+// the smallest stride >= n that is r mod 16 doubles (r = 16 / lines): a half-warp's transposed
+// accesses (NL lines x 16/NL positions) and 16 consecutive positions of one line (the march's
+// reads) both hit distinct bank pairs
+constexpr int pad16(int n, int r) { return n + ((16 + r - n % 16) % 16); }
 
 #ifdef ECHO_YZ_LINE_MAJOR
 constexpr bool kYzLineMajor = true;
@@ -87,11 +104,14 @@ constexpr bool kYzLineMajor = true;
 constexpr bool kYzLineMajor = false;
 #endif
 
-template <int AX>
+// V = 1: the transposed y/z geometry (ECHO_YZ_TRANS)
+template <int AX, int V = 0>
 struct Geo {
-  static constexpr GeomSpec S = (AX == 0) ? kGeomX : kGeomYZ;
-  // line-major thread mapping (slot fastest): the x sweep, and y/z with ECHO_YZ_LINE_MAJOR
-  static constexpr bool LM = (AX == 0) || kYzLineMajor;
+  static constexpr bool TRANS = V == 1;
+  static_assert(!TRANS || AX != 0, "the transposed geometry is the y/z sweeps'");
+  static constexpr GeomSpec S = TRANS ? kGeomYZT : (AX == 0) ? kGeomX : kGeomYZ;
+  // line-major thread mapping (slot fastest): the x sweep, and y/z with ECHO_YZ_LINE_MAJOR or TRANS
+  static constexpr bool LM = (AX == 0) || kYzLineMajor || TRANS;
   static constexpr int NL = S.nl;
   static constexpr int CH = S.ch;                             // cells per chunk = threads per line
   static constexpr int LOG_NL = ilog2(NL);
@@ -103,11 +123,19 @@ struct Geo {
 #else
   static constexpr bool TIGHT = false;
 #endif
-  static constexpr int RING = TIGHT ? CH + 10
+  // TRANS: multiples of 16 (a line's 16 consecutive positions stay on distinct bank pairs across
+  // the wrap) that fit 3 CTAs of 8 lines per SM
+  static constexpr int RING = TRANS ? (CH + 10 + 15) / 16 * 16
+                            : TIGHT ? CH + 10
                                     : (CH + 10 <= 16) ? 16 : (CH + 10 <= 32) ? 32 : (CH + 10 <= 64) ? 64 : CH + 16;
   // face-flux ring: B(c) writes faces B+2..B+CH+1 while faces B-2..B+1 are still needed by D(c+1)
-  static constexpr int RINGF = TIGHT ? CH + 4
+  static constexpr int RINGF = TRANS ? (CH + 4 + 15) / 16 * 16
+                             : TIGHT ? CH + 4
                                      : (CH + 4 <= 8) ? 8 : (CH + 4 <= 32) ? 32 : (CH + 4 <= 64) ? 64 : CH + 16;
+  // line strides of the primitive ring and of the rhs-contribution buffer (TRANS: both are
+  // written or read transposed, so padded to 2 mod 16)
+  static constexpr int LSP = TRANS ? pad16(RING, 16 / NL) : RING;
+  static constexpr int LSD = TRANS ? pad16(CH, 16 / NL) : CH;
   // first chunk: its A phase reaches down to the ghost cell -3 (WENO of cells -3.. for faces -3..)
   static constexpr int C_FIRST = -((6 + CH - 1) / CH);
   static constexpr int B_FIRST = C_FIRST * CH;
@@ -119,26 +147,35 @@ struct Geo {
   static constexpr int DELTA = LM ? 1 : NL;                   // lane distance between slots i and i+1
   static constexpr int SLOTS_PER_WARP = 32 / DELTA;           // consecutive slots inside one warp
   static constexpr int NEDGE = CH / SLOTS_PER_WARP;           // warp-edge slots per line
-  static constexpr int VP = NL * RING;                        // variable stride, primitive ring
+  static constexpr int VP = NL * LSP;                         // variable stride, primitive ring
   static constexpr int VF = NL * RINGF;                       // component stride, F ring
   static constexpr int VA = NL * CH;                          // component stride, accumulation buffer
   static constexpr int VE = NL * NEDGE;                       // variable stride, edge buffers
+  static constexpr int VD = NL * LSD;                         // component stride, TRANS rhs contributions
   static constexpr int OFF_P = 0;
   static constexpr int OFF_F = OFF_P + 8 * VP;
   static constexpr int OFF_A = OFF_F + 7 * VF;
   // the y/z accumulation buffer (none with ECHO_ACC_REGS: the old values are held in registers)
-  static constexpr int OFF_E = OFF_A + ((AX == 0 || ECHO_ACC_REGS) ? 0 : 7 * VA);  // left states qL at warp edges [2][8]
+  static constexpr int OFF_D = OFF_A + ((AX == 0 || ECHO_ACC_REGS || TRANS) ? 0 : 7 * VA);
+  static constexpr int OFF_E = OFF_D + (TRANS ? 7 * VD : 0);  // left states qL at warp edges [2][8]
   static constexpr int OFF_HE = OFF_E + 2 * 8 * VE;                 // DER fluxes H at warp edges [2][7]
   static constexpr int TOTAL = OFF_HE + 2 * 7 * VE;
   static constexpr size_t SMEM = sizeof(double) * TOTAL + NL * RR;  // + A31 flag ring (bytes)
   // x sweep with one warp per line: every exchange of the march (ring, edges, flags, loads) stays
   // inside the warp, so the chunk barriers are warp barriers and the warps run decoupled
   // (likewise any one-warp CTA, e.g. y/z: 8 lines x 4 cells)
-  static constexpr bool WARP_LOCAL = (LM && CH == 32) || THREADS == 32;
+  static constexpr bool WARP_LOCAL = !TRANS && ((LM && CH == 32) || THREADS == 32);
   static_assert(is_pow2(NL) && is_pow2(CH), "NL and CH must be powers of two");
   static_assert(CH >= 4 && THREADS <= 1024 && THREADS >= 32 && (LM ? CH >= 32 : NL <= 32),
                 "unsupported line geometry");
   static_assert(AX != 0 || NL * CH <= 1024, "x geometry");
+  static_assert(!TRANS || (CH == 32 && ECHO_ACC_REGS), "TRANS: 32-cell chunks, accumulator in registers");
+  // shared-memory offsets: primitive ring, face-flux ring, accumulation / contribution buffers
+  // (conflict-free: slot/position fastest for line-major mappings, line fastest otherwise)
+  static ECHO_HD int pofs(int t, int pos) { return LM ? t * LSP + pos : pos * NL + t; }
+  static ECHO_HD int fofs(int t, int pos) { return LM ? t * RINGF + pos : pos * NL + t; }
+  static ECHO_HD int aofs(int t, int i) { return LM ? t * CH + i : i * NL + t; }
+  static ECHO_HD int dofs(int t, int i) { return t * LSD + i; }
   // a ring position of cell/face x (x may be negative)
   static ECHO_HD int ring(int x) {
     if constexpr (is_pow2(RING)) return x & (RING - 1);
@@ -151,23 +188,25 @@ struct Geo {
   }
 };
 
-template <int AX>
+template <int AX, class GE = Geo<AX>>
 ECHO_HD int ringf(int x) {
-  constexpr int RF = Geo<AX>::RINGF;
+  constexpr int RF = GE::RINGF;
   if constexpr (is_pow2(RF)) return x & (RF - 1);
   else return ((x % RF) + RF) % RF;
 }
-template <int AX>
+template <int AX, class GE = Geo<AX>>
 ECHO_HD int wrapf(int p) {
-  constexpr int RF = Geo<AX>::RINGF;
+  constexpr int RF = GE::RINGF;
   if constexpr (is_pow2(RF)) return p & (RF - 1);
   else return p >= RF ? p - RF : (p < 0 ? p + RF : p);
 }
 
-template <int AX, int LEN>
-ECHO_HD int loff(int t, int pos) {  // conflict-free: slot/position fastest for x, line fastest for y/z
-  return Geo<AX>::LM ? t * LEN + pos : pos * Geo<AX>::NL + t;
-}
+// the sweep geometry of axis AX and divergence treatment DM (UCT keeps the lane-over-lines y/z
+// geometry: its face-data stores are per lane)
+template <int AX, int DM>
+struct GeoSel {
+  using type = Geo<AX, (AX != 0 && DM != 2 && ECHO_YZ_TRANS) ? 1 : 0>;
+};
 
 ECHO_HD int first_axis(int comp) { return comp == 0 ? 1 : 0; }
 template <int AX, bool DN>
@@ -204,9 +243,9 @@ struct LineGeom {
   long long nunits;
 };
 
-template <int AX>
+template <int AX, class GE = Geo<AX>>
 ECHO_D void unit_origin(const LineGeom& lg, long long unit, int& t0, int& zz) {
-  t0 = (int)(unit % lg.tt_groups) * Geo<AX>::NL;
+  t0 = (int)(unit % lg.tt_groups) * GE::NL;
   zz = (int)(unit / lg.tt_groups) + lg.zoff;
 }
 
@@ -224,17 +263,16 @@ ECHO_D long long axis_stride(const GridP& g) {
 }
 
 // cp.async of the primitives of cell x of line t (line record base lb) into the ring
-template <int AX>
+template <int AX, class GE = Geo<AX>>
 ECHO_D void load_cells(const GridP& g, const LineGeom& lg, long long lb, int t, int x, bool vec,
                        const double* __restrict__ P, const double* __restrict__ UB, unsigned sbase) {
-  using GE = Geo<AX>;
   // slab z sweep: ghosts are stored planes (-kZH .. n + kZH - 1); the clamp only touches the
   // cells past the line end that the last chunk's window over-fetches (never used)
   const int ag = lg.stored ? min(max(x + lg.coff, -g.zhalo), g.n[AX] + g.zhalo - 1)
                            : map_index(x, lg.na, g.bc[AX][0], g.bc[AX][1]);
   const long long off = lb + ag * axis_stride<AX>(g);
   const long long vs = g.vs;
-  const unsigned s = sbase + 8u * (GE::OFF_P + loff<AX, GE::RING>(t, GE::ring(x)));
+  const unsigned s = sbase + 8u * (GE::OFF_P + GE::pofs(t, GE::ring(x)));
 #pragma unroll
   for (int v = 0; v < 8; v++) {
     const double* src = (v < 5 ? P : UB) + off + v * vs;
@@ -249,18 +287,36 @@ ECHO_D long long line_base(const GridP& g, const LineGeom& lg, int t0, int zz, i
   return base_of<AX>(g, 0, min(t0 + t, lg.nt - 1), zz);
 }
 
-// the first window [-5, CH + 5) of a line group (cells -5..4 feed the prologue chunk)
-template <int AX>
+// the first window [-5, CH + 5) of a line group (cells -5..4 feed the prologue chunk); (t, i): the
+// loading thread's line and slot (TRANS: its transposed pair)
+template <int AX, class GE = Geo<AX>>
 ECHO_D void load_window(const GridP& g, const LineGeom& lg, long long unit, int t, int i,
                         const double* __restrict__ P, const double* __restrict__ UB, unsigned sbase) {
-  using GE = Geo<AX>;
   int t0, zz;
-  unit_origin<AX>(lg, unit, t0, zz);
+  unit_origin<AX, GE>(lg, unit, t0, zz);
   const bool vec = !GE::LM && lg.vec16 && (t0 + GE::NL <= lg.nt);
   if (vec && (t & 1)) return;
   const long long lb = line_base<AX>(g, lg, t0, zz, t);
 #pragma unroll
-  for (int x = -kG + i; x <= GE::B_FIRST + 2 * GE::CH + 4; x += GE::CH) load_cells<AX>(g, lg, lb, t, x, vec, P, UB, sbase);
+  for (int x = -kG + i; x <= GE::B_FIRST + 2 * GE::CH + 4; x += GE::CH) load_cells<AX, GE>(g, lg, lb, t, x, vec, P, UB, sbase);
+}
+
+// TRANS: R (cell X0p + iT of line tT) = old value accT + the contribution in the shared buffer
+template <int AX, class GE, bool DN>
+ECHO_D void store_contrib(const GridP& g, const LineGeom& lg, double* R, long long lbT, bool lineT_ok, int tT, int iT,
+                          int X0p, const double (&accT)[7], const double* smem) {
+  if (!(X0p + iT < lg.na && lineT_ok)) return;
+  const long long vs = g.vs;
+  const double idxa = g.idx[AX];
+  double* dst = R + lbT + (long long)(X0p + iT + lg.coff) * axis_stride<AX>(g);
+#pragma unroll
+  for (int q = 0; q < 7; q++) {
+    const double dq = smem[GE::OFF_D + q * GE::VD + GE::dofs(tT, iT)];
+    double v;
+    if (q < 5 || DN) v = accumulates<AX, DN>(q) ? fma(dq, idxa, accT[q]) : dq * idxa;
+    else v = accumulates<AX, DN>(q) ? accT[q] + dq : dq;
+    dst[out_slot<AX, DN>(q) * vs] = v;
+  }
 }
 
 // DM: divergence treatment 0 field-CD (EMF Omega into R slots 5..7), 1 none (B flux
@@ -273,12 +329,13 @@ template <int AX, bool KS, int DER, int REC, int DM>
 ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const LineGeom& lg, const long long unit,
                        const long long next, const double* __restrict__ P, const double* __restrict__ UB, double* R,
                        const double* __restrict__ Bface, double* __restrict__ FSo, double* smem, bool& dep_waited) {
-  using GE = Geo<AX>;
+  using GE = typename GeoSel<AX, DM>::type;
+  constexpr bool TR = GE::TRANS;
   constexpr bool DN = DM == 1;
   constexpr bool UCT = DM == 2;
   constexpr int CH = GE::CH, RING = GE::RING, RINGF = GE::RINGF, RR = GE::RR;
   // A31 flags as ballots: warp-local kernels whose chunk of a line lies in one warp
-  constexpr bool kBallot = ECHO_BALLOT_FLAGS && GE::WARP_LOCAL && (GE::LM ? CH == 32 : CH * GE::NL == 32);
+  constexpr bool kBallot = ECHO_BALLOT_FLAGS && (GE::LM ? CH == 32 : (GE::WARP_LOCAL && CH * GE::NL == 32));
   unsigned char* rough = reinterpret_cast<unsigned char*>(smem + GE::TOTAL);  // [NL][RR] face flags
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const int tid = threadIdx.x;
@@ -291,23 +348,27 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
   const double idxa = g.idx[AX];
   const double kFluxScale = AX == 0 ? idxa : 1.0;
   const long long vs = g.vs;
+  // TRANS: the transposed pair (line, slot) of this thread for every global access
+  const int tT = TR ? (tid & (GE::NL - 1)) : t;
+  const int iT = TR ? (tid >> GE::LOG_NL) : i;
 
   {
     int t0, zz;
-    unit_origin<AX>(lg, unit, t0, zz);
+    unit_origin<AX, GE>(lg, unit, t0, zz);
     const bool line_ok = t0 + t < lg.nt;
     const long long lb = line_base<AX>(g, lg, t0, zz, t);
     const long long as = axis_stride<AX>(g);
     const int tt = min(t0 + t, lg.nt - 1);
     const bool vec = !GE::LM && lg.vec16 && (t0 + GE::NL <= lg.nt);
+    const long long lbT = TR ? line_base<AX>(g, lg, t0, zz, tT) : lb;  // (TRANS) line tT's record base
+    const bool lineT_ok = t0 + tT < lg.nt;
     unsigned long long fhist = 0ull;  // A31 flags of this line's faces, newest chunk in the top CH bits
     int rb = GE::ring(GE::B_FIRST);  // primitive-ring position of the chunk base B
-    int rbf = ringf<AX>(GE::B_FIRST);  // face-flux-ring position of B
-    // Chunk c (base B = c CH): A = WENO of cells B+3+i, B = HLL at faces B+2+i, D = DER + flux
-    // difference of the cells of chunk c-1 (their faces up to B+1 were written by B(c-1)), so one
-    // chunk needs two barriers.  c = -1 is the prologue (A/B of the line start), c = nchunks the
-    // epilogue (D of the last chunk).
-    for (int c = GE::C_FIRST; c <= lg.nchunks; c++, rb = GE::wrap(rb + CH), rbf = wrapf<AX>(rbf + CH)) {
+    int rbf = ringf<AX, GE>(GE::B_FIRST);  // face-flux-ring position of B
+    double accT[7];  // (TRANS) the old rhs/EMF values of cell (tT, X0 + iT), added by the next chunk
+    // (TRANS) store_contrib: the rhs contributions of the previous chunk's output cells X0p + slot
+    // (written to the shared buffer by their lanes in D2) added to the accumulator, transposed
+    for (int c = GE::C_FIRST; c <= lg.nchunks; c++, rb = GE::wrap(rb + CH), rbf = wrapf<AX, GE>(rbf + CH)) {
       const int B = c * CH;
       const int par = c & 1;
       const bool ab = c < lg.nchunks;       // A and B phases
@@ -317,12 +378,20 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
       if constexpr (GE::WARP_LOCAL) __syncwarp();
       else __syncthreads();  // (0) primitives of chunk c landed; F, flags and edges of chunk c-1 visible
       double acc[7];  // ECHO_ACC_REGS: the old rhs/EMF values of the output cell, in registers
+      if constexpr (TR) {
+        if (c >= 2) store_contrib<AX, GE, DN>(g, lg, R, lbT, lineT_ok, tT, iT, X0 - CH, accT, smem);  // chunk c-1's
+      }
       if (AX != 0 && d2) {  // old rhs/EMF values of the output cells (accumulated in D)
         if (!dep_waited) {  // the previous sweep's R (uniform: every thread reaches it at the same chunk)
           asm volatile("griddepcontrol.wait;" ::: "memory");
           dep_waited = true;
         }
-        if constexpr (ECHO_ACC_REGS) {  // plain loads issued now, consumed in D2 (latency behind A, D1)
+        if constexpr (TR) {  // plain loads (transposed pair), added when the next chunk stores
+          const int a = min(X0 + iT, lg.na - 1) + lg.coff;
+          const double* src = R + lbT + (long long)a * as;
+#pragma unroll
+          for (int q = 0; q < 7; q++) accT[q] = !accumulates<AX, DN>(q) ? 0.0 : src[out_slot<AX, DN>(q) * vs];
+        } else if constexpr (ECHO_ACC_REGS) {  // plain loads issued now, consumed in D2 (latency behind A, D1)
           const int a = min(X0 + i, lg.na - 1) + lg.coff;
           const double* src = R + lb + a * as;
 #pragma unroll
@@ -331,7 +400,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
         } else if (!(vec && (t & 1))) {
           const int a = min(X0 + i, lg.na - 1) + lg.coff;
           const double* src = R + lb + a * as;
-          const unsigned s = sbase + 8u * (GE::OFF_A + loff<AX, CH>(t, i));
+          const unsigned s = sbase + 8u * (GE::OFF_A + GE::aofs(t, i));
 #pragma unroll
           for (int q = 0; q < 7; q++) {
             if (!accumulates<AX, DN>(q) || (UCT && q >= 5)) continue;
@@ -356,7 +425,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
       } else {
         int pos[5];
 #pragma unroll
-        for (int m = 0; m < 5; m++) pos[m] = loff<AX, RING>(t, GE::wrap(rr - 2 + m));
+        for (int m = 0; m < 5; m++) pos[m] = GE::pofs(t, GE::wrap(rr - 2 + m));
         constexpr bool CHAR = REC == 6;  // A44: the hydro states per face from the characteristic fields
 #pragma unroll
         for (int v = 0; v < 8; v++) {
@@ -382,7 +451,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
           constexpr int cmp[3] = {1 + AX, 1 + (AX + 1) % 3, 1 + (AX + 2) % 3};
 #pragma unroll
           for (int m = 0; m < 6; m++) {
-            const int ps = loff<AX, RING>(t, GE::wrap(rr - 3 + m));
+            const int ps = GE::pofs(t, GE::wrap(rr - 3 + m));
             q6[m][0] = smem[GE::OFF_P + 0 * GE::VP + ps];
 #pragma unroll
             for (int d = 0; d < 3; d++) q6[m][1 + d] = smem[GE::OFF_P + cmp[d] * GE::VP + ps];
@@ -437,7 +506,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
         }
         int fpos[5];
 #pragma unroll
-        for (int m = 0; m < 5; m++) fpos[m] = loff<AX, RINGF>(t, wrapf<AX>(rbf - CH + i - 2 + m));
+        for (int m = 0; m < 5; m++) fpos[m] = GE::fofs(t, wrapf<AX, GE>(rbf - CH + i - 2 + m));
 #pragma unroll
         for (int q = 0; q < 7; q++) {
           const double* Fq = smem + GE::OFF_F + q * GE::VF;
@@ -463,9 +532,9 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
          // (the prologue's window already holds chunk 0's cells)
         if (c <= GE::C_FIRST || c >= lg.nchunks) {  // (the window holds the first two chunks)
         } else if (c + 1 < lg.nchunks) {
-          if (!(vec && (t & 1))) load_cells<AX>(g, lg, lb, t, B + CH + kG + i, vec, P, UB, sbase);
+          if (!(vec && (t & 1))) load_cells<AX, GE>(g, lg, lbT, tT, B + CH + kG + iT, vec, P, UB, sbase);
         } else if (next >= 0 && next < lg.nunits) {
-          load_window<AX>(g, lg, next, t, i, P, UB, sbase);
+          load_window<AX, GE>(g, lg, next, tT, iT, P, UB, sbase);
         }
         cp_async_commit();
       }
@@ -487,7 +556,20 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
 #pragma unroll
           for (int q = 0; q < 7; q++) Hm[q] = smem[GE::OFF_HE + par * 7 * GE::VE + q * GE::VE + eslot_in * GE::NL + t];
         }
-        if (X0 + i < lg.na && line_ok) {
+        if constexpr (TR) {  // the contributions to the shared buffer; the next chunk adds them (transposed)
+          if (X0 + i < lg.na && line_ok) {
+#pragma unroll
+            for (int q = 0; q < 7; q++) {
+              double d;
+              if (q < 5 || DN) d = Hm[q] - H[q];  // (times 1/Delta in store_contrib)
+              else {
+                const double hs = 0.25 * (H[q] + Hm[q]);
+                d = (q == 5) ? -hs : hs;
+              }
+              smem[GE::OFF_D + q * GE::VD + GE::dofs(t, i)] = d;
+            }
+          }
+        } else if (X0 + i < lg.na && line_ok) {
           double* dst = R + lb + (X0 + i + lg.coff) * as;
 #pragma unroll
           for (int q = 0; q < 7; q++) {
@@ -503,7 +585,7 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
               d = (q == 5) ? -hs : hs;
             }
             dst[out_slot<AX, DN>(q) * vs] =
-                accumulates<AX, DN>(q) ? ((ECHO_ACC_REGS ? acc[q] : smem[GE::OFF_A + q * GE::VA + loff<AX, CH>(t, i)]) + d) : d;
+                accumulates<AX, DN>(q) ? ((ECHO_ACC_REGS ? acc[q] : smem[GE::OFF_A + q * GE::VA + GE::aofs(t, i)]) + d) : d;
           }
         }
       }
@@ -559,11 +641,15 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
           } else {
             face_hll(FlatMet());
           }
-          const int fp = loff<AX, RINGF>(t, wrapf<AX>(rbf + 2 + i));
+          const int fp = GE::fofs(t, wrapf<AX, GE>(rbf + 2 + i));
 #pragma unroll
           for (int q = 0; q < 7; q++) smem[GE::OFF_F + q * GE::VF + fp] = F[q];
         }
       }
+    }
+    if constexpr (TR) {  // the last chunk's contributions (its D2 ran in the epilogue chunk)
+      __syncthreads();
+      store_contrib<AX, GE, DN>(g, lg, R, lbT, lineT_ok, tT, iT, (lg.nchunks - 1) * CH, accT, smem);
     }
   }
 }
@@ -579,27 +665,29 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
 #endif
 template <int AX, bool KS, int REC, int DM>
 constexpr int sweep_bps() {
-  return REC == 6 ? (Geo<AX>::BPS + 1) / 2
-                  : ((KS && AX == 0) ? ECHO_KSX_BPS : ((DM == 2 && AX == 0) ? ECHO_UCTX_BPS : Geo<AX>::BPS));
+  using GE = typename GeoSel<AX, DM>::type;
+  return REC == 6 ? (GE::BPS + 1) / 2
+                  : ((KS && AX == 0) ? ECHO_KSX_BPS : ((DM == 2 && AX == 0) ? ECHO_UCTX_BPS : GE::BPS));
 }
 
 template <int AX, bool KS, int DER, int REC, int DM>
-__global__ void __launch_bounds__(Geo<AX>::THREADS, (sweep_bps<AX, KS, REC, DM>()))
+__global__ void __launch_bounds__(GeoSel<AX, DM>::type::THREADS, (sweep_bps<AX, KS, REC, DM>()))
 k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
         const double* __restrict__ UB, double* R, const double* __restrict__ Bface, double* __restrict__ FSo) {
-  using GE = Geo<AX>;
+  using GE = typename GeoSel<AX, DM>::type;
   extern __shared__ double smem[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const int tid = threadIdx.x;
-  const int t = GE::LM ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));
-  const int i = GE::LM ? (tid & (GE::CH - 1)) : (tid >> GE::LOG_NL);
+  // the first window's loads: the thread's own (line, slot), or its transposed pair (TRANS)
+  const int t = (GE::LM && !GE::TRANS) ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));
+  const int i = (GE::LM && !GE::TRANS) ? (tid & (GE::CH - 1)) : (tid >> GE::LOG_NL);
   // programmatic dependent launch (ECHO_PDL): the next sweep's CTAs may start as this grid's
   // CTAs retire, and run their first chunks (which read only P and U) over its tail; a y/z
   // sweep waits for the previous sweep's grid before its first access to R
   if constexpr (ECHO_PDL && AX != 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   bool dep_waited = !(ECHO_PDL && AX != 0);
   long long unit = blockIdx.x;
-  if (unit < lg.nunits) load_window<AX>(g, lg, unit, t, i, P, UB, sbase);
+  if (unit < lg.nunits) load_window<AX, GE>(g, lg, unit, t, i, P, UB, sbase);
   cp_async_commit();
   for (; unit < lg.nunits; unit += gridDim.x)
     march_unit<AX, KS, DER, REC, DM>(g, e, mt, lg, unit, unit + gridDim.x, P, UB, R, Bface, FSo, smem, dep_waited);
@@ -607,9 +695,8 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
 }
 
 // line-group geometry of a sweep launch (the slab extension included)
-template <int AX>
+template <int AX, class GE = Geo<AX>>
 inline LineGeom make_line_geom(const GridP& g, const double* P, const double* R, const PlaneRange& zr = PlaneRange{}) {
-  using GE = Geo<AX>;
   LineGeom lg;
   lg.na = g.n[AX];
   lg.nt = g.n[AX == 0 ? 1 : 0];
