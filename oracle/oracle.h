@@ -27,7 +27,8 @@
  *   state prims P5 : rho, u~^1, u~^2, u~^3, p               (u~ = W v)
  *   conserved   U8 : sqrt(gamma) * (D, S_1, S_2, S_3, tau, B^1, B^2, B^3)
  * Parity status of every function: see DESIGN.md §4 (all pinned except the
- * blast-wave / torus dynamics beyond the invariants, "parity unpinned").
+ * blast-wave / torus dynamics beyond the invariants, "parity unpinned"; the
+ * shock capturing itself is pinned by 1-D exact relativistic Riemann solutions).
  */
 #ifndef ECHO_ORACLE_H
 #define ECHO_ORACLE_H
