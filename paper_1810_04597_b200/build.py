@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libecho_b200.so")
 SOURCES = ["march.cu", "fused.cu", "update.cu", "uct.cu", "api.cu", "metric_tables.cpp"]
-HEADERS = ["echo_dev.cuh", "echo_kernels.h", "metric_tables.h", "cell_physics.cuh", "march_impl.cuh"]
+HEADERS = ["echo_dev.cuh", "echo_kernels.h", "metric_tables.h", "cell_physics.cuh", "march_impl.cuh", "march_pair.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
@@ -29,9 +29,24 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _includes(path: str, seen: set) -> None:
+    """the csrc headers `path` includes, recursively (quoted includes only)"""
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith("#include \""):
+                h = line.split("\"")[1]
+                hp = os.path.join(CSRC, h)
+                if h in HEADERS and hp not in seen:
+                    seen.add(hp)
+                    _includes(hp, seen)
+
+
 def _compile(src: str, verbose: bool, build_dir: str = BUILD, defines: tuple = ()) -> str:
     obj = os.path.join(build_dir, os.path.basename(src) + ".o")
-    deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "echo.h")]
+    hdrs: set = set()
+    _includes(os.path.join(CSRC, src), hdrs)
+    deps = [os.path.join(CSRC, src)] + sorted(hdrs) + [os.path.join(ROOT, "include", "echo.h")]
     if not _stale(obj, deps):
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", os.path.join(CSRC, src), "-o", obj]

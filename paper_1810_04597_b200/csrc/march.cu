@@ -1,14 +1,43 @@
 // march.cu — launchers of the axis-sweep kernels K2x/K2y/K2z (march_impl.cuh).
-#include "march_impl.cuh"
+#include "march_pair.cuh"
 
 namespace echo {
 namespace march {
+
+// the x sweep with two cells per lane (march_pair.cuh); its own per-device grid cap
+template <bool KS, int DER, int REC, int DM>
+static cudaError_t launch_x2(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB,
+                             double* R, const double* Bface, double* FSo, cudaStream_t st, const PlaneRange& zr) {
+  auto kern = k_march_x2<KS, DER, REC, DM>;
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> grid_caps[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int grid_cap = dev < kMaxDev ? grid_caps[dev].load(std::memory_order_relaxed) : 0;
+  if (!grid_cap) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GeoX2::SMEM);
+    if (err != cudaSuccess) return err;
+    int sms, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GeoX2::THREADS, GeoX2::SMEM);
+    grid_cap = sms * (per > 0 ? per : 1);
+    if (dev < kMaxDev) grid_caps[dev].store(grid_cap, std::memory_order_relaxed);
+  }
+  const LineGeom lg = make_line_geom<0, GeoX2>(g, P, R, zr);
+  const unsigned blocks = (unsigned)(lg.nunits < grid_cap ? lg.nunits : grid_cap);
+  kern<<<blocks, GeoX2::THREADS, GeoX2::SMEM, st>>>(g, e, mt, lg, P, UB, R, Bface, FSo);
+  return cudaGetLastError();
+}
 
 template <int AX, bool KS, int DER, int REC, int DM>
 static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt, const double* P, const double* UB,
                               double* R, const double* Bface, double* FSo, cudaStream_t st,
                               const PlaneRange& zr) {
   using GE = typename GeoSel<AX, DM>::type;
+  if constexpr (AX == 0 && REC != 6 && ECHO_X_PAIR) {  // 16-byte pairs need 16-byte aligned fields
+    if ((((uintptr_t)P) | ((uintptr_t)UB) | ((uintptr_t)R)) % 16 == 0)
+      return launch_x2<KS, DER, REC, DM>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
+  }
   auto kern = k_march<AX, KS, DER, REC, DM>;
   // per device (the attribute and the occupancy are per-device properties); the cache is
   // written at most once per device, racing writers store the same value
