@@ -26,9 +26,10 @@
  *   user prims  P8 : rho, v^1, v^2, v^3, p, B^1, B^2, B^3   (v contravariant)
  *   state prims P5 : rho, u~^1, u~^2, u~^3, p               (u~ = W v)
  *   conserved   U8 : sqrt(gamma) * (D, S_1, S_2, S_3, tau, B^1, B^2, B^3)
- * Parity status of every function: see DESIGN.md §4 (all pinned except the
- * blast-wave / torus dynamics beyond the invariants, "parity unpinned"; the
- * shock capturing itself is pinned by 1-D exact relativistic Riemann solutions).
+ * Parity status of every function: see DESIGN.md §4 (every function pinned; the
+ * multi-dimensional blast / torus evolutions have no closed form and are covered
+ * by the pins of their parts, 1-D exact relativistic Riemann solutions and the
+ * torus-equilibrium convergence).
  */
 #ifndef ECHO_ORACLE_H
 #define ECHO_ORACLE_H
