@@ -68,3 +68,27 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
+
+
+def build_c_demo(lib_path, out_dir):
+    """examples/echo_c_demo.c against include/echo.h as plain C99 (-Wall -Wextra -Werror), linked
+    to the library: the boundary needs no CUDA header, C++ or Python"""
+    exe = os.path.join(out_dir, "echo_c_demo")
+    libdir = os.path.dirname(lib_path)
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "echo_c_demo.c"), "-L" + libdir, "-lecho_b200",
+           "-Wl,-rpath," + libdir, "-lm", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_demo_builds_and_reports_no_device(lib_path, tmp_path):
+    import torch
+
+    exe = build_c_demo(lib_path, str(tmp_path))
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    if torch.cuda.is_available():  # (the GPU run of the same program: tests/test_gpu_c_demo.py)
+        assert r.returncode == 0, r.stdout + r.stderr
+    else:  # echo_create -> ECHO_E_CUDA, named; the demo's "skipped" exit
+        assert r.returncode == 77, r.stdout + r.stderr
+        assert "no CUDA device" in r.stdout
