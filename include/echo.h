@@ -302,6 +302,21 @@ int echo_check_guards(echo_ctx* ctx);
 int echo_set_debug(echo_ctx* ctx, int flags);
 int echo_check_finite(echo_ctx* ctx);
 
+/* ---- checkpoint / restart (SURVEY.md §5 "Checkpoint/resume") ----
+ * A checkpoint is the raw device state that the next step reads, taken at a step boundary: U^n,
+ * the state primitives with their per-cell con2prim guess (and, in a curved metric, B) and, with
+ * divb = 2, the staggered field b^n: echo_checkpoint_doubles(ctx) doubles in an internal record
+ * layout that only echo_checkpoint_load of a context created with the same grid, metric and EOS
+ * reads.  Loading it and stepping continues bit for bit as if the run had not stopped (same
+ * states, same CFL dt), unlike a restart through echo_set_prims(echo_get_prims()), which
+ * re-derives U from rounded primitives.  Save: ECHO_E_ORDER without a state or inside a step
+ * (after echo_stage 1 or 2).  Slab contexts (ECHO_BC_HALO): echo_checkpoint_doubles = 0 and
+ * ECHO_E_ORDER (checkpoint the whole domain instead).  Host buffers synchronise, device buffers
+ * are stream-ordered.  The event counters are not part of the state. */
+long long echo_checkpoint_doubles(const echo_ctx* ctx);
+int echo_checkpoint_save(echo_ctx* ctx, double* buf, int on_device);
+int echo_checkpoint_load(echo_ctx* ctx, const double* buf, int on_device);
+
 /* Text of the last error of ctx ("" if none); NULL ctx gives the last echo_create error. */
 const char* echo_last_error(const echo_ctx* ctx);
 

@@ -693,6 +693,63 @@ int echo_get_face_field(echo_ctx* c, double* b3, int on_device) {
   return export_field(c, b3, bcur(c), 3, on_device, "echo_get_face_field");
 }
 
+// ---- checkpoint / restart (SURVEY §5 "Checkpoint/resume"): the raw device state the next step
+// reads — U^n, the P record (hydro primitives, the per-cell Newton guess / the curved-metric B)
+// and, with divb = 2, the staggered field record — owned planes only, record layout
+static int ckpt_arrays(echo_ctx* c, double* arr[3]) {
+  arr[0] = c->Un;
+  arr[1] = c->P;
+  arr[2] = is_uct(c) ? c->Bst : nullptr;
+  return is_uct(c) ? 3 : 2;
+}
+
+long long echo_checkpoint_doubles(const echo_ctx* c) {
+  if (!c || c->g.zhalo) return 0;
+  const long long per = (long long)c->plane * c->g.n[2];
+  return (c->g.divb == 2 ? 3 : 2) * per;
+}
+
+static int ckpt_copy(echo_ctx* c, double* buf, bool save, int on_device, const char* where) {
+  double* arr[3];
+  const int na = ckpt_arrays(c, arr);
+  const size_t per = c->plane * (size_t)c->g.n[2];
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice
+                                        : (save ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice);
+  for (int a = 0; a < na; a++) {
+    double* dev = arr[a];
+    double* usr = buf + a * per;
+    CK(cudaMemcpyAsync(save ? usr : dev, save ? dev : usr, sizeof(double) * per, kind, c->st), where);
+  }
+  if (!on_device) CK(cudaStreamSynchronize(c->st), where);
+  return ECHO_OK;
+}
+
+int echo_checkpoint_save(echo_ctx* c, double* buf, int on_device) {
+  if (!c || !buf) return c ? fail(c, ECHO_E_ARG, "echo_checkpoint_save: NULL buffer") : ECHO_E_ARG;
+  if (c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_checkpoint_save: not for slab contexts (halo boundaries)");
+  if (!c->have_state || (is_uct(c) && !c->have_faces))
+    return fail(c, ECHO_E_ORDER, "echo_checkpoint_save: no state (echo_set_prims / echo_set_face_field first)");
+  if (c->next_stage != 1 || c->swept)
+    return fail(c, ECHO_E_ORDER, "echo_checkpoint_save: inside a step (stage 1 or 2 done): finish it with echo_stage");
+  return ckpt_copy(c, buf, true, on_device, "echo_checkpoint_save");
+}
+
+int echo_checkpoint_load(echo_ctx* c, const double* buf, int on_device) {
+  if (!c || !buf) return c ? fail(c, ECHO_E_ARG, "echo_checkpoint_load: NULL buffer") : ECHO_E_ARG;
+  if (c->g.zhalo) return fail(c, ECHO_E_ORDER, "echo_checkpoint_load: not for slab contexts (halo boundaries)");
+  int rc = ckpt_copy(c, const_cast<double*>(buf), false, on_device, "echo_checkpoint_load");
+  if (rc) return rc;
+  c->have_state = true;
+  c->have_faces = is_uct(c);
+  c->cfl_valid = false;
+  c->next_stage = 1;
+  c->xahead = false;
+  c->swept = 0;
+  c->swept_int = 0;
+  c->inducted = 0;
+  return ECHO_OK;
+}
+
 int echo_set_cons(echo_ctx* c, const double* u8, int on_device) {
   if (!c || !u8) return c ? fail(c, ECHO_E_ARG, "echo_set_cons: NULL buffer") : ECHO_E_ARG;
   if (!c->have_state) return fail(c, ECHO_E_ORDER, "echo_set_cons: needs a prior echo_set_prims (con2prim guess)");

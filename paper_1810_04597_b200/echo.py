@@ -98,6 +98,9 @@ _sig = {
     "echo_set_debug": (C.c_int, [_P, C.c_int]),
     "echo_check_finite": (C.c_int, [_P]),
     "echo_check_guards": (C.c_int, [_P]),
+    "echo_checkpoint_doubles": (C.c_longlong, [_P]),
+    "echo_checkpoint_save": (C.c_int, [_P, _P, C.c_int]),
+    "echo_checkpoint_load": (C.c_int, [_P, _P, C.c_int]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -375,6 +378,20 @@ def halo_fill(ctx, side: int):
     return _check(ctx, _lib.echo_halo_fill(ctx, int(side)))
 
 
+def checkpoint_doubles(ctx) -> int:
+    return int(_lib.echo_checkpoint_doubles(ctx))
+
+
+def checkpoint_save(ctx, buf):
+    p, d = _buf(buf, True)
+    return _check(ctx, _lib.echo_checkpoint_save(ctx, p, d))
+
+
+def checkpoint_load(ctx, buf):
+    p, d = _buf(buf)
+    return _check(ctx, _lib.echo_checkpoint_load(ctx, p, d))
+
+
 # ------------------------------------------------------- convenience
 class Echo:
     """Owns one context; `problem` is an echo_inputs.Problem (or anything with grid_kwargs())."""
@@ -463,3 +480,13 @@ class Echo:
 
     def check_guards(self):
         return check_guards(self.ctx)
+
+    def checkpoint(self, out=None):
+        """the raw state at a step boundary (echo_checkpoint_save): a host array, or `out`"""
+        out = np.zeros(checkpoint_doubles(self.ctx)) if out is None else out
+        checkpoint_save(self.ctx, out)
+        return out
+
+    def restore(self, buf):
+        """continue bit for bit from a checkpoint of a context with the same configuration"""
+        return checkpoint_load(self.ctx, buf)
