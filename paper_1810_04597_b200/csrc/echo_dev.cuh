@@ -240,7 +240,8 @@ ECHO_D void speeds(const M& m, const EosP& e, const double* pr, const State& s, 
   const double DmN = Dn - N;
   const double den = fma(-s.v2, N, Dn);
   // 1 - v^2 = 1 / W^2 (exact in real arithmetic)
-  const double Q = (N * s.W2i) * fma(m.gi_diag(j), den, -vj * vj * DmN);
+  // (flat: den - v_j^2 (Dn - N) as one FMA)
+  const double Q = (N * s.W2i) * (M::kFlat ? fma(-vj * vj, DmN, den) : fma(m.gi_diag(j), den, -vj * vj * DmN));
   const double sq = fsqrt(Q);
   const double iden = M::kFlat ? frcp(den) : m.alpha() * frcp(den);
   const double c0 = M::kFlat ? vj * (DmN * iden) : fma(vj * DmN, iden, -m.beta(j));
@@ -279,7 +280,7 @@ ECHO_D void hll_face(const M& m, const EosP& e, const double* pl, const double* 
   const double den = sR - sL;
   if (den > 0.0) {
     const double inv = (M::kFlat ? scale : m.sqrtg() * scale) * frcp(den);
-    const double a = sR * inv, b = sL * inv, c = sL * sR * inv;
+    const double a = sR * inv, b = sL * inv, c = a * sL;
 #pragma unroll
     for (int q = 0; q < 7; q++) F[q] = fma(c, uR[q] - uL[q], fma(a, fL[q], -b * fR[q]));
   } else {
@@ -405,8 +406,17 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
     SR = fma(3.0, p12, fma(6.0, p02, p01));
   }
   // left: alpha_k ~ d_k / s_k ~ (p12, d1 p02, d2 p01); right (mirror): (p01, d1 p02, d2 p12)
-  const double NL = fma(p01, C2, fma(p02, C1, p12 * C0));
-  const double NR = fma(p12, E2, fma(p02, E1, p01 * E0));
+  double NL, NR;
+  if (REC == 0) {
+    // C1 = 1.25 (dm + 3 dp), E1 = -1.25 (dp + 3 dm): the common 1.25 rides on p02 (one multiply
+    // instead of two)
+    const double q02 = 1.25 * p02;
+    NL = fma(p01, C2, fma(q02, fma(3.0, dp, dm), p12 * C0));
+    NR = fma(p12, E2, fma(-q02, fma(3.0, dm, dp), p01 * E0));
+  } else {
+    NL = fma(p01, C2, fma(p02, C1, p12 * C0));
+    NR = fma(p12, E2, fma(p02, E1, p01 * E0));
+  }
   // both normalisations through one reciprocal: 1/(SL SR)
   const double inv = frcp(SL * SR);
   qL = fma(NL, SR * inv, u0);
