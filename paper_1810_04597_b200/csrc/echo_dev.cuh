@@ -417,10 +417,16 @@ ECHO_D void weno5_both(double um2, double um1, double u0, double up1, double up2
     NL = fma(p01, C2, fma(p02, C1, p12 * C0));
     NR = fma(p12, E2, fma(p02, E1, p01 * E0));
   }
+#ifdef ECHO_WENO_TWO_RCP
+  // two independent reciprocals (same FP64 count, one more MUFU, a dependency chain 2 shorter)
+  qL = fma(NL, frcp(SL), u0);
+  qR = fma(NR, frcp(SR), u0);
+#else
   // both normalisations through one reciprocal: 1/(SL SR)
   const double inv = frcp(SL * SR);
   qL = fma(NL, SR * inv, u0);
   qR = fma(NR, SL * inv, u0);
+#endif
 }
 
 // --------------------------------------------------------------- MP5 (A33)
