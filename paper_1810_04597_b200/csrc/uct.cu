@@ -141,6 +141,17 @@ k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restric
 // step instead of six from planes far apart); the in-plane samples (z-face data and b^z along
 // y or x) are loaded per step.  Same arithmetic as uct_emf_one.
 constexpr int kZSeg = 16;  // planes per thread
+#ifndef ECHO_ZSEG_IC
+#define ECHO_ZSEG_IC 16  // planes per thread of the induction and cell-update marches
+#endif
+constexpr int kZSegIC = ECHO_ZSEG_IC;
+#ifndef ECHO_INDUCT_BPS
+#define ECHO_INDUCT_BPS 8  // CTAs per SM the induction march is compiled for (64 registers; 1: no cap,
+                           // 108 registers: 220.4 vs 213.7 ms/step UCT at 512^3, profiles/r02_uct_ic_ab)
+#endif
+#ifndef ECHO_UCT_CELL_BPS
+#define ECHO_UCT_CELL_BPS 6  // CTAs per SM of the flat-metric cell-update march (80 registers)
+#endif
 #ifndef ECHO_EMF_ZM_BPS
 #define ECHO_EMF_ZM_BPS 3  // (168 registers, 52-104 B of spills; 2 CTAs/SM: variant "emf2" below)
 #endif
@@ -287,7 +298,7 @@ k_uct_induct(const GridP g, int mode, int s, double dt, const double* dtp, const
 // The same induction marching along z: one thread per (i, j) column and kZSeg planes keeps
 // the two along-z EMF streams (E^y for b^x, E^x for b^y) in 6-entry register windows.
 template <int DER>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, ECHO_INDUCT_BPS)
 k_uct_induct_zm(const GridP g, int mode, int s, double dt, const double* dtp, const double* __restrict__ Ed,
                 double* Bst, double* __restrict__ Lout) {
   if (dtp) {
@@ -297,8 +308,8 @@ k_uct_induct_zm(const GridP g, int mode, int s, double dt, const double* dtp, co
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= g.n[0]) return;
-  const int k0 = blockIdx.z * kZSeg;
-  const int k1 = min(k0 + kZSeg, g.n[2]);
+  const int k0 = blockIdx.z * kZSegIC;
+  const int k1 = min(k0 + kZSegIC, g.n[2]);
   const long long vs = g.vs;
   double wy[6], wx[6];  // E^y and E^x at (i, j, k-3 .. k+2)
   {
@@ -463,7 +474,7 @@ k_uct_cell(const GridP g, const EosP e, const MetTables mt, int s, double dt, co
 // the same marching along z (one thread per (i, j) column and kZSeg planes): the centring's
 // b^z samples along z come from a 6-entry register window
 template <bool KS>
-__global__ void __launch_bounds__(128, KS ? 4 : 6)  // KS: spill-free at 128 registers
+__global__ void __launch_bounds__(128, KS ? 4 : ECHO_UCT_CELL_BPS)  // KS: spill-free at 128 registers
 k_uct_cell_zm(const GridP g, const EosP e, const MetTables mt, int s, double dt, const double* dtp,
               const double* __restrict__ R, const double* Un, const double* Us, double* Uout, double* P,
               const double* __restrict__ Bst, unsigned long long* counters, unsigned long long* cfl_out) {
@@ -473,8 +484,8 @@ k_uct_cell_zm(const GridP g, const EosP e, const MetTables mt, int s, double dt,
   }
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
-  const int k0 = blockIdx.z * kZSeg;
-  const int k1 = min(k0 + kZSeg, g.n[2]);
+  const int k0 = blockIdx.z * kZSegIC;
+  const int k1 = min(k0 + kZSegIC, g.n[2]);
   const int slot = s == 3 ? 0 : 3;
   const long long vs = g.vs;
   int nfl = 0, nfa = 0;
@@ -574,7 +585,7 @@ cudaError_t launch_uct_emf(const GridP& g, const double* const FS[3], const doub
 cudaError_t launch_uct_induct(const GridP& g, int mode, int s, double dt, const double* dtp, const double* Ed,
                               double* Bst, double* Lout, cudaStream_t st) {
   if (ECHO_INDUCT_ZMARCH) {
-    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSeg - 1) / kZSeg));
+    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSegIC - 1) / kZSegIC));
     if (g.der == 4) k_uct_induct_zm<4><<<zb, 128, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
     else if (g.der == 2) k_uct_induct_zm<2><<<zb, 128, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
     else k_uct_induct_zm<6><<<zb, 128, 0, st>>>(g, mode, s, dt, dtp, Ed, Bst, Lout);
@@ -595,7 +606,7 @@ cudaError_t launch_uct_cell(bool ks, const GridP& g, const EosP& e, const MetTab
                             double* P, const double* Bst, unsigned long long* counters, unsigned long long* cfl_out,
                             cudaStream_t st) {
   if (ECHO_CELL_ZMARCH) {
-    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSeg - 1) / kZSeg));
+    const dim3 zb((unsigned)((g.n[0] + 127) / 128), (unsigned)g.n[1], (unsigned)((g.n[2] + kZSegIC - 1) / kZSegIC));
     if (ks)
       k_uct_cell_zm<true><<<zb, 128, 0, st>>>(g, e, mt, s, dt, dtp, R, Un, Us, Uout, P, Bst, counters, cfl_out);
     else
