@@ -117,8 +117,14 @@ ECHO_D double uct_emf_one(const GridP& g, const double* const FS[3], const doubl
 }
 
 // grid (cells / kCellThreads, 3): blockIdx.y = the EMF component
+// -DECHO_EMF_BPS=n: the E^z kernel compiled for n CTAs per SM (default: ptxas's own budget)
+#ifdef ECHO_EMF_BPS
+#define ECHO_EMF_BOUNDS __launch_bounds__(kCellThreads, ECHO_EMF_BPS)
+#else
+#define ECHO_EMF_BOUNDS __launch_bounds__(kCellThreads)
+#endif
 template <int REC>
-__global__ void __launch_bounds__(kCellThreads)
+__global__ void ECHO_EMF_BOUNDS
 k_uct_emf(const GridP g, const double* __restrict__ FSx, const double* __restrict__ FSy,
           const double* __restrict__ FSz, const double* __restrict__ Bin, double* __restrict__ Ed, int cc0) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -146,8 +152,13 @@ constexpr int kZSeg = 16;  // planes per thread
 #endif
 constexpr int kZSegIC = ECHO_ZSEG_IC;
 #ifndef ECHO_INDUCT_BPS
-#define ECHO_INDUCT_BPS 8  // CTAs per SM the induction march is compiled for (64 registers; 1: no cap,
-                           // 108 registers: 220.4 vs 213.7 ms/step UCT at 512^3, profiles/r02_uct_ic_ab)
+#define ECHO_INDUCT_BPS 8  // CTAs per SM the induction march is compiled for (64 registers;
+                           // 0: ptxas's own budget; profiles/r02_uct_ic_ab)
+#endif
+#if ECHO_INDUCT_BPS > 0
+#define ECHO_INDUCT_BOUNDS __launch_bounds__(128, ECHO_INDUCT_BPS)
+#else
+#define ECHO_INDUCT_BOUNDS __launch_bounds__(128)
 #endif
 #ifndef ECHO_UCT_CELL_BPS
 #define ECHO_UCT_CELL_BPS 6  // CTAs per SM of the flat-metric cell-update march (80 registers)
@@ -298,7 +309,7 @@ k_uct_induct(const GridP g, int mode, int s, double dt, const double* dtp, const
 // The same induction marching along z: one thread per (i, j) column and kZSeg planes keeps
 // the two along-z EMF streams (E^y for b^x, E^x for b^y) in 6-entry register windows.
 template <int DER>
-__global__ void __launch_bounds__(128, ECHO_INDUCT_BPS)
+__global__ void ECHO_INDUCT_BOUNDS
 k_uct_induct_zm(const GridP g, int mode, int s, double dt, const double* dtp, const double* __restrict__ Ed,
                 double* Bst, double* __restrict__ Lout) {
   if (dtp) {
