@@ -654,7 +654,8 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
   }
 }
 
-// CTAs per SM of a sweep: half for rec = 6 (its per-face eigen-projection needs ~2x the registers);
+// CTAs per SM of a sweep: about half for rec = 6 (its per-face eigen-projection needs ~2x the registers;
+// ECHO_REC6_X_BPS / ECHO_REC6_YZ_BPS);
 // the Kerr-Schild x sweep (face metric records) spilled 164 B at the x sweep's 80 registers: 4 CTAs (128)
 #ifndef ECHO_KSX_BPS
 #define ECHO_KSX_BPS 4
@@ -663,10 +664,16 @@ ECHO_D void march_unit(const GridP& g, const EosP& e, const MetTables& mt, const
 #ifndef ECHO_UCTX_BPS
 #define ECHO_UCTX_BPS 5
 #endif
+#ifndef ECHO_REC6_X_BPS
+#define ECHO_REC6_X_BPS 3
+#endif
+#ifndef ECHO_REC6_YZ_BPS
+#define ECHO_REC6_YZ_BPS 10  // 164 registers (6: 240): 120.2-120.3 vs 123.6-123.7 ms/step with rec 6 (profiles/r02_rec6_ab)
+#endif
 template <int AX, bool KS, int REC, int DM>
 constexpr int sweep_bps() {
   using GE = typename GeoSel<AX, DM>::type;
-  return REC == 6 ? (GE::BPS + 1) / 2
+  return REC == 6 ? (AX == 0 ? ECHO_REC6_X_BPS : ECHO_REC6_YZ_BPS)
                   : ((KS && AX == 0) ? ECHO_KSX_BPS : ((DM == 2 && AX == 0) ? ECHO_UCTX_BPS : GE::BPS));
 }
 
