@@ -39,6 +39,9 @@ static cudaError_t launch_one(const GridP& g, const EosP& e, const MetTables& mt
       return launch_x2<KS, DER, REC, DM>(g, e, mt, P, UB, R, Bface, FSo, st, zr);
   }
   auto kern = k_march<AX, KS, DER, REC, DM>;
+#ifdef ECHO_YZ_MAXNREG
+  if constexpr (AX != 0 && REC != 6 && !ECHO_PDL) kern = k_march_mr<AX, KS, DER, REC, DM>;
+#endif
   // per device (the attribute and the occupancy are per-device properties); the cache is
   // written at most once per device, racing writers store the same value
   constexpr int kMaxDev = 64;

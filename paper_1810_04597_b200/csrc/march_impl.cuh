@@ -701,6 +701,30 @@ k_march(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, cons
   cp_async_wait0();
 }
 
+// -DECHO_YZ_MAXNREG=n: the y/z sweeps compiled with a register cap of n (__maxnreg__, which cannot be
+// combined with __launch_bounds__) instead of the CTAs-per-SM bound, e.g. 152 registers = 13 one-warp
+// CTAs per SM, a budget between the 12 (168) and 14 (128) that launch bounds can express
+#ifdef ECHO_YZ_MAXNREG
+template <int AX, bool KS, int DER, int REC, int DM>
+__global__ void __maxnreg__(ECHO_YZ_MAXNREG)
+k_march_mr(const GridP g, const EosP e, const MetTables mt, const LineGeom lg, const double* __restrict__ P,
+           const double* __restrict__ UB, double* R, const double* __restrict__ Bface, double* __restrict__ FSo) {
+  using GE = typename GeoSel<AX, DM>::type;
+  extern __shared__ double smem[];
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const int tid = threadIdx.x;
+  const int t = (GE::LM && !GE::TRANS) ? (tid >> GE::LOG_CH) : (tid & (GE::NL - 1));
+  const int i = (GE::LM && !GE::TRANS) ? (tid & (GE::CH - 1)) : (tid >> GE::LOG_NL);
+  bool dep_waited = true;
+  long long unit = blockIdx.x;
+  if (unit < lg.nunits) load_window<AX, GE>(g, lg, unit, t, i, P, UB, sbase);
+  cp_async_commit();
+  for (; unit < lg.nunits; unit += gridDim.x)
+    march_unit<AX, KS, DER, REC, DM>(g, e, mt, lg, unit, unit + gridDim.x, P, UB, R, Bface, FSo, smem, dep_waited);
+  cp_async_wait0();
+}
+#endif
+
 // line-group geometry of a sweep launch (the slab extension included)
 template <int AX, class GE = Geo<AX>>
 inline LineGeom make_line_geom(const GridP& g, const double* P, const double* R, const PlaneRange& zr = PlaneRange{}) {
