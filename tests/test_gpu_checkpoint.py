@@ -106,3 +106,17 @@ def test_checkpoint_refused_inside_a_step(E):
     g.stage(2, dt)
     g.stage(3, dt)
     g.checkpoint()  # at the step boundary again
+
+
+def test_checkpoint_refused_on_slabs_and_without_state(E):
+    p = I.problem(0, n=(16, 12, 8))
+    g = E.Echo(p, bc=((0, 0), (0, 0), (E.BC_HALO, E.BC_HALO)))
+    assert E.checkpoint_doubles(g.ctx) == 0
+    with pytest.raises(E.EchoError) as ei:
+        E.checkpoint_save(g.ctx, np.zeros(16))
+    assert ei.value.code == E.E_ORDER and "slab" in str(ei.value)
+    g.close()
+    h = E.Echo(p)  # a state is needed before a save
+    with pytest.raises(E.EchoError) as ei:
+        h.checkpoint()
+    assert ei.value.code == E.E_ORDER
