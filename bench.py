@@ -597,6 +597,9 @@ def main(argv=None):
     ap.add_argument("--cpu-n1", type=int, default=128, help="single-thread oracle sample grid (0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args(argv)
+    if args.warmup < 3:  # timing rule: at least 3 untimed warm-up steps; the line reports the count run
+        print(f"bench.py: --warmup {args.warmup} raised to 3 (at least 3 warm-up steps)", file=sys.stderr)
+        args.warmup = 3
     world, rank, local = dist_setup()
     if args.impl == "reference":
         return run_reference(args, world, rank)
