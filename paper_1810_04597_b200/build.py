@@ -5,6 +5,7 @@
 from __future__ import annotations
 
 import concurrent.futures as cf
+import fcntl
 import os
 import subprocess
 import sys
@@ -66,20 +67,33 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
     libecho_b200_<variant>.so with extra -D `defines` in its own object dir."""
     build_dir = BUILD if not variant else BUILD + "_" + variant
     lib = LIB if not variant else LIB.replace(".so", f"_{variant}.so")
+    # The object dir is not shipped to the GPU boxes (.gpurunignore): a library newer than
+    # every source and header is current without its objects, so no rank recompiles it.
+    if not force and not variant and not _stale(lib, _all_deps()):
+        return lib
     os.makedirs(build_dir, exist_ok=True)
-    if force:
-        for f in os.listdir(build_dir):
-            os.remove(os.path.join(build_dir, f))
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose, build_dir, tuple(defines)), SOURCES))
-    if _stale(lib, objs):
-        tmp = lib + f".tmp{os.getpid()}"
-        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-        os.replace(tmp, lib)
+    # one builder at a time: torchrun starts N ranks that all call build() (bench.py)
+    with open(os.path.join(build_dir, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if force:
+            for f in os.listdir(build_dir):
+                if f != ".lock":
+                    os.remove(os.path.join(build_dir, f))
+        with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            objs = list(ex.map(lambda s: _compile(s, verbose, build_dir, tuple(defines)), SOURCES))
+        if _stale(lib, objs):
+            tmp = lib + f".tmp{os.getpid()}"
+            cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+            os.replace(tmp, lib)
     return lib
+
+
+def _all_deps() -> list[str]:
+    return ([os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, h) for h in HEADERS]
+            + [os.path.join(ROOT, "include", "echo.h")])
 
 
 if __name__ == "__main__":
