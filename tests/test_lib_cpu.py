@@ -92,3 +92,17 @@ def test_c_demo_builds_and_reports_no_device(lib_path, tmp_path):
     else:  # echo_create -> ECHO_E_CUDA, named; the demo's "skipped" exit
         assert r.returncode == 77, r.stdout + r.stderr
         assert "no CUDA device" in r.stdout
+
+
+def test_current_library_needs_no_objects(lib_path, tmp_path, monkeypatch):
+    """A library newer than every source is current without its object dir (which does not travel
+    to the GPU boxes, .gpurunignore): build() must not recompile it on every box and rank."""
+    import time
+
+    from paper_1810_04597_b200 import build
+
+    monkeypatch.setattr(build, "BUILD", str(tmp_path / "no_objects"))
+    t = time.time()
+    assert build.build() == lib_path
+    assert time.time() - t < 5.0
+    assert not (tmp_path / "no_objects").exists()
