@@ -12,9 +12,10 @@ checked against the oracle's at every step.
   config 4 (256 x 128 x 256 Kerr-Schild torus, floors firing in the atmosphere): 10 steps.
 * UCT (divb = 2) on configs 1 and 4: 10 steps, the staggered field included (config 4 with
   ECHO_FULL_UCT4=1, to keep the suite's oracle time well inside the driver's budget).
-* config 3 (512^3): 5 steps.  The oracle needs ~45 GB of host RAM and ~10 min of host
-  CPU for it, so it runs only with ECHO_FULL_CFG3=1 (the committed log of that run is
-  profiles/r02_fullsize_parity.txt).
+* config 3 (512^3): 5 steps, ECHO_FULL_CFG3_STEPS=10 for north_star's 10.  The
+  oracle needs ~45 GB of host RAM and ~15 min of host CPU per 5 steps, so it runs only with
+  ECHO_FULL_CFG3=1 (the committed logs: profiles/r02_fullsize_parity.txt, 5 steps, and
+  profiles/r02_fullsize_cfg3_10.txt, 10 steps).
 """
 import os
 import time
@@ -94,7 +95,7 @@ def test_full_size_10_step_parity(E, orc, cfg):
 @pytest.mark.skipif(os.environ.get("ECHO_FULL_CFG3") != "1",
                     reason="512^3 oracle: ~45 GB host RAM, ~10 min; set ECHO_FULL_CFG3=1 (log in profiles/)")
 def test_full_size_cfg3_5_step_parity(E, orc):
-    _run(E, orc, 3, 5)
+    _run(E, orc, 3, int(os.environ.get("ECHO_FULL_CFG3_STEPS", "5")))
 
 
 @pytest.mark.parametrize("cfg", [1, pytest.param(4, marks=pytest.mark.skipif(
