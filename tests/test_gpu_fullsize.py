@@ -10,8 +10,9 @@ checked against the oracle's at every step.
 
 * config 1 (128^3 CP Alfven wave), config 2 (256^3 blast, A31 active at the shock),
   config 4 (256 x 128 x 256 Kerr-Schild torus, floors firing in the atmosphere): 10 steps.
-* UCT (divb = 2) on configs 1 and 4: 10 steps, the staggered field included (config 4 with
-  ECHO_FULL_UCT4=1, to keep the suite's oracle time well inside the driver's budget).
+* UCT (divb = 2) on configs 1, 4 and 2: 10 steps, the staggered field included (config 4 with
+  ECHO_FULL_UCT4=1, config 2 with ECHO_FULL_UCT2=1, to keep the suite's oracle time well inside
+  the driver's budget).
 * config 3 (512^3): 5 steps, ECHO_FULL_CFG3_STEPS=10 for north_star's 10.  The
   oracle needs ~45 GB of host RAM and ~15 min of host CPU per 5 steps, so it runs only with
   ECHO_FULL_CFG3=1 (the committed logs: profiles/r02_fullsize_parity.txt, 5 steps, and
@@ -99,7 +100,9 @@ def test_full_size_cfg3_5_step_parity(E, orc):
 
 
 @pytest.mark.parametrize("cfg", [1, pytest.param(4, marks=pytest.mark.skipif(
-    os.environ.get("ECHO_FULL_UCT4") != "1", reason="~2.5 min of host oracle: ECHO_FULL_UCT4=1 (log in profiles/)"))])
+    os.environ.get("ECHO_FULL_UCT4") != "1", reason="~2.5 min of host oracle: ECHO_FULL_UCT4=1 (log in profiles/)")),
+    pytest.param(2, marks=pytest.mark.skipif(
+        os.environ.get("ECHO_FULL_UCT2") != "1", reason="256^3 UCT oracle: ECHO_FULL_UCT2=1 (log in profiles/)"))])
 def test_full_size_10_step_parity_uct(E, orc, cfg):
     """UCT (divb = 2, readings A37-A43) at the same full sizes: configs 1 (128^3) and 4
     (256 x 128 x 256, Kerr-Schild), 10 steps, every cell, the staggered field included.  Config 4
